@@ -1,0 +1,261 @@
+/* sc_oracle.c — plain, slow, obviously-correct CPU oracle for the
+ * software-context hot path (ChameleonAPI drafts bundled in arXiv 2310.07240's
+ * source).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Nothing on the product path may link, import or
+ * execute this file: only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference leg use it.  It shares no code, header,
+ * table or constant with paper_2310_07240_b200/ (the CUDA path).
+ *
+ * Every function follows the paper's text in its order and notation, in
+ * double precision (the paper fixes no precision).  Citations are
+ * PAPER.md:<line> (Section / Equation) under /root/reference; the readings
+ * A1..A19 taken where the paper is silent are listed in DESIGN.md §3.
+ *
+ * Pins (tests/test_oracle_*.py): the paper's worked example,
+ * the non-critical-error example, the paper's Python listing
+ * executed verbatim, brute force over every label subset for
+ * C <= 12 against the argmax characterisation, step-function limit of the loss
+ * vs the incorrect-decision indicator, central finite
+ * differences for the gradient, the True-False special case of the weights
+ * and an O(M^2) literal recount of N_i.
+ * "Parity unpinned": the absolute loss scale depends on k, theta and the batch
+ * reduction, which the paper leaves open (readings A3, A11, A14).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+typedef struct {
+  int32_t C;                  /* number of API labels                                */
+  int32_t n_apps;             /* number of applications (software contexts)          */
+  const int32_t* n_lists;     /* [n_apps] number of target classes W_1..W_m per app  */
+  const int64_t* list_off;    /* per app n_lists[a]+1 offsets, concatenated          */
+  const int32_t* list_labels; /* label ids of every list, in code order              */
+  double tau;                 /* label c is in the API output iff z_c > tau          */
+  double k;                   /* steepness of S(x) = 1/(1+e^{-kx})                   */
+} orc_ctx;
+
+/* ---------------------------------------------------------------- context */
+
+static int64_t app_base(const orc_ctx* x, int32_t app) {
+  int64_t b = 0;
+  for (int32_t a = 0; a < app; ++a) b += x->n_lists[a] + 1;
+  return b;
+}
+
+/* The listing's "if obj.name in Recycle: ... if obj.name in Compost: ..."
+ * (PAPER.md:128-134): the first list, in code order, that contains label c;
+ * -1 if none.  Reading A5: a label in several lists belongs to the first. */
+int32_t orc_first_list(const orc_ctx* x, int32_t app, int32_t c) {
+  const int64_t b = app_base(x, app);
+  for (int32_t j = 0; j < x->n_lists[app]; ++j)
+    for (int64_t t = x->list_off[b + j]; t < x->list_off[b + j + 1]; ++t)
+      if (x->list_labels[t] == c) return j;
+  return -1;
+}
+
+/* a1: per-label result of that scan for every label (done once per app). */
+void orc_compile(const orc_ctx* x, int32_t app, int8_t* cat) {
+  for (int32_t c = 0; c < x->C; ++c) cat[c] = (int8_t)orc_first_list(x, app, c);
+}
+
+/* ---------------------------------------------------------------- decision */
+
+static _Thread_local const double* t_sort_z; /* qsort has no context argument */
+static int cmp_confidence(const void* pa, const void* pb) {
+  const int32_t a = *(const int32_t*)pa, b = *(const int32_t*)pb;
+  const double za = t_sort_z[a], zb = t_sort_z[b];
+  if (za > zb) return -1;          /* descending confidence */
+  if (za < zb) return 1;
+  return (a < b) ? -1 : (a > b);   /* reading A4: equal confidence -> smaller label id first */
+}
+
+/* Decision(API(x)) for one input, simulated literally:
+ * API output = labels with z_c > tau (reading A3), ranked by
+ * descending confidence; the app walks them and returns the
+ * branch of the first label found in a list.  Falling off
+ * the loop is the default decision D' = n_lists (reading A6). */
+int32_t orc_decide(const orc_ctx* x, int32_t app, const int8_t* cat, const double* z, int32_t* scratch) {
+  int32_t n = 0;
+  for (int32_t c = 0; c < x->C; ++c)
+    if (z[c] > x->tau) scratch[n++] = c;
+  t_sort_z = z;
+  qsort(scratch, (size_t)n, sizeof(int32_t), cmp_confidence);
+  for (int32_t t = 0; t < n; ++t)
+    if (cat[scratch[t]] >= 0) return cat[scratch[t]];
+  return x->n_lists[app];
+}
+
+/* G_i: the target classes the ground truth intersects, {j : W_j ∩ ŷ_i ≠ ∅}
+ * (PAPER.md:2028 for 𝒲_i, :2038 for y_i), as a bit set over j. */
+uint32_t orc_gt_set(const int8_t* cat, const int32_t* labels, int64_t n) {
+  uint32_t G = 0;
+  for (int64_t t = 0; t < n; ++t)
+    if (cat[labels[t]] >= 0) G |= 1u << cat[labels[t]];
+  return G;
+}
+
+/* Eq. goal counts Decision(API(x_i)) ≠ Decision(ŷ_i).
+ * Reading A7: with the ground truth as API output the app reaches any j in G_i
+ * (depending on order), and the default iff G_i = ∅. */
+int32_t orc_correct(uint32_t G, int32_t d, int32_t n_lists) {
+  if (G == 0) return d == n_lists;
+  return d < n_lists && ((G >> d) & 1u);
+}
+
+/* ---------------------------------------------------------------- loss */
+
+static double sigma(double z) {               /* p_c = σ(z_c), reading A2 */
+  if (z >= 0) return 1.0 / (1.0 + exp(-z));
+  const double e = exp(z);
+  return e / (1.0 + e);
+}
+static double S(double k, double x) { return sigma(k * x); }
+static double dS(double k, double x) { return k * sigma(k * x) * sigma(-k * x); }
+static double dsigma(double z) { return sigma(z) * sigma(-z); }
+
+/* Multi-Choice API-output-order loss, Eq. api_output:
+ *   L = (M/N_i) ( y_i S(max(P⁻, θ) − P⁺) + (1 − y_i) S(P⁻ − θ) )
+ * P⁺ = max_{c ∈ 𝒲_i} p_c, P⁻ = max_{c ∈ 𝕎∖𝒲_i} p_c, θ = σ(τ) (reading A3),
+ * max over ∅ = −∞ (A9).  w = M/N_i is passed in.  σ is increasing, so
+ * max_c σ(z_c) = σ(max_c z_c): the arg max is taken over z (smallest id on
+ * ties, A8) and σ applied after, which keeps the arg max exact where σ
+ * saturates in floating point.  Gradient: chain rule with the whole
+ * subgradient on the arg max (A10); P⁻ receives gradient through max(P⁻, θ)
+ * only when P⁻ > θ, i.e. z⁻ > τ.
+ * Outputs: ell (unweighted), L = w·ell, and up to two gradient entries. */
+void orc_loss_row(const orc_ctx* x, const int8_t* cat, const double* z, uint32_t G, double w,
+                  double* ell_out, double* L_out,
+                  int32_t* c_plus, double* g_plus, int32_t* c_minus, double* g_minus) {
+  const double theta = sigma(x->tau);
+  const int y = G != 0;
+  int32_t cp = -1, cm = -1;
+  for (int32_t c = 0; c < x->C; ++c) {
+    if (cat[c] < 0) continue;                                       /* c ∉ 𝕎 */
+    if ((G >> cat[c]) & 1u) { if (cp < 0 || z[c] > z[cp]) cp = c; } /* c ∈ 𝒲_i      */
+    else                     { if (cm < 0 || z[c] > z[cm]) cm = c; } /* c ∈ 𝕎 ∖ 𝒲_i */
+  }
+  const double Pp = cp >= 0 ? sigma(z[cp]) : -INFINITY;
+  const double Pm = cm >= 0 ? sigma(z[cm]) : -INFINITY;
+  const int m_over = cm >= 0 && z[cm] > x->tau;                     /* P⁻ > θ */
+  double ell = 0.0, gp = 0.0, gm = 0.0;
+  int32_t op = -1, om = -1;
+  if (y) {
+    const double a = m_over ? Pm : theta;                           /* max(P⁻, θ) */
+    ell = S(x->k, a - Pp);
+    const double d = dS(x->k, a - Pp);
+    gp = -w * d * dsigma(z[cp]); op = cp;
+    if (m_over) { gm = w * d * dsigma(z[cm]); om = cm; }
+  } else if (cm >= 0) {
+    ell = S(x->k, Pm - theta);
+    gm = w * dS(x->k, Pm - theta) * dsigma(z[cm]); om = cm;
+  }
+  *ell_out = ell;
+  *L_out = w * ell;
+  *c_plus = op; *g_plus = gp; *c_minus = om; *g_minus = gm;
+}
+
+/* ---------------------------------------------------------------- weights */
+
+/* N_i and M/N_i by the literal definitions: for a
+ * target input N_i = Σ_j 1[ŷ_j ∩ 𝒲_i ≠ ∅]; for a non-target input N_i =
+ * Σ_j 1[ŷ_j ∩ 𝕎 = ∅] (reading A12: ŷ_j).  O(M²) — small M only.
+ * Rows are one app's inputs; cat is that app's compiled map. */
+void orc_weights_literal(const int8_t* cat, int64_t M, const int64_t* gt_off, const int32_t* gt_lab,
+                         double* w_row) {
+  for (int64_t i = 0; i < M; ++i) {
+    const uint32_t Gi = orc_gt_set(cat, gt_lab + gt_off[i], gt_off[i + 1] - gt_off[i]);
+    int64_t N = 0;
+    for (int64_t j = 0; j < M; ++j) {
+      int hit = 0, any_mapped = 0;
+      for (int64_t t = gt_off[j]; t < gt_off[j + 1]; ++t) {
+        const int8_t cj = cat[gt_lab[t]];
+        if (cj >= 0) { any_mapped = 1; if ((Gi >> cj) & 1u) hit = 1; }
+      }
+      N += Gi ? hit : !any_mapped;
+    }
+    w_row[i] = (double)M / (double)N;   /* N >= 1: row i counts itself */
+  }
+}
+
+/* The same definition evaluated once per distinct G (rows with equal G_i have
+ * equal N_i): H[m] = #{j : G_j = m};  N(m) = Σ_{m'} H[m']·1[m' ∩ m ≠ ∅] for
+ * m ≠ ∅, N(∅) = H[∅].  w[m] = M/N(m), and 0 for masks no input has (A13). */
+void orc_weights_by_mask(int32_t n_apps, const uint64_t* H, double* w) {
+  for (int32_t a = 0; a < n_apps; ++a) {
+    const uint64_t* h = H + (int64_t)a * 256;
+    uint64_t M = 0;
+    for (int m = 0; m < 256; ++m) M += h[m];
+    for (int m = 0; m < 256; ++m) {
+      uint64_t N = 0;
+      if (m == 0) N = h[0];
+      else for (int q = 0; q < 256; ++q) if (q & m) N += h[q];
+      w[(int64_t)a * 256 + m] = N ? (double)M / (double)N : 0.0;
+    }
+  }
+}
+
+/* ---------------------------------------------------------------- batch */
+
+static double load_z(const void* logits, int32_t dtype, int64_t idx) {
+  if (dtype == 0) return (double)((const float*)logits)[idx];
+  uint32_t u = (uint32_t)((const uint16_t*)logits)[idx] << 16;   /* bf16 -> f32 bits */
+  float f; memcpy(&f, &u, 4);
+  return (double)f;
+}
+
+/* Every output of the hot path for `rows` inputs.  Any output may be NULL.
+ * Counters ACCUMULATE (+=).  w: [n_apps*256] per-mask weights, NULL = 1.
+ * grad_idx/grad_val: [rows*2], slot 0 = c⁺, slot 1 = c⁻, −1/0 when absent;
+ * values multiplied by grad_scale.  Returns 0, or -1 on a non-finite logit
+ * (reading A18) or an out-of-range id. */
+int orc_eval(const orc_ctx* x, int64_t rows, int64_t ld, int32_t dtype, const void* logits,
+             const int64_t* gt_off, const int32_t* gt_lab, const uint16_t* app,
+             const double* w, double grad_scale,
+             uint8_t* decision, uint8_t* gt_mask, uint8_t* correct,
+             uint64_t* n_incorrect, uint64_t* hist_pred, uint64_t* hist_gt,
+             double* loss_sum, double* loss_row, int32_t* grad_idx, double* grad_val) {
+  const int32_t C = x->C;
+  int8_t* cat = (int8_t*)malloc((size_t)x->n_apps * (size_t)(C > 0 ? C : 1));
+  double* z = (double*)malloc(sizeof(double) * (size_t)(C > 0 ? C : 1));
+  int32_t* scratch = (int32_t*)malloc(sizeof(int32_t) * (size_t)(C > 0 ? C : 1));
+  int rc = 0;
+  for (int32_t a = 0; a < x->n_apps; ++a) orc_compile(x, a, cat + (int64_t)a * C);
+  for (int64_t i = 0; i < rows && rc == 0; ++i) {
+    const int32_t a = app ? (int32_t)app[i] : 0;
+    if (a >= x->n_apps) { rc = -1; break; }
+    const int8_t* ca = cat + (int64_t)a * C;
+    for (int32_t c = 0; c < C; ++c) {
+      z[c] = load_z(logits, dtype, i * ld + c);
+      if (!isfinite(z[c])) rc = -1;
+    }
+    if (rc) break;
+    const int32_t D = x->n_lists[a];
+    const int32_t d = orc_decide(x, a, ca, z, scratch);
+    if (decision) decision[i] = (uint8_t)d;
+    if (hist_pred) hist_pred[(int64_t)a * 16 + d] += 1;
+    if (!gt_off) continue;
+    for (int64_t t = gt_off[i]; t < gt_off[i + 1]; ++t)
+      if (gt_lab[t] < 0 || gt_lab[t] >= C) rc = -1;
+    if (rc) break;
+    const uint32_t G = orc_gt_set(ca, gt_lab + gt_off[i], gt_off[i + 1] - gt_off[i]);
+    const int32_t ok = orc_correct(G, d, D);
+    if (gt_mask) gt_mask[i] = (uint8_t)G;
+    if (correct) correct[i] = (uint8_t)ok;
+    if (n_incorrect) n_incorrect[a] += (uint64_t)!ok;
+    if (hist_gt) hist_gt[(int64_t)a * 256 + G] += 1;
+    if (loss_sum || loss_row || grad_idx || grad_val) {
+      const double wi = w ? w[(int64_t)a * 256 + G] : 1.0;
+      double ell, L, gp, gm; int32_t cp, cm;
+      orc_loss_row(x, ca, z, G, wi, &ell, &L, &cp, &gp, &cm, &gm);
+      if (loss_sum) loss_sum[a] += L;
+      if (loss_row) loss_row[i] = L;
+      if (grad_idx) { grad_idx[2 * i] = cp; grad_idx[2 * i + 1] = cm; }
+      if (grad_val) { grad_val[2 * i] = gp * grad_scale; grad_val[2 * i + 1] = gm * grad_scale; }
+    }
+  }
+  free(cat); free(z); free(scratch);
+  return rc;
+}

@@ -1,0 +1,57 @@
+"""Mutation check of the oracle's pins (run by hand: python tests/mutate_oracle.py).
+
+Each mutation is a plausible slip in sc_oracle.c (dropped term, wrong sign,
+wrong index, flipped comparison).  The CPU pin suite must fail for every one.
+"""
+import os
+import subprocess
+import sys
+import tempfile
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SRC = open(os.path.join(ROOT, "oracle", "sc_oracle.c")).read()
+
+MUTATIONS = [
+    ("threshold >= instead of >", "if (z[c] > x->tau) scratch[n++] = c;", "if (z[c] >= x->tau) scratch[n++] = c;"),
+    ("ascending confidence", "if (za > zb) return -1;", "if (za < zb) return -1;"),
+    ("ties to larger id", "return (a < b) ? -1 : (a > b);", "return (a > b) ? -1 : (a < b);"),
+    ("last list wins", "if (x->list_labels[t] == c) return j;", "if (x->list_labels[t] == c && j == x->n_lists[app]-1) return j;"),
+    ("G ignores mapping", "if (cat[labels[t]] >= 0) G |= 1u << cat[labels[t]];", "G |= 1u;"),
+    ("correct ignores G", "return d < n_lists && ((G >> d) & 1u);", "return d < n_lists;"),
+    ("drop max(P-,theta)", "const double a = m_over ? Pm : theta;", "const double a = Pm;"),
+    ("swap P+ P-", "ell = S(x->k, a - Pp);", "ell = S(x->k, Pp - a);"),
+    ("y=0 term uses P+", "ell = S(x->k, Pm - theta);", "ell = S(x->k, theta - Pm);"),
+    ("gradient sign", "gp = -w * d * dsigma(z[cp]); op = cp;", "gp = w * d * dsigma(z[cp]); op = cp;"),
+    ("dS missing k", "return k * sigma(k * x) * sigma(-k * x);", "return sigma(k * x) * sigma(-k * x);"),
+    ("P- over all W", "else                     { if (cm < 0 || z[c] > z[cm]) cm = c; }", "{ if (cm < 0 || z[c] > z[cm]) cm = c; }"),
+    ("N counts G subset not intersect", "else for (int q = 0; q < 256; ++q) if (q & m) N += h[q];", "else for (int q = 0; q < 256; ++q) if ((q & m) == q) N += h[q];"),
+    ("literal N non-target wrong", "N += Gi ? hit : !any_mapped;", "N += Gi ? hit : 1;"),
+    ("weight inverted", "w_row[i] = (double)M / (double)N;", "w_row[i] = (double)N / (double)M;"),
+]
+
+
+def main():
+    failures = []
+    with tempfile.TemporaryDirectory() as td:
+        for name, old, new in MUTATIONS:
+            assert SRC.count(old) == 1, name
+            src = os.path.join(td, "m.c")
+            so = os.path.join(td, f"m{len(failures)}_{abs(hash(name))}.so")
+            open(src, "w").write(SRC.replace(old, new))
+            subprocess.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-o", so, src, "-lm"])
+            env = dict(os.environ, ORACLE_SO=so)
+            r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-m", "not gpu", "-p", "no:cacheprovider",
+                                "tests/test_oracle_paper.py", "tests/test_oracle_bruteforce.py",
+                                "tests/test_oracle_loss.py", "tests/test_oracle_weights.py"],
+                               cwd=ROOT, env=env, capture_output=True, text=True)
+            killed = r.returncode != 0
+            print(f"{'KILLED ' if killed else 'SURVIVED'}  {name}")
+            if not killed:
+                failures.append(name)
+    if failures:
+        print("surviving mutations:", failures)
+        sys.exit(1)
+
+
+if __name__ == "__main__":
+    main()
