@@ -1,0 +1,179 @@
+/* sc.h — C ABI of libsc, the B200 (sm_100a) software-context evaluator.
+ *
+ * What it computes (ChameleonAPI drafts bundled in arXiv 2310.07240; PAPER.md
+ * under /root/reference, see SURVEY.md §0 and DESIGN.md):
+ *   an application turns a multi-label API output into a decision,
+ *   z = Decision(API(x)), by walking the output labels in
+ *   descending confidence and returning the branch of the first
+ *   label found in one of its lists, checked in code order (the Heapsortcypher
+ *   listing).  For a batch of B inputs with logits [B, C] and
+ *   ground-truth label sets ŷ_i, libsc produces in one read of the logits:
+ *     - the decision of every input,
+ *     - the incorrect-decision count of Eq. goal,
+ *     - the histogram of ground-truth category masks G_i used for the
+ *       rebalancing weights M/N_i and the histogram of
+ *       predicted decisions,
+ *     - the forward and backward of the Multi-Choice API-output-order loss,
+ *       Eq. api_output, weighted by M/N_i.
+ *
+ * Notation.  D' = number of lists of an application (0..8); decision ids
+ * 0..D'-1 are the lists in code order and D' is the default (no label matched,
+ * reading A6).  cat[c] = first list containing label c (reading A5).  G_i =
+ * bit set of the lists the ground truth of input i intersects;
+ * y_i = [G_i != 0].  tau = threshold on logits: label c is an
+ * API output iff z_c > tau (reading A3); theta = sigma(tau).
+ *
+ * Conventions for every call below.
+ *   - Device pointers are caller-owned and must stay valid until the work
+ *     enqueued on `stream` completes.  Calls are stream-ordered and
+ *     asynchronous; hot calls never allocate and never synchronise.
+ *   - Every uint64_t / double output ACCUMULATES (+=): zero it once, then the
+ *     batch may be split into chunks, shards or resumed passes.  Per-row
+ *     outputs are overwritten.  Any output pointer may be NULL (= not wanted).
+ *   - Host-side validation failures return SC_ERR_INVALID_ARG before anything
+ *     is enqueued; CUDA launch failures return SC_ERR_CUDA.  sc_last_error()
+ *     gives a thread-local message for the last non-OK status.  No call aborts
+ *     or exits; no C++ exception crosses the ABI.
+ *   - Device-side preconditions (finite logits, GT ids in [0,C), app ids <
+ *     n_apps) are not checked on the device: violating them gives unspecified
+ *     (but memory-safe within the documented buffers) results.
+ */
+#ifndef SC_H
+#define SC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SC_OK = 0,
+  SC_ERR_INVALID_ARG = 1,
+  SC_ERR_OOM = 2,
+  SC_ERR_CUDA = 3,
+  SC_ERR_UNSUPPORTED = 4
+} sc_status;
+
+typedef enum { SC_F32 = 0, SC_BF16 = 1 } sc_dtype;
+
+typedef enum {
+  SC_ORDER_API_OUTPUT = 0, /* Multi-Choice, API-output order — implemented   */
+  SC_ORDER_APP_CHOICE = 1  /* Multi-Choice, application-choice order — NEXT */
+} sc_order;
+
+/* cudaStream_t without pulling in CUDA headers: pass a cudaStream_t (or 0). */
+typedef void* sc_stream;
+
+typedef struct sc_context_s* sc_context; /* library-owned; immutable after load */
+
+/* sc_context_load — upload the applications' extracted software contexts
+ * ("summary of the software decision process": target classes, decision type,
+ * examination order) once, before any batch.
+ *   C            number of API labels, 1 <= C < 2^23.
+ *   n_apps       number of applications, 1..65535; batch rows pick one via sc_batch.app.
+ *   n_lists      host [n_apps]: D'_a, the number of lists of app a, 0..8.
+ *   list_off     host: for each app, n_lists[a]+1 offsets into list_labels,
+ *                concatenated app after app (list j of app a is
+ *                list_labels[list_off[b+j] .. list_off[b+j+1]), b = sum_{a'<a}(n_lists[a']+1)).
+ *   list_labels  host: label ids in [0, C), lists in code order.  A label may
+ *                appear in several lists; it belongs to the first (reading A5).
+ *   tau          logit threshold (finite); theta = sigma(tau) is computed in double.
+ *   k            steepness of S(x) = 1/(1+e^{-kx}), finite, > 0.
+ *   order        SC_ORDER_API_OUTPUT; SC_ORDER_APP_CHOICE returns SC_ERR_UNSUPPORTED.
+ *   out          receives the handle.
+ * The host arrays are copied; the context allocates its device tables on the
+ * current CUDA device (synchronously) and is usable from any stream/thread on it.
+ * Errors: SC_ERR_INVALID_ARG (bad sizes, ids, tau, k), SC_ERR_UNSUPPORTED,
+ * SC_ERR_OOM (device allocation), SC_ERR_CUDA. */
+sc_status sc_context_load(int32_t C, int32_t n_apps, const int32_t* n_lists, const int64_t* list_off,
+                          const int32_t* list_labels, float tau, float k, sc_order order,
+                          sc_context* out);
+
+/* sc_context_free — release the context's device tables (synchronises the device). NULL is a no-op. */
+sc_status sc_context_free(sc_context ctx);
+
+/* sc_context_info — D'_a of app a (n_lists), and the number of mapped labels |𝕎_a|. */
+sc_status sc_context_info(sc_context ctx, int32_t app, int32_t* n_lists, int32_t* n_mapped);
+
+/* A batch of inputs (rows).  All pointers are device pointers.
+ *   logits   [rows, ld] row-major, dtype elements; base 16-B aligned and
+ *            ld*sizeof(elt) % 16 == 0; ld >= C; columns C..ld-1 are never read
+ *            as values (they may hold anything).  May be NULL only for sc_decision_hist.
+ *   gt_off   [rows+1] int64 CSR offsets into gt_lab (any base, non-decreasing) —
+ *   gt_lab   ... the ground-truth label ids ŷ_i of row i, in [0,C), duplicates allowed.
+ *   gt_mask  [rows] uint8, optional: the precomputed G_i of each row, as written by
+ *            sc_decision_hist.  When non-NULL it replaces gt_off/gt_lab.
+ *            Bytes up to the next 16-B boundary past either end may be read (never
+ *            crossing a page; contents ignored).
+ *   app      [rows] uint16 application ids < n_apps, or NULL (every row is app 0);
+ *            same 16-B-boundary over-read note as gt_mask.
+ * A batch "has GT" iff gt_mask != NULL or gt_off != NULL. */
+typedef struct {
+  const void*     logits;
+  sc_dtype        dtype;
+  int64_t         rows;
+  int64_t         ld;
+  const int64_t*  gt_off;
+  const int32_t*  gt_lab;
+  const uint8_t*  gt_mask;
+  const uint16_t* app;
+} sc_batch;
+
+/* sc_decide — decisions and counters, no loss.
+ *   decision     [rows] uint8: 0..D'-1 or D' (default).
+ *   n_incorrect  [n_apps] += #{i : decision_i not in Decision(ŷ_i)} (Eq. goal; reading A7). Needs GT.
+ *   hist_pred    [n_apps*16] += #{i : decision_i = d} at [app*16 + d].
+ *   hist_gt      [n_apps*256] += #{i : G_i = m} at [app*256 + m].  Needs GT. */
+sc_status sc_decide(sc_context ctx, const sc_batch* batch, uint8_t* decision, uint64_t* n_incorrect,
+                    uint64_t* hist_pred, uint64_t* hist_gt, sc_stream stream);
+
+/* sc_decision_hist — ground-truth-only pre-pass (reads ~18 B/row, never the logits):
+ *   hist_gt      [n_apps*256] += mask histogram H (the per-class
+ *                marginals are h[d] = sum_{m ∋ d} H[m], h[default] = H[0]).
+ *   gt_mask_out  [rows] uint8, optional: G_i per row, for sc_batch.gt_mask.
+ * batch->logits is ignored; batch needs gt_off/gt_lab. */
+sc_status sc_decision_hist(sc_context ctx, const sc_batch* batch, uint64_t* hist_gt, uint8_t* gt_mask_out,
+                           sc_stream stream);
+
+/* sc_weights_from_hist — rebalancing weights from the GLOBAL mask histogram
+ * (PAPER.md:2014, :2020, :2029): per app, M = sum_m H[m]; N(m) = #inputs whose
+ * ground truth intersects m's lists = M - sum_{m' ∩ m = ∅} H[m'] for m != 0,
+ * N(0) = H[0] (non-target inputs); w[m] = M/N(m) in double rounded to float,
+ * 0 when N(m) = 0 (reading A13).
+ *   hist_gt  device [n_apps*256] uint64 (all ranks' counts, e.g. after an allreduce)
+ *   w        device [n_apps*256] float, overwritten. */
+sc_status sc_weights_from_hist(sc_context ctx, const uint64_t* hist_gt, float* w, sc_stream stream);
+
+/* sc_loss_fwd_bwd — the fused hot path: one read of each logit row gives the
+ * decision, the counters, and Eq. api_output with its gradient:
+ *   L_i = w[G_i] ( y_i S(max(P⁻,θ) − P⁺) + (1−y_i) S(P⁻ − θ) ),
+ *   P⁺ = σ(max_{c: cat[c] ∈ G_i} z_c), P⁻ = σ(max_{c ∈ 𝕎, cat[c] ∉ G_i} z_c), max ∅ = −∞.
+ * The arg maxima are exact (ties to the smaller label id, A8); P⁻ enters
+ * max(P⁻,θ) and gets gradient only when its logit is > tau (A10).
+ *   w           device [n_apps*256] float (from sc_weights_from_hist) or NULL (all 1).
+ *   grad_scale  multiplies every gradient entry (e.g. 1/B_global, reading A14).
+ *   loss_sum    [n_apps] double += sum_i L_i (unscaled).
+ *   loss_row    [rows] float, L_i.
+ *   grad_idx    [rows*2] int32: slot 0 = c⁺ (y_i = 1), slot 1 = c⁻ (when it gets
+ *   grad_val    [rows*2] float   gradient), -1 / 0.0f when absent.  All other
+ *                                dL_i/dz_c are exactly 0.
+ *   grad_dense  [rows*ld] float: the full gradient (zeros + at most 2 entries),
+ *               every element written, including the padding columns.
+ *   decision, n_incorrect, hist_pred, hist_gt: as in sc_decide (same pass).
+ * Needs GT.  Computes in fp32, accumulates loss_sum in fp64. */
+sc_status sc_loss_fwd_bwd(sc_context ctx, const sc_batch* batch, const float* w, float grad_scale,
+                          double* loss_sum, float* loss_row, int32_t* grad_idx, float* grad_val,
+                          float* grad_dense, uint8_t* decision, uint64_t* n_incorrect, uint64_t* hist_pred,
+                          uint64_t* hist_gt, sc_stream stream);
+
+/* Thread-local text for the last non-OK status of this thread ("" if none). */
+const char* sc_last_error(void);
+
+/* Number of kernel launches enqueued by this process (for bench accounting). */
+uint64_t sc_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SC_H */

@@ -1,0 +1,361 @@
+// sc_api.cu — host side of libsc: the C ABI declared in include/sc.h.
+// Validation, the context compile (a1), launch configuration and dispatch.
+#include "sc.h"
+#include "sc_internal.cuh"
+
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+struct sc_context_s {
+  int32_t C = 0, n_apps = 0, max_ent = 0;
+  float tau = 0.f, theta = 0.5f, k = 1.f;
+  int device = 0;
+  std::vector<int32_t> nlists, n_mapped;
+  uint8_t* d_cat = nullptr;
+  uint32_t* d_ent = nullptr;
+  int32_t* d_ent_off = nullptr;
+  uint8_t* d_nlists = nullptr;
+};
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<uint64_t> g_launches{0};
+
+sc_status fail(sc_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+sc_status cuda_fail(cudaError_t e, const char* what) {
+  return fail(e == cudaErrorMemoryAllocation ? SC_ERR_OOM : SC_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+constexpr size_t kSmemMax = 227 * 1024;
+
+struct DeviceInfo {
+  int sms = 0;
+  bool eval_attr = false;
+};
+
+DeviceInfo& device_info(int dev) {
+  static std::mutex mu;
+  static DeviceInfo infos[64];
+  std::lock_guard<std::mutex> lock(mu);
+  DeviceInfo& d = infos[dev & 63];
+  if (d.sms == 0) {
+    cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
+    if (d.sms <= 0) d.sms = 148;
+  }
+  if (!d.eval_attr) {
+    if (sc::set_eval_smem_limit(kSmemMax) == cudaSuccess) d.eval_attr = true;
+  }
+  return d;
+}
+
+int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+sc::DevContext dev_ctx(const sc_context_s* c) {
+  sc::DevContext d;
+  d.cat = c->d_cat;
+  d.ent = c->d_ent;
+  d.ent_off = c->d_ent_off;
+  d.nlists = c->d_nlists;
+  d.C = c->C;
+  d.n_apps = c->n_apps;
+  d.max_ent = c->max_ent;
+  d.tau = c->tau;
+  d.theta = c->theta;
+  d.k = c->k;
+  return d;
+}
+
+sc_status check_batch_common(const sc_context_s* ctx, const sc_batch* b) {
+  if (!ctx) return fail(SC_ERR_INVALID_ARG, "ctx is NULL");
+  if (!b) return fail(SC_ERR_INVALID_ARG, "batch is NULL");
+  if (b->rows < 0) return fail(SC_ERR_INVALID_ARG, "rows < 0");
+  if (b->gt_off && !b->gt_lab && !b->gt_mask) return fail(SC_ERR_INVALID_ARG, "gt_off without gt_lab");
+  return SC_OK;
+}
+
+int stage_kb_override() {
+  const char* s = std::getenv("SC_STAGE_KB");
+  if (!s) return 0;
+  const int v = std::atoi(s);
+  return (v >= 8 && v <= 200) ? v : 0;
+}
+
+// The fused pass behind sc_decide and sc_loss_fwd_bwd.
+sc_status run_eval(const sc_context_s* ctx, const sc_batch* b, const float* w, float grad_scale, double* loss_sum,
+                   float* loss_row, int32_t* grad_idx, float* grad_val, float* grad_dense, uint8_t* decision,
+                   uint64_t* n_incorrect, uint64_t* hist_pred, uint64_t* hist_gt, bool loss_call, cudaStream_t st) {
+  if (sc_status s = check_batch_common(ctx, b)) return s;
+  if (b->dtype != SC_F32 && b->dtype != SC_BF16) return fail(SC_ERR_INVALID_ARG, "unknown dtype %d", (int)b->dtype);
+  const bool has_gt = b->gt_mask || b->gt_off;
+  const bool want_loss = loss_call && (loss_sum || loss_row || grad_idx || grad_val || grad_dense);
+  if ((n_incorrect || hist_gt || loss_call) && !has_gt)
+    return fail(SC_ERR_INVALID_ARG, "n_incorrect / hist_gt / loss need ground truth (gt_mask or gt_off+gt_lab)");
+  if (b->rows == 0) return SC_OK;
+  if (!b->logits) return fail(SC_ERR_INVALID_ARG, "logits is NULL");
+  const int64_t elt = b->dtype == SC_F32 ? 4 : 2;
+  if (b->ld < ctx->C) return fail(SC_ERR_INVALID_ARG, "ld (%lld) < C (%d)", (long long)b->ld, ctx->C);
+  if ((b->ld * elt) % 16) return fail(SC_ERR_INVALID_ARG, "ld*sizeof(elt) must be a multiple of 16");
+  if (reinterpret_cast<uintptr_t>(b->logits) % 16) return fail(SC_ERR_INVALID_ARG, "logits not 16-B aligned");
+  if (grad_dense && reinterpret_cast<uintptr_t>(grad_dense) % 16)
+    return fail(SC_ERR_INVALID_ARG, "grad_dense not 16-B aligned");
+  if (b->app && reinterpret_cast<uintptr_t>(b->app) % 2) return fail(SC_ERR_INVALID_ARG, "app not 2-B aligned");
+
+  int dev = 0;
+  if (cudaError_t e = cudaGetDevice(&dev)) return cuda_fail(e, "cudaGetDevice");
+  if (dev != ctx->device) return fail(SC_ERR_INVALID_ARG, "context belongs to device %d, current is %d", ctx->device, dev);
+  DeviceInfo& di = device_info(dev);
+  if (!di.eval_attr) return fail(SC_ERR_CUDA, "cannot raise the kernel's shared-memory limit");
+
+  sc::EvalParams p{};
+  p.ctx = dev_ctx(ctx);
+  p.logits = static_cast<const uint8_t*>(b->logits);
+  p.rows = b->rows;
+  p.ld = b->ld;
+  p.ld_bytes = b->ld * elt;
+  p.bf16 = b->dtype == SC_BF16;
+  p.gt_off = b->gt_mask ? nullptr : b->gt_off;
+  p.gt_lab = b->gt_mask ? nullptr : b->gt_lab;
+  p.gt_mask = b->gt_mask;
+  p.app = b->app;
+  p.has_gt = has_gt;
+  p.w = want_loss ? w : nullptr;
+  p.grad_scale = grad_scale;
+  p.want_loss = want_loss;
+  p.loss_sum = loss_call ? loss_sum : nullptr;
+  p.loss_row = loss_call ? loss_row : nullptr;
+  p.grad_idx = loss_call ? grad_idx : nullptr;
+  p.grad_val = loss_call ? grad_val : nullptr;
+  p.grad_dense = loss_call ? grad_dense : nullptr;
+  p.decision = decision;
+  p.n_incorrect = reinterpret_cast<unsigned long long*>(n_incorrect);
+  p.hist_pred = reinterpret_cast<unsigned long long*>(hist_pred);
+  p.hist_gt = reinterpret_cast<unsigned long long*>(hist_gt);
+
+  // ---- schedule: stage = R rows (or R row-chunks) in shared memory
+  const int W = sc::kConsumerWarps;
+  const int64_t stage_cap = (stage_kb_override() ? stage_kb_override() : 64) * 1024;
+  p.copy_row_bytes = static_cast<int32_t>(round_up(static_cast<int64_t>(ctx->C) * elt, 16));
+  int64_t logits_region;
+  if (W * p.ld_bytes <= stage_cap) {
+    const int64_t rpw = std::max<int64_t>(1, std::min<int64_t>(16, stage_cap / (W * p.ld_bytes)));
+    p.R = static_cast<int32_t>(W * rpw);
+    p.nchunks = 1;
+    p.chunk_bytes = static_cast<int32_t>(p.ld_bytes);
+    p.chunk_elems = static_cast<int32_t>(b->ld);
+    logits_region = p.R * p.ld_bytes;
+  } else {
+    p.R = W;
+    p.chunk_bytes = static_cast<int32_t>((stage_cap / W) / 16 * 16);
+    p.chunk_elems = static_cast<int32_t>(p.chunk_bytes / elt);
+    p.nchunks = static_cast<int32_t>((p.copy_row_bytes + p.chunk_bytes - 1) / p.chunk_bytes);
+    logits_region = static_cast<int64_t>(p.R) * p.chunk_bytes;
+  }
+  p.nunits = (b->rows + p.R - 1) / p.R;
+  p.mask_off = static_cast<int32_t>(round_up(logits_region, 128));
+  p.app_off = static_cast<int32_t>(p.mask_off + round_up(p.R + 32, 16));
+  p.stage_bytes = static_cast<int32_t>(round_up(p.app_off + round_up(2 * p.R + 32, 16), 128));
+
+  // entries: one shared list (1 app), per-warp slots (several apps), or straight from global
+  int64_t ent_bytes = 0;
+  if (ctx->n_apps == 1 && static_cast<int64_t>(ctx->max_ent) * 4 <= 64 * 1024) {
+    p.ent_mode = 0;
+    ent_bytes = round_up(static_cast<int64_t>(ctx->max_ent) * 4, 128);
+  } else if (ctx->n_apps > 1 && static_cast<int64_t>(W) * ctx->max_ent * 4 <= 48 * 1024) {
+    p.ent_mode = 1;
+    p.ent_slot = ctx->max_ent;
+    ent_bytes = round_up(static_cast<int64_t>(W) * ctx->max_ent * 4, 128);
+  } else {
+    p.ent_mode = 2;
+  }
+  const bool wtab = want_loss && w && ctx->n_apps == 1;
+  const int64_t other = ent_bytes + (wtab ? 1024 : 0) + 2 * 8 * 8 + 256;
+  int64_t S = (static_cast<int64_t>(kSmemMax) - other) / p.stage_bytes;
+  if (S > 8) S = 8;
+  if (S < 2) return fail(SC_ERR_UNSUPPORTED, "row too large for the shared-memory pipeline");
+  p.stages = static_cast<int32_t>(S);
+  int64_t off = S * p.stage_bytes;
+  p.ent_smem_off = static_cast<int32_t>(off);
+  off += ent_bytes;
+  p.wtab_off = wtab ? static_cast<int32_t>(off) : -1;
+  off += wtab ? 1024 : 0;
+  p.bar_off = static_cast<int32_t>(round_up(off, 8));
+  off = p.bar_off + 2 * 8 * S;
+  const size_t smem = static_cast<size_t>(off);
+
+  const int grid = static_cast<int>(std::min<int64_t>(p.nunits, di.sms));
+  if (cudaError_t e = sc::launch_eval(p, grid, smem, st)) return cuda_fail(e, "eval kernel launch");
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return SC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+sc_status sc_context_load(int32_t C, int32_t n_apps, const int32_t* n_lists, const int64_t* list_off,
+                          const int32_t* list_labels, float tau, float k, sc_order order, sc_context* out) {
+  if (!out) return fail(SC_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  if (order == SC_ORDER_APP_CHOICE) return fail(SC_ERR_UNSUPPORTED, "SC_ORDER_APP_CHOICE is not implemented yet");
+  if (order != SC_ORDER_API_OUTPUT) return fail(SC_ERR_INVALID_ARG, "unknown order %d", (int)order);
+  if (C < 1 || C >= (1 << 23)) return fail(SC_ERR_INVALID_ARG, "C must be in [1, 2^23)");
+  if (n_apps < 1 || n_apps > 65535) return fail(SC_ERR_INVALID_ARG, "n_apps must be in [1, 65535]");
+  if (!n_lists || !list_off) return fail(SC_ERR_INVALID_ARG, "n_lists / list_off is NULL");
+  if (!std::isfinite(tau)) return fail(SC_ERR_INVALID_ARG, "tau must be finite");
+  if (!(k > 0.f) || !std::isfinite(k)) return fail(SC_ERR_INVALID_ARG, "k must be finite and > 0");
+  // validate the CSR
+  int64_t base = 0, total = 0;
+  for (int32_t a = 0; a < n_apps; ++a) {
+    if (n_lists[a] < 0 || n_lists[a] > 8) return fail(SC_ERR_INVALID_ARG, "n_lists[%d] = %d not in [0, 8]", a, n_lists[a]);
+    for (int32_t j = 0; j < n_lists[a]; ++j) {
+      if (list_off[base + j + 1] < list_off[base + j]) return fail(SC_ERR_INVALID_ARG, "list_off not non-decreasing (app %d)", a);
+    }
+    if (n_lists[a] > 0 && list_off[base] < 0) return fail(SC_ERR_INVALID_ARG, "negative list_off");
+    total = std::max<int64_t>(total, list_off[base + n_lists[a]]);
+    base += n_lists[a] + 1;
+  }
+  if (total > 0 && !list_labels) return fail(SC_ERR_INVALID_ARG, "list_labels is NULL");
+
+  auto* ctx = new sc_context_s();
+  ctx->C = C;
+  ctx->n_apps = n_apps;
+  ctx->tau = tau;
+  ctx->k = k;
+  ctx->theta = static_cast<float>(1.0 / (1.0 + std::exp(-static_cast<double>(tau))));
+  ctx->nlists.assign(n_lists, n_lists + n_apps);
+  // a1: cat[app][c] = first list, in code order, containing c (the listing's if-chain)
+  std::vector<uint8_t> cat(static_cast<size_t>(n_apps) * C, sc::kCatNone);
+  std::vector<uint32_t> ent;
+  std::vector<int32_t> ent_off(n_apps + 1, 0);
+  base = 0;
+  for (int32_t a = 0; a < n_apps; ++a) {
+    uint8_t* ca = cat.data() + static_cast<size_t>(a) * C;
+    for (int32_t j = 0; j < n_lists[a]; ++j) {
+      for (int64_t t = list_off[base + j]; t < list_off[base + j + 1]; ++t) {
+        const int32_t c = list_labels[t];
+        if (c < 0 || c >= C) {
+          delete ctx;
+          return fail(SC_ERR_INVALID_ARG, "label %d of app %d list %d not in [0, C)", c, a, j);
+        }
+        if (ca[c] == sc::kCatNone) ca[c] = static_cast<uint8_t>(j);
+      }
+    }
+    base += n_lists[a] + 1;
+    for (int32_t c = 0; c < C; ++c)
+      if (ca[c] != sc::kCatNone) ent.push_back(static_cast<uint32_t>(c) << 8 | ca[c]);
+    ent_off[a + 1] = static_cast<int32_t>(ent.size());
+    ctx->n_mapped.push_back(ent_off[a + 1] - ent_off[a]);
+    ctx->max_ent = std::max(ctx->max_ent, ent_off[a + 1] - ent_off[a]);
+  }
+  if (ent.empty()) ent.push_back(0);
+  std::vector<uint8_t> nl(n_apps);
+  for (int32_t a = 0; a < n_apps; ++a) nl[a] = static_cast<uint8_t>(n_lists[a]);
+
+  cudaError_t e = cudaGetDevice(&ctx->device);
+  if (!e) e = cudaMalloc(&ctx->d_cat, cat.size());
+  if (!e) e = cudaMalloc(&ctx->d_ent, ent.size() * 4);
+  if (!e) e = cudaMalloc(&ctx->d_ent_off, ent_off.size() * 4);
+  if (!e) e = cudaMalloc(&ctx->d_nlists, nl.size());
+  if (!e) e = cudaMemcpy(ctx->d_cat, cat.data(), cat.size(), cudaMemcpyHostToDevice);
+  if (!e) e = cudaMemcpy(ctx->d_ent, ent.data(), ent.size() * 4, cudaMemcpyHostToDevice);
+  if (!e) e = cudaMemcpy(ctx->d_ent_off, ent_off.data(), ent_off.size() * 4, cudaMemcpyHostToDevice);
+  if (!e) e = cudaMemcpy(ctx->d_nlists, nl.data(), nl.size(), cudaMemcpyHostToDevice);
+  if (e) {
+    sc_context_free(ctx);
+    return cuda_fail(e, "context upload");
+  }
+  *out = ctx;
+  return SC_OK;
+}
+
+sc_status sc_context_free(sc_context ctx) {
+  if (!ctx) return SC_OK;
+  cudaFree(ctx->d_cat);
+  cudaFree(ctx->d_ent);
+  cudaFree(ctx->d_ent_off);
+  cudaFree(ctx->d_nlists);
+  delete ctx;
+  return SC_OK;
+}
+
+sc_status sc_context_info(sc_context ctx, int32_t app, int32_t* n_lists, int32_t* n_mapped) {
+  if (!ctx) return fail(SC_ERR_INVALID_ARG, "ctx is NULL");
+  if (app < 0 || app >= ctx->n_apps) return fail(SC_ERR_INVALID_ARG, "app out of range");
+  if (n_lists) *n_lists = ctx->nlists[app];
+  if (n_mapped) *n_mapped = ctx->n_mapped[app];
+  return SC_OK;
+}
+
+sc_status sc_decide(sc_context ctx, const sc_batch* batch, uint8_t* decision, uint64_t* n_incorrect,
+                    uint64_t* hist_pred, uint64_t* hist_gt, sc_stream stream) {
+  return run_eval(ctx, batch, nullptr, 1.f, nullptr, nullptr, nullptr, nullptr, nullptr, decision, n_incorrect,
+                  hist_pred, hist_gt, false, static_cast<cudaStream_t>(stream));
+}
+
+sc_status sc_loss_fwd_bwd(sc_context ctx, const sc_batch* batch, const float* w, float grad_scale, double* loss_sum,
+                          float* loss_row, int32_t* grad_idx, float* grad_val, float* grad_dense, uint8_t* decision,
+                          uint64_t* n_incorrect, uint64_t* hist_pred, uint64_t* hist_gt, sc_stream stream) {
+  return run_eval(ctx, batch, w, grad_scale, loss_sum, loss_row, grad_idx, grad_val, grad_dense, decision,
+                  n_incorrect, hist_pred, hist_gt, true, static_cast<cudaStream_t>(stream));
+}
+
+sc_status sc_decision_hist(sc_context ctx, const sc_batch* b, uint64_t* hist_gt, uint8_t* gt_mask_out,
+                           sc_stream stream) {
+  if (sc_status s = check_batch_common(ctx, b)) return s;
+  if (!b->gt_off || !b->gt_lab) return fail(SC_ERR_INVALID_ARG, "sc_decision_hist needs gt_off and gt_lab");
+  if (b->rows == 0 || (!hist_gt && !gt_mask_out)) return SC_OK;
+  int dev = 0;
+  if (cudaError_t e = cudaGetDevice(&dev)) return cuda_fail(e, "cudaGetDevice");
+  if (dev != ctx->device) return fail(SC_ERR_INVALID_ARG, "context belongs to device %d, current is %d", ctx->device, dev);
+  DeviceInfo& di = device_info(dev);
+  sc::HistParams p{};
+  p.ctx = dev_ctx(ctx);
+  p.rows = b->rows;
+  p.gt_off = b->gt_off;
+  p.gt_lab = b->gt_lab;
+  p.app = b->app;
+  p.hist_gt = reinterpret_cast<unsigned long long*>(hist_gt);
+  p.gt_mask_out = gt_mask_out;
+  const size_t hbytes = static_cast<size_t>(ctx->n_apps) * 256 * 8;
+  p.smem_hist = hbytes <= 48 * 1024;
+  const int64_t blocks = std::min<int64_t>((b->rows + 255) / 256, static_cast<int64_t>(di.sms) * 8);
+  if (cudaError_t e = sc::launch_hist(p, static_cast<int>(blocks), p.smem_hist ? hbytes : 0,
+                                      static_cast<cudaStream_t>(stream)))
+    return cuda_fail(e, "hist kernel launch");
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return SC_OK;
+}
+
+sc_status sc_weights_from_hist(sc_context ctx, const uint64_t* hist_gt, float* w, sc_stream stream) {
+  if (!ctx) return fail(SC_ERR_INVALID_ARG, "ctx is NULL");
+  if (!hist_gt || !w) return fail(SC_ERR_INVALID_ARG, "hist_gt / w is NULL");
+  if (cudaError_t e = sc::launch_weights(reinterpret_cast<const unsigned long long*>(hist_gt), w, ctx->n_apps,
+                                         static_cast<cudaStream_t>(stream)))
+    return cuda_fail(e, "weights kernel launch");
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return SC_OK;
+}
+
+const char* sc_last_error(void) { return g_err.c_str(); }
+
+uint64_t sc_launch_count(void) { return g_launches.load(); }
+
+}  // extern "C"

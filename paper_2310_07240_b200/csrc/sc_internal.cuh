@@ -1,0 +1,87 @@
+// sc_internal.cuh — shared between the libsc host code and its sm_100a kernels.
+// Not part of the ABI (include/sc.h is).  Nothing here is shared with oracle/.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace sc {
+
+constexpr int kConsumerWarps = 16;                 // W: consumer warps per CTA
+constexpr int kThreads = 32 * (1 + kConsumerWarps);  // + 1 TMA producer warp
+constexpr uint32_t kNone = 0xFFFFFFFFu;            // "no label" key
+constexpr uint8_t kCatNone = 0xFF;                 // label in no list
+
+// Device-side context tables (built once by sc_context_load).
+struct DevContext {
+  const uint8_t* cat;       // [n_apps*C]  first list containing label c, or kCatNone   (a1)
+  const uint32_t* ent;      // per app, mapped labels sorted by id: key = c << 8 | cat[c]
+  const int32_t* ent_off;   // [n_apps+1]
+  const uint8_t* nlists;    // [n_apps]  D'
+  int32_t C, n_apps, max_ent;
+  float tau, theta, k;
+};
+
+// Parameters of the fused evaluation kernel (decide + counters + loss fwd/bwd).
+struct EvalParams {
+  DevContext ctx;
+  // batch
+  const uint8_t* logits;    // byte pointer, rows of ld_bytes
+  int64_t rows;
+  int64_t ld;               // elements
+  int64_t ld_bytes;
+  int32_t bf16;             // 0: f32, 1: bf16
+  const int64_t* gt_off;
+  const int32_t* gt_lab;
+  const uint8_t* gt_mask;
+  const uint16_t* app;
+  int32_t has_gt;
+  // loss
+  const float* w;
+  float grad_scale;
+  int32_t want_loss;
+  // outputs (NULL = not wanted)
+  double* loss_sum;
+  float* loss_row;
+  int32_t* grad_idx;
+  float* grad_val;
+  float* grad_dense;
+  uint8_t* decision;
+  unsigned long long* n_incorrect;
+  unsigned long long* hist_pred;
+  unsigned long long* hist_gt;
+  // schedule (host-computed)
+  int32_t R;                // rows per unit (multiple of kConsumerWarps)
+  int32_t nchunks;          // column chunks per row (1: whole rows, R rows copied at once)
+  int32_t chunk_bytes;      // bytes per row-chunk in smem (nchunks > 1)
+  int32_t chunk_elems;
+  int32_t copy_row_bytes;   // bytes of a row that carry labels 0..C-1, rounded up to 16
+  int64_t nunits;
+  int32_t stages;
+  int32_t stage_bytes;
+  int32_t mask_off;         // sideband offsets inside a stage
+  int32_t app_off;
+  int32_t ent_mode;         // 0: one shared smem list (n_apps==1), 1: per-warp smem slot, 2: global
+  int32_t ent_smem_off;     // byte offset of entry storage
+  int32_t ent_slot;         // entries per warp slot (mode 1)
+  int32_t wtab_off;         // byte offset of smem weight table (n_apps==1 && w), or -1
+  int32_t bar_off;          // byte offset of the mbarriers
+};
+
+struct HistParams {
+  DevContext ctx;
+  int64_t rows;
+  const int64_t* gt_off;
+  const int32_t* gt_lab;
+  const uint16_t* app;
+  unsigned long long* hist_gt;
+  uint8_t* gt_mask_out;
+  int32_t smem_hist;        // 1: CTA-private shared histogram (n_apps*256 counters)
+};
+
+// Launchers (sc_kernels.cu).  Return cudaError_t of the launch.
+cudaError_t launch_eval(const EvalParams& p, int grid, size_t smem, cudaStream_t st);
+cudaError_t launch_hist(const HistParams& p, int grid, size_t smem, cudaStream_t st);
+cudaError_t launch_weights(const unsigned long long* hist, float* w, int n_apps, cudaStream_t st);
+cudaError_t set_eval_smem_limit(size_t smem);
+
+}  // namespace sc

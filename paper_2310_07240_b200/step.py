@@ -1,0 +1,182 @@
+"""One data-parallel step of the hot path over the C ABI.
+
+    sc_decision_hist  (GT only: G_i per row + mask histogram)
+    -> all_reduce(hist_gt)                      [N > 1: the global N_i, PAPER.md:2029]
+    -> sc_weights_from_hist                     (M/N per mask, identical on every rank)
+    -> sc_loss_fwd_bwd (one read of the logits: decision, counters, loss, gradient)
+    -> all_reduce(n_incorrect, hist_pred), all_reduce(loss_sum)   [N > 1]
+
+Rows shard contiguously across ranks (``shard_range``); per-row outputs stay on
+their rank and only the aggregates cross GPUs.  torch.distributed (NCCL on GPUs,
+gloo in the CPU tests) is plumbing; every step of the path runs in libsc kernels.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from . import Batch, Context, sc_decision_hist, sc_loss_fwd_bwd, sc_weights_from_hist
+
+
+def shard_range(rows: int, rank: int, world: int):
+    """Contiguous row shard [lo, hi) of rank `rank` (sizes differ by at most one row)."""
+    base, rem = divmod(rows, world)
+    lo = rank * base + min(rank, rem)
+    return lo, lo + base + (1 if rank < rem else 0)
+
+
+def _pg_active(group) -> bool:
+    import torch.distributed as dist
+    return dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1
+
+
+def allreduce_(t: torch.Tensor, group=None):
+    """Sum-allreduce in place when a process group with >1 rank is active (exact for int64)."""
+    if _pg_active(group):
+        import torch.distributed as dist
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return t
+
+
+@dataclass
+class StepOutputs:
+    decision: torch.Tensor     # uint8 [rows]       (this rank's rows)
+    gt_mask: torch.Tensor      # uint8 [rows]
+    grad_idx: torch.Tensor     # int32 [rows*2]
+    grad_val: torch.Tensor     # float32 [rows*2]
+    hist_gt: torch.Tensor      # int64 [n_apps*256]  global after the step
+    counts: torch.Tensor       # int64 [n_apps*17]   n_incorrect | hist_pred(16), global
+    loss_sum: torch.Tensor     # float64 [n_apps]    global
+    w: torch.Tensor            # float32 [n_apps*256]
+    loss_row: torch.Tensor | None = None
+    grad_dense: torch.Tensor | None = None
+
+    def n_incorrect(self, n_apps: int):
+        return self.counts[:n_apps]
+
+    def hist_pred(self, n_apps: int):
+        return self.counts[n_apps:].view(n_apps, 16)
+
+
+class Evaluator:
+    """Preallocated buffers + the step sequence for batches of up to `max_rows` rows."""
+
+    def __init__(self, ctx: Context, max_rows: int, device="cuda", want_loss_row=False, dense_ld: int = 0,
+                 group=None):
+        self.ctx, self.group = ctx, group
+        na = ctx.n_apps
+        dev = torch.device(device)
+        r = max(int(max_rows), 1)
+        self.out = StepOutputs(
+            decision=torch.empty(r, dtype=torch.uint8, device=dev),
+            gt_mask=torch.empty(r + 16, dtype=torch.uint8, device=dev),
+            grad_idx=torch.empty(2 * r, dtype=torch.int32, device=dev),
+            grad_val=torch.empty(2 * r, dtype=torch.float32, device=dev),
+            hist_gt=torch.zeros(na * 256, dtype=torch.int64, device=dev),
+            counts=torch.zeros(na * 17, dtype=torch.int64, device=dev),
+            loss_sum=torch.zeros(na, dtype=torch.float64, device=dev),
+            w=torch.empty(na * 256, dtype=torch.float32, device=dev),
+            loss_row=torch.empty(r, dtype=torch.float32, device=dev) if want_loss_row else None,
+            grad_dense=torch.empty(r * dense_ld, dtype=torch.float32, device=dev) if dense_ld else None,
+        )
+
+    def step(self, logits, gt_off, gt_lab, app=None, grad_scale: float | None = None, global_rows: int | None = None):
+        o, ctx, na = self.out, self.ctx, self.ctx.n_apps
+        rows = logits.shape[0]
+        if grad_scale is None:
+            grad_scale = 1.0 / max(1, global_rows if global_rows is not None else rows)
+        o.hist_gt.zero_()
+        o.counts.zero_()
+        o.loss_sum.zero_()
+        gt_batch = Batch(logits=None, gt_off=gt_off, gt_lab=gt_lab, app=app, rows=rows)
+        sc_decision_hist(ctx, gt_batch, hist_gt=o.hist_gt, gt_mask_out=o.gt_mask)
+        allreduce_(o.hist_gt, self.group)
+        sc_weights_from_hist(ctx, o.hist_gt, o.w)
+        sc_loss_fwd_bwd(ctx, Batch(logits=logits, gt_mask=o.gt_mask, app=app), w=o.w, grad_scale=grad_scale,
+                        loss_sum=o.loss_sum, loss_row=o.loss_row, grad_idx=o.grad_idx, grad_val=o.grad_val,
+                        grad_dense=o.grad_dense, decision=o.decision, n_incorrect=o.counts[:na],
+                        hist_pred=o.counts[na:])
+        allreduce_(o.counts, self.group)
+        allreduce_(o.loss_sum, self.group)
+        return o
+
+    # ---------------------------------------------------------------- end to end (host buffers)
+
+    def host_outputs(self, rows: int):
+        """Pinned host buffers for step_host's per-row results and aggregates."""
+        na = self.ctx.n_apps
+        pin = dict(pin_memory=True)
+        return dict(decision=torch.empty(rows, dtype=torch.uint8, **pin),
+                    grad_idx=torch.empty(2 * rows, dtype=torch.int32, **pin),
+                    grad_val=torch.empty(2 * rows, dtype=torch.float32, **pin),
+                    counts=torch.empty(na * 17, dtype=torch.int64, **pin),
+                    hist_gt=torch.empty(na * 256, dtype=torch.int64, **pin),
+                    loss_sum=torch.empty(na, dtype=torch.float64, **pin))
+
+    def step_host(self, h_logits, h_gt_off, h_gt_lab, host_out, h_app=None, grad_scale=None,
+                  global_rows=None, chunk_rows: int = 1 << 16):
+        """The same step with inputs and outputs in (pinned) host memory.
+
+        The small ground truth goes first (pre-pass + weights need all of it); the logits
+        then stream host->device in chunks on a copy stream, double-buffered, each chunk's
+        sc_loss_fwd_bwd overlapping the next chunk's copy; per-row results stream back."""
+        o, ctx, na = self.out, self.ctx, self.ctx.n_apps
+        dev = o.decision.device
+        rows, C = h_logits.shape
+        if grad_scale is None:
+            grad_scale = 1.0 / max(1, global_rows if global_rows is not None else rows)
+        if not hasattr(self, "_stage") or self._stage[0].shape[0] < chunk_rows or self._stage[0].shape[1] != C \
+                or self._stage[0].dtype != h_logits.dtype:
+            self._stage = [torch.empty((chunk_rows, C), dtype=h_logits.dtype, device=dev) for _ in range(2)]
+            self._copy_stream = torch.cuda.Stream(dev)
+            self._d_off = None
+        if self._d_off is None or self._d_off.numel() < rows + 1 or self._d_lab.numel() < h_gt_lab.numel():
+            self._d_off = torch.empty(rows + 1, dtype=torch.int64, device=dev)
+            self._d_lab = torch.empty(max(1, h_gt_lab.numel()), dtype=torch.int32, device=dev)
+            self._d_app = torch.empty(rows, dtype=torch.int16, device=dev) if h_app is not None else None
+        comp = torch.cuda.current_stream(dev)
+        cp = self._copy_stream
+        d_off = self._d_off[:rows + 1]
+        d_off.copy_(h_gt_off, non_blocking=True)
+        d_lab = self._d_lab[:h_gt_lab.numel()]
+        d_lab.copy_(h_gt_lab, non_blocking=True)
+        d_app = None
+        if h_app is not None:
+            d_app = self._d_app[:rows]
+            d_app.copy_(h_app, non_blocking=True)
+        o.hist_gt.zero_()
+        o.counts.zero_()
+        o.loss_sum.zero_()
+        sc_decision_hist(ctx, Batch(gt_off=d_off, gt_lab=d_lab, app=d_app, rows=rows), hist_gt=o.hist_gt,
+                         gt_mask_out=o.gt_mask)
+        allreduce_(o.hist_gt, self.group)
+        sc_weights_from_hist(ctx, o.hist_gt, o.w)
+        free = [torch.cuda.Event(), torch.cuda.Event()]
+        ready = [torch.cuda.Event(), torch.cuda.Event()]
+        for e in free:
+            e.record(comp)
+        for ci, lo in enumerate(range(0, rows, chunk_rows)):
+            hi = min(rows, lo + chunk_rows)
+            buf = self._stage[ci & 1]
+            with torch.cuda.stream(cp):
+                cp.wait_event(free[ci & 1])
+                buf[:hi - lo].copy_(h_logits[lo:hi], non_blocking=True)
+                ready[ci & 1].record(cp)
+            comp.wait_event(ready[ci & 1])
+            sc_loss_fwd_bwd(ctx, Batch(logits=buf[:hi - lo], gt_mask=o.gt_mask[lo:], app=None if d_app is None
+                                       else d_app[lo:hi]),
+                            w=o.w, grad_scale=grad_scale, loss_sum=o.loss_sum, grad_idx=o.grad_idx[2 * lo:2 * hi],
+                            grad_val=o.grad_val[2 * lo:2 * hi], decision=o.decision[lo:hi],
+                            n_incorrect=o.counts[:na], hist_pred=o.counts[na:])
+            free[ci & 1].record(comp)
+        allreduce_(o.counts, self.group)
+        allreduce_(o.loss_sum, self.group)
+        host_out["decision"][:rows].copy_(o.decision[:rows], non_blocking=True)
+        host_out["grad_idx"][:2 * rows].copy_(o.grad_idx[:2 * rows], non_blocking=True)
+        host_out["grad_val"][:2 * rows].copy_(o.grad_val[:2 * rows], non_blocking=True)
+        host_out["counts"].copy_(o.counts, non_blocking=True)
+        host_out["hist_gt"].copy_(o.hist_gt, non_blocking=True)
+        host_out["loss_sum"].copy_(o.loss_sum, non_blocking=True)
+        comp.synchronize()
+        return host_out
