@@ -96,7 +96,9 @@ class ClockSampler:
         while not self._stop.is_set():
             try:
                 self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
-                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                fn = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                    nv.nvmlDeviceGetCurrentClocksThrottleReasons
+                r = fn(self.h)
                 for bit, name in self.REASONS.items():
                     if r & bit and name != "gpu_idle":
                         self.reasons.add(name)
@@ -152,8 +154,9 @@ def cpu_oracle_rate(seconds: float, threads: int | None = None, seed_rows=0):
     pre = orc.eval(b["logits"], b["gt_off"], b["gt_lab"], want_loss=False)
     orc.eval(b["logits"], b["gt_off"], b["gt_lab"], w=Oracle.weights_by_mask(pre["hist_gt"]))
     per_row = (time.perf_counter() - t) / chunk
-    n_chunks = max(threads, int(seconds * threads / (per_row * chunk)))
-    batches = [wl.host_batch(seed_rows + i * chunk, chunk) for i in range(n_chunks)]
+    n_chunks = max(threads, int(seconds / (per_row * chunk)))  # ~`seconds` of CPU work in total
+    with ThreadPoolExecutor(threads) as ex:
+        batches = list(ex.map(lambda i: wl.host_batch(seed_rows + i * chunk, chunk), range(n_chunks)))
 
     def hist(bb):
         return orc.eval(bb["logits"], bb["gt_off"], bb["gt_lab"], want_loss=False)["hist_gt"]
@@ -316,7 +319,7 @@ def run_ours(args):
         rate, rows, dt, threads = cpu_oracle_rate(args.cpu_seconds)
         line["cpu_baseline"] = {"value": rate, "unit": "samples/s", "cores": threads, "kind": "oracle",
                                 "sample": f"{rows} rows of cfg2 (rows 0..{rows - 1}), GT pre-pass + weights + full "
-                                          f"oracle pass, {threads} threads x 512-row chunks, {dt:.1f} s"}
+                                          f"oracle pass, {threads} threads x 512-row chunks, {dt:.2f} s wall"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
