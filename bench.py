@@ -38,8 +38,11 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--rows", type=int, default=ROWS_PER_GPU, help="rows per GPU (default: the config's 2^20)")
+    ap.add_argument("--rows", type=int, default=0, help="rows per GPU (default: 2^20 for cfg2)")
     ap.add_argument("--dtype", default="f32", choices=["f32", "bf16"])
+    ap.add_argument("--config", type=int, default=CFG, choices=[1, 2, 3, 4, 5],
+                    help="BASELINE.json config (default 2, the metric's config; others for characterisation)")
+    ap.add_argument("--kernel", default=None, choices=["tma", "gather"], help="force an eval kernel (default: auto)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -56,17 +59,42 @@ def dist_env():
     return world, rank, local
 
 
-def workload_name(dtype):
-    return f"cfg2_imagenet1k: C=1000 labels, D=4 (Recycle/Compost/Donate x10 + default), {dtype} logits"
+WORKLOADS = {
+    1: "cfg1_heapsortcypher: C=32 labels, D=4 (the paper's Recycle/Compost/Donate + default)",
+    2: "cfg2_imagenet1k: C=1000 labels, D=4 (Recycle/Compost/Donate x10 + default)",
+    3: "cfg3_openimages20k: C=20000 labels, D=8 (7 lists + default)",
+    4: "cfg4_multiapp256: C=1000 labels, 256 applications (per-row app id), contiguous rows per app",
+    5: "cfg5_rebalance64m: C=1000 labels, D=4 (cfg2's context), 64M rows over 8 GPUs",
+}
+DEFAULT_ROWS = {1: 4096, 2: 1 << 20, 3: 1 << 19, 4: 1 << 22, 5: 1 << 23}
 
 
-def touched_sector_bytes(spec, ld, elt):
-    """Bytes of the 32-B sectors of a row that hold at least one mapped label."""
+def workload_name(cfg, dtype):
+    return f"{WORKLOADS[cfg]}, {dtype} logits"
+
+
+def touched_sector_bytes(spec, ld, elt, rows=None, layout_rows_per_app=1 << 18):
+    """Mean bytes per row of the 32-B sectors holding at least one mapped label of the
+    row's application (SURVEY.md §8(d)'s algorithmic minimum), row base addresses r*ld*elt."""
     import numpy as np
-    mapped = spec.mapped()[0]
-    cols = np.nonzero(mapped)[0]
-    sectors = np.unique((cols * elt) // 32)
-    return int(len(sectors) * 32)
+    m = spec.mapped()
+    per_app = []
+    for a in range(spec.n_apps):
+        cols = np.nonzero(m[a])[0]
+        if len(cols) == 0:
+            per_app.append(0.0)
+            continue
+        if (ld * elt) % 32 == 0:
+            per_app.append(len(np.unique((cols * elt) // 32)) * 32.0)
+        else:  # rows not sector aligned: average over the two phases
+            tot = 0
+            for ph in (0, 16):
+                tot += len(np.unique((ph + cols * elt) // 32)) * 32
+            per_app.append(tot / 2)
+    if rows is None or spec.n_apps == 1:
+        return float(np.mean(per_app))
+    apps = (np.arange(rows) // layout_rows_per_app) % spec.n_apps
+    return float(np.mean(np.asarray(per_app)[apps]))
 
 
 class ClockSampler:
@@ -124,80 +152,103 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
-def load_traffic(dtype):
-    path = os.path.join(ROOT, "profiles", f"ncu_eval_cfg2_{dtype}.json")
+def load_traffic(cfg, dtype, kernel, rows):
+    """dram read+write bytes per launch of the eval kernel from the committed ncu summary
+    (profiles/ncu_eval_cfg{cfg}_{dtype}_{kernel}.json), scaled to this launch's rows."""
+    path = os.path.join(ROOT, "profiles", f"ncu_eval_cfg{cfg}_{dtype}_{kernel}.json")
     try:
         d = json.load(open(path))
-        return d.get("dram_bytes_per_launch"), d
+        return d["dram_bytes_per_row"] * rows, path
     except Exception:
         return None, None
 
 
 # ------------------------------------------------------------------ CPU oracle timing
 
+class OracleSample:
+    """A bounded sample of the cfg2 workload on the host plus the oracle (as it stands)
+    timed over it with `threads` host threads (512-row chunks; ctypes releases the GIL)."""
+
+    chunk = 512
+
+    def __init__(self, cpu_seconds: float, threads: int | None = None, seed_rows: int = 0):
+        from concurrent.futures import ThreadPoolExecutor
+
+        import synth
+        from oracle import Oracle
+        self.Oracle = Oracle
+        spec = synth.config_context(CFG)
+        self.wl = synth.Workload(spec, seed=CFG)
+        self.orc = Oracle.from_spec(spec)
+        self.threads = threads or os.cpu_count() or 1
+        b = self.wl.host_batch(seed_rows, self.chunk)
+        t = time.perf_counter()
+        pre = self.orc.eval(b["logits"], b["gt_off"], b["gt_lab"], want_loss=False)
+        self.orc.eval(b["logits"], b["gt_off"], b["gt_lab"], w=Oracle.weights_by_mask(pre["hist_gt"]))
+        per_row = (time.perf_counter() - t) / self.chunk
+        # ~cpu_seconds of oracle work in total (summed over threads)
+        n_chunks = max(self.threads, int(cpu_seconds / (per_row * self.chunk)))
+        n_chunks = min(n_chunks, (1 << 18) // self.chunk)  # <= 1 GB of host logits
+        with ThreadPoolExecutor(self.threads) as ex:
+            self.batches = list(ex.map(lambda i: self.wl.host_batch(seed_rows + i * self.chunk, self.chunk),
+                                       range(n_chunks)))
+        self.rows = n_chunks * self.chunk
+        self.first_row = seed_rows
+
+    def run(self):
+        """One pass of the hot path over the sample: GT pre-pass, weights, full pass. -> seconds"""
+        from concurrent.futures import ThreadPoolExecutor
+        orc, Oracle, rows = self.orc, self.Oracle, self.rows
+
+        def hist(bb):
+            return orc.eval(bb["logits"], bb["gt_off"], bb["gt_lab"], want_loss=False)["hist_gt"]
+
+        def full(args):
+            bb, w = args
+            return orc.eval(bb["logits"], bb["gt_off"], bb["gt_lab"], w=w, grad_scale=1.0 / rows)
+
+        t0 = time.perf_counter()
+        with ThreadPoolExecutor(self.threads) as ex:
+            H = sum(ex.map(hist, self.batches))
+            w = Oracle.weights_by_mask(H)
+            list(ex.map(full, [(bb, w) for bb in self.batches]))
+        return time.perf_counter() - t0
+
+    def describe(self, dt):
+        return (f"{self.rows} rows of cfg2 (rows {self.first_row}..{self.first_row + self.rows - 1}), GT pre-pass + "
+                f"weights + full oracle pass, {self.threads} threads x {self.chunk}-row chunks, {dt:.2f} s wall")
+
+
 def cpu_oracle_rate(seconds: float, threads: int | None = None, seed_rows=0):
     """Oracle (as it stands) on host cores over a bounded sample of the same workload."""
-    from concurrent.futures import ThreadPoolExecutor
-
-    import numpy as np
-
-    import synth
-    from oracle import Oracle
-    spec = synth.config_context(CFG)
-    wl = synth.Workload(spec, seed=CFG)
-    orc = Oracle.from_spec(spec)
-    threads = threads or os.cpu_count() or 1
-    # calibrate on one small chunk, then size the sample to ~`seconds` of oracle work
-    chunk = 512
-    b = wl.host_batch(seed_rows, chunk)
-    t = time.perf_counter()
-    pre = orc.eval(b["logits"], b["gt_off"], b["gt_lab"], want_loss=False)
-    orc.eval(b["logits"], b["gt_off"], b["gt_lab"], w=Oracle.weights_by_mask(pre["hist_gt"]))
-    per_row = (time.perf_counter() - t) / chunk
-    n_chunks = max(threads, int(seconds / (per_row * chunk)))  # ~`seconds` of CPU work in total
-    with ThreadPoolExecutor(threads) as ex:
-        batches = list(ex.map(lambda i: wl.host_batch(seed_rows + i * chunk, chunk), range(n_chunks)))
-
-    def hist(bb):
-        return orc.eval(bb["logits"], bb["gt_off"], bb["gt_lab"], want_loss=False)["hist_gt"]
-
-    def full(args):
-        bb, w = args
-        return orc.eval(bb["logits"], bb["gt_off"], bb["gt_lab"], w=w, grad_scale=1.0 / (n_chunks * chunk))
-
-    t0 = time.perf_counter()
-    with ThreadPoolExecutor(threads) as ex:
-        H = sum(ex.map(hist, batches))
-        w = Oracle.weights_by_mask(H)
-        list(ex.map(full, [(bb, w) for bb in batches]))
-    dt = time.perf_counter() - t0
-    rows = n_chunks * chunk
-    return rows / dt, rows, dt, threads
+    s = OracleSample(seconds, threads, seed_rows)
+    dt = s.run()
+    return s.rows / dt, s.rows, dt, s.threads, s
 
 
 def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
         return 0
-    # each step: a bounded sample sized so warmup+steps finish within ~2.5 minutes
-    budget = 150.0 / max(1, args.steps + args.warmup)
-    rates = []
+    # each step: one oracle pass over a bounded sample, sized so warmup+steps end in ~2.5 minutes
+    threads = os.cpu_count() or 1
+    budget_wall = 150.0 / max(1, args.steps + args.warmup)
+    sample = OracleSample(max(0.05, min(budget_wall, 10.0)) * threads)
+    times = []
     for i in range(args.warmup + args.steps):
-        r, rows, dt, threads = cpu_oracle_rate(max(0.2, min(budget, 10.0)), seed_rows=(i % 64) * 4096)
+        dt = sample.run()
         if i >= args.warmup:
-            rates.append((rows, dt))
-    total_rows = sum(r for r, _ in rates)
-    total_t = sum(t for _, t in rates)
-    value = total_rows / total_t
+            times.append(dt)
+    total_t = sum(times)
+    value = sample.rows * len(times) / total_t
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total_t / max(1, len(rates)),
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total_t / max(1, len(times)),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload_name("f32"), "C": 1000, "rows_per_step": total_rows // max(1, len(rates)),
-                   "parallelism": "host threads"},
-        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": threads, "kind": "oracle",
-                         "sample": f"{total_rows // max(1, len(rates))} rows of cfg2 per step (oracle/sc_oracle.c, "
-                                   f"{threads} threads over 512-row chunks)"},
+        "config": {"workload": workload_name(CFG, "f32"), "C": 1000, "rows_per_step": sample.rows,
+                   "parallelism": f"{sample.threads} host threads"},
+        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": sample.threads, "kind": "oracle",
+                         "sample": sample.describe(total_t / max(1, len(times))) + " per step"},
         "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -210,22 +261,34 @@ def run_ours(args):
     import numpy as np
     import torch
 
+    if args.kernel:
+        os.environ["SC_KERNEL"] = args.kernel
+    cfg = args.config
+
     world, rank, local = dist_env()
+    # SC_BENCH_SHARE_GPU=1: every rank on cuda:0 with gloo (exercises the N > 1 path on one GPU)
+    share = os.environ.get("SC_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     group = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     import paper_2310_07240_b200 as sc
     import synth
     from paper_2310_07240_b200.step import Evaluator
 
-    spec = synth.config_context(CFG)
-    B = args.rows
-    wl = synth.Workload(spec, seed=CFG, dtype=args.dtype)
+    spec = synth.config_context(cfg)
+    B = args.rows or DEFAULT_ROWS[cfg]
+    wl = synth.Workload(spec, seed=cfg, dtype=args.dtype, rows_per_app=1 << 18)
     data = wl.device_batch(rank * B, B, device=dev)  # this rank's rows of the global dataset
     logits, gt_off, gt_lab = data["logits"], data["gt_off"], data["gt_lab"]
+    app = data.get("app")
     ctx = sc.Context(spec.C, spec.lists, spec.tau, spec.k, multi_app=True)
     ev = Evaluator(ctx, B, device=dev, group=group)
     global_rows = B * world
@@ -237,7 +300,7 @@ def run_ours(args):
 
     stream = torch.cuda.current_stream(dev)
     for _ in range(args.warmup):
-        ev.step(logits, gt_off, gt_lab, global_rows=global_rows)
+        ev.step(logits, gt_off, gt_lab, app=app, global_rows=global_rows)
     torch.cuda.synchronize(dev)
 
     k_start = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -262,7 +325,7 @@ def run_ours(args):
         t_start.record(stream)
         for i in range(args.steps):
             idx["i"] = i
-            ev.step(logits, gt_off, gt_lab, global_rows=global_rows)
+            ev.step(logits, gt_off, gt_lab, app=app, global_rows=global_rows)
         t_end.record(stream)
         torch.cuda.synchronize(dev)
         barrier()
@@ -280,30 +343,32 @@ def run_ours(args):
 
     # sanity: the outputs of the last step are self-consistent
     o = ev.out
-    assert int(o.hist_gt.sum()) == global_rows and int(o.hist_pred(1).sum()) == global_rows
+    assert int(o.hist_gt.sum()) == global_rows and int(o.hist_pred(spec.n_apps).sum()) == global_rows
 
     # roofline of the dominant kernel (eval_kernel behind sc_loss_fwd_bwd)
     elt = 4 if args.dtype == "f32" else 2
     ld = logits.stride(0)
-    sect = touched_sector_bytes(spec, ld, elt)
-    per_row = sect + 1 + 1 + 8 + 8  # touched logit sectors + G_i in + decision out + sparse grad out
+    sect = touched_sector_bytes(spec, ld, elt, rows=B)
+    per_row = sect + 1 + 1 + 8 + 8 + (2 if app is not None else 0)  # sectors + G_i + decision + sparse grad (+ app id)
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     peak = peaks.get("hbm_gbs", 6650.0)
     achieved = B * per_row / (k_ms / 1e3) / 1e9
-    traffic, _ = load_traffic(args.dtype)
+    kname = sc.sc_last_kernel()
+    traffic, tpath = load_traffic(cfg, args.dtype, kname, B)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "kernel": "eval_kernel (sc_loss_fwd_bwd)", "kernel_ms": k_ms,
                 "algorithmic_bytes_per_row": per_row, "dense_bytes_per_row": ld * elt + 18,
                 "dense_frac": B * (ld * elt + 18) / (k_ms / 1e3) / 1e9 / peak,
+                "eval_kernel": kname, "traffic_source": tpath,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)" if peaks else "fallback 6.65 TB/s"}
 
     line = {
         "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
-        "config": {"workload": workload_name(args.dtype), "C": 1000, "rows_per_gpu": B, "global_batch": global_rows,
-                   "parallelism": f"dp{world}", "l2": "no flush: 4 GB of logits per step per GPU > 126 MB L2",
+        "config": {"workload": workload_name(cfg, args.dtype), "C": spec.C, "rows_per_gpu": B, "global_batch": global_rows,
+                   "parallelism": f"dp{world}", "l2": f"no flush: {B * ld * elt / 1e9:.2f} GB of logits per step per GPU > 126 MB L2",
                    "grad": "sparse (<= 2 entries/row)"},
         "roofline": roofline,
         "gpu_launches": int(launches),
@@ -316,10 +381,9 @@ def run_ours(args):
     del data, logits
     torch.cuda.empty_cache()
     if rank == 0 and not args.no_cpu_baseline:
-        rate, rows, dt, threads = cpu_oracle_rate(args.cpu_seconds)
+        rate, rows, dt, threads, smp = cpu_oracle_rate(args.cpu_seconds)
         line["cpu_baseline"] = {"value": rate, "unit": "samples/s", "cores": threads, "kind": "oracle",
-                                "sample": f"{rows} rows of cfg2 (rows 0..{rows - 1}), GT pre-pass + weights + full "
-                                          f"oracle pass, {threads} threads x 512-row chunks, {dt:.2f} s wall"}
+                                "sample": smp.describe(dt)}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -336,12 +400,15 @@ def run_e2e(args, ev, data, global_rows, dev, barrier, world):
     h_off = torch.empty(data["gt_off"].shape, dtype=torch.int64, pin_memory=True).copy_(data["gt_off"])
     h_lab = torch.empty(data["gt_lab"].shape, dtype=torch.int32, pin_memory=True).copy_(data["gt_lab"])
     host_out = ev.host_outputs(B)
-    ev.step_host(h_logits, h_off, h_lab, host_out, global_rows=global_rows)  # warm-up
+    h_app = None
+    if data.get("app") is not None:
+        h_app = torch.empty(data["app"].shape, dtype=torch.int16, pin_memory=True).copy_(data["app"])
+    ev.step_host(h_logits, h_off, h_lab, host_out, h_app=h_app, global_rows=global_rows)  # warm-up
     torch.cuda.synchronize(dev)
     barrier()
     t0 = time.perf_counter()
     for _ in range(args.e2e_steps):
-        ev.step_host(h_logits, h_off, h_lab, host_out, global_rows=global_rows)
+        ev.step_host(h_logits, h_off, h_lab, host_out, h_app=h_app, global_rows=global_rows)
     torch.cuda.synchronize(dev)
     dt = time.perf_counter() - t0
     if world > 1:
@@ -349,7 +416,8 @@ def run_e2e(args, ev, data, global_rows, dev, barrier, world):
         t = torch.tensor([dt], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dt = float(t[0])
-    h2d = h_logits.numel() * h_logits.element_size() + h_off.numel() * 8 + h_lab.numel() * 4
+    h2d = h_logits.numel() * h_logits.element_size() + h_off.numel() * 8 + h_lab.numel() * 4 + \
+        (h_app.numel() * 2 if h_app is not None else 0)
     d2h = sum(t.numel() * t.element_size() for t in host_out.values())
     del h_logits
     return {"value": global_rows * args.e2e_steps / dt, "unit": "samples/s", "h2d_bytes_per_step": int(h2d),

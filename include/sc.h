@@ -173,6 +173,11 @@ const char* sc_last_error(void);
 /* Number of kernel launches enqueued by this process (for bench accounting). */
 uint64_t sc_launch_count(void);
 
+/* Name of the evaluation kernel the last sc_decide / sc_loss_fwd_bwd call of this
+ * thread launched: "tma_ring" (dense rows staged through shared memory) or
+ * "gather_epl<N>" (sector-sparse loads of the mapped labels only). */
+const char* sc_last_kernel(void);
+
 #ifdef __cplusplus
 }
 #endif

@@ -20,7 +20,7 @@ from . import build as _build
 
 __all__ = [
     "ScError", "Context", "Batch", "sc_context_load", "sc_context_free", "sc_decide", "sc_decision_hist",
-    "sc_weights_from_hist", "sc_loss_fwd_bwd", "sc_last_error", "sc_launch_count", "library_path",
+    "sc_weights_from_hist", "sc_loss_fwd_bwd", "sc_last_error", "sc_launch_count", "sc_last_kernel", "library_path",
 ]
 
 SC_OK, SC_ERR_INVALID_ARG, SC_ERR_OOM, SC_ERR_CUDA, SC_ERR_UNSUPPORTED = range(5)
@@ -77,6 +77,8 @@ def _load():
     lib.sc_last_error.argtypes = []
     lib.sc_launch_count.restype = ctypes.c_uint64
     lib.sc_launch_count.argtypes = []
+    lib.sc_last_kernel.restype = ctypes.c_char_p
+    lib.sc_last_kernel.argtypes = []
     return lib
 
 
@@ -89,6 +91,10 @@ def sc_last_error() -> str:
 
 def sc_launch_count() -> int:
     return int(_lib.sc_launch_count())
+
+
+def sc_last_kernel() -> str:
+    return _lib.sc_last_kernel().decode()
 
 
 def _check(status: int):

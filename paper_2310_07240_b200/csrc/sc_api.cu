@@ -19,6 +19,8 @@ struct sc_context_s {
   float tau = 0.f, theta = 0.5f, k = 1.f;
   int device = 0;
   std::vector<int32_t> nlists, n_mapped;
+  int64_t touched_sectors[2] = {0, 0};  // sum over apps of 32-B sectors holding mapped labels (f32, bf16)
+  int64_t touched_lines[2] = {0, 0};    // same for 128-B lines (the granularity HBM is read at, measured)
   uint8_t* d_cat = nullptr;
   uint32_t* d_ent = nullptr;
   int32_t* d_ent_off = nullptr;
@@ -28,6 +30,7 @@ struct sc_context_s {
 namespace {
 
 thread_local std::string g_err;
+thread_local std::string g_last_kernel;
 std::atomic<uint64_t> g_launches{0};
 
 sc_status fail(sc_status st, const char* fmt, ...) {
@@ -91,6 +94,11 @@ sc_status check_batch_common(const sc_context_s* ctx, const sc_batch* b) {
   return SC_OK;
 }
 
+double gather_threshold() {
+  const char* s = std::getenv("SC_GATHER_MAX_FRAC");
+  return s ? std::atof(s) : 0.9;
+}
+
 int stage_kb_override() {
   const char* s = std::getenv("SC_STAGE_KB");
   if (!s) return 0;
@@ -149,13 +157,63 @@ sc_status run_eval(const sc_context_s* ctx, const sc_batch* b, const float* w, f
   p.hist_pred = reinterpret_cast<unsigned long long*>(hist_pred);
   p.hist_gt = reinterpret_cast<unsigned long long*>(hist_gt);
 
+  // ---- kernel choice: sector-sparse gather when the mapped labels leave enough row sectors untouched
+  {
+    const char* kenv = std::getenv("SC_KERNEL");
+    const int dt = b->dtype == SC_BF16 ? 1 : 0;
+    // HBM is read in 128-B lines here (measured: sector-sparse loads still move whole lines),
+    // so the sparse gather only pays when whole lines of the row stay untouched; it also
+    // wins for multi-app batches (no per-stage side-band / per-row context switch cost).
+    const int64_t lines_row = (static_cast<int64_t>(ctx->C) * elt + 127) / 128;
+    const double frac = static_cast<double>(ctx->touched_lines[dt]) / (static_cast<double>(lines_row) * ctx->n_apps);
+    bool gather = ctx->max_ent <= 1024 && (frac <= gather_threshold() || ctx->n_apps > 1);
+    if (kenv && std::string(kenv) == "tma") gather = false;
+    if (kenv && std::string(kenv) == "gather" && ctx->max_ent <= 1024) gather = true;
+    if (gather) {
+      if (const char* g = std::getenv("SC_L2_FETCH")) {  // experiment: L2 fetch granularity hint (bytes)
+        static int applied = -1;
+        const int v = std::atoi(g);
+        if (v != applied) {
+          cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, static_cast<size_t>(v));
+          applied = v;
+        }
+      }
+      int epl = 1;
+      while (epl * 32 < ctx->max_ent) epl *= 2;
+      p.wtab_off = (want_loss && w && ctx->n_apps == 1) ? 0 : -1;
+      if (cudaError_t e = sc::launch_gather(p, epl, di.sms, st)) return cuda_fail(e, "gather kernel launch");
+      g_last_kernel = "gather_epl" + std::to_string(epl);
+      g_launches.fetch_add(1, std::memory_order_relaxed);
+      return SC_OK;
+    }
+  }
   // ---- schedule: stage = R rows (or R row-chunks) in shared memory
   const int W = sc::kConsumerWarps;
-  const int64_t stage_cap = (stage_kb_override() ? stage_kb_override() : 64) * 1024;
+  const int64_t stage_cap = 64 * 1024;
   p.copy_row_bytes = static_cast<int32_t>(round_up(static_cast<int64_t>(ctx->C) * elt, 16));
+  const bool whole_rows = W * p.ld_bytes <= stage_cap;
+  // mapped labels in registers when whole rows fit a stage and |W| <= 1024
+  int epl = 0;
+  if (whole_rows && ctx->max_ent <= 1024 && !(std::getenv("SC_EPL") && std::atoi(std::getenv("SC_EPL")) == 0))
+    epl = std::max(0, sc::eval_epl_for(ctx->max_ent));
   int64_t logits_region;
-  if (W * p.ld_bytes <= stage_cap) {
-    const int64_t rpw = std::max<int64_t>(1, std::min<int64_t>(16, stage_cap / (W * p.ld_bytes)));
+  p.ng = 1;
+  if (epl > 0) {
+    // NG groups of W/NG warps, small stages (~16 KB) so a group releases its stage early
+    const char* ng_env = std::getenv("SC_NG");
+    p.ng = ng_env ? std::atoi(ng_env) : 4;
+    if (p.ng != 1 && p.ng != 2 && p.ng != 4 && p.ng != 8 && p.ng != 16) p.ng = 4;
+    const int wg = W / p.ng;
+    const int64_t target = (stage_kb_override() ? stage_kb_override() : 16) * 1024;
+    const int64_t rpw = std::max<int64_t>(1, std::min<int64_t>(32, target / (wg * p.ld_bytes)));
+    p.R = static_cast<int32_t>(wg * rpw);
+    p.nchunks = 1;
+    p.chunk_bytes = static_cast<int32_t>(p.ld_bytes);
+    p.chunk_elems = static_cast<int32_t>(b->ld);
+    logits_region = p.R * p.ld_bytes;
+  } else if (whole_rows) {
+    const int64_t cap = (stage_kb_override() ? stage_kb_override() : 64) * 1024;
+    const int64_t rpw = std::max<int64_t>(1, std::min<int64_t>(16, cap / (W * p.ld_bytes)));
     p.R = static_cast<int32_t>(W * rpw);
     p.nchunks = 1;
     p.chunk_bytes = static_cast<int32_t>(p.ld_bytes);
@@ -173,9 +231,19 @@ sc_status run_eval(const sc_context_s* ctx, const sc_batch* b, const float* w, f
   p.app_off = static_cast<int32_t>(p.mask_off + round_up(p.R + 32, 16));
   p.stage_bytes = static_cast<int32_t>(round_up(p.app_off + round_up(2 * p.R + 32, 16), 128));
 
-  // entries: one shared list (1 app), per-warp slots (several apps), or straight from global
+  // entries: in registers (epl > 0), else one shared list (1 app), per-warp slots
+  // (several apps), or straight from global
   int64_t ent_bytes = 0;
-  if (ctx->n_apps == 1 && static_cast<int64_t>(ctx->max_ent) * 4 <= 64 * 1024) {
+  p.pmtab_off = -1;
+  p.pmtab_bits = 0;
+  int64_t pmtab_bytes = 0;
+  if (epl > 0) {
+    p.ent_mode = 3;  // lane registers
+    if (ctx->n_apps == 1) {
+      p.pmtab_bits = ctx->nlists[0];
+      pmtab_bytes = (int64_t(1) << p.pmtab_bits) * 32 * 4;
+    }
+  } else if (ctx->n_apps == 1 && static_cast<int64_t>(ctx->max_ent) * 4 <= 64 * 1024) {
     p.ent_mode = 0;
     ent_bytes = round_up(static_cast<int64_t>(ctx->max_ent) * 4, 128);
   } else if (ctx->n_apps > 1 && static_cast<int64_t>(W) * ctx->max_ent * 4 <= 48 * 1024) {
@@ -186,22 +254,32 @@ sc_status run_eval(const sc_context_s* ctx, const sc_batch* b, const float* w, f
     p.ent_mode = 2;
   }
   const bool wtab = want_loss && w && ctx->n_apps == 1;
-  const int64_t other = ent_bytes + (wtab ? 1024 : 0) + 2 * 8 * 8 + 256;
+  const int64_t max_stages = epl > 0 ? 32 : 8;
+  const int64_t other = ent_bytes + pmtab_bytes + (wtab ? 1024 : 0) + 2 * 8 * max_stages + 256;
   int64_t S = (static_cast<int64_t>(kSmemMax) - other) / p.stage_bytes;
-  if (S > 8) S = 8;
-  if (S < 2) return fail(SC_ERR_UNSUPPORTED, "row too large for the shared-memory pipeline");
+  if (S > max_stages) S = max_stages;
+  S -= S % p.ng;  // stage s always belongs to group s % ng
+  if (S < 2 * p.ng) return fail(SC_ERR_UNSUPPORTED, "row too large for the shared-memory pipeline");
   p.stages = static_cast<int32_t>(S);
   int64_t off = S * p.stage_bytes;
   p.ent_smem_off = static_cast<int32_t>(off);
   off += ent_bytes;
+  if (pmtab_bytes) {
+    p.pmtab_off = static_cast<int32_t>(off);
+    off += pmtab_bytes;
+  }
   p.wtab_off = wtab ? static_cast<int32_t>(off) : -1;
   off += wtab ? 1024 : 0;
   p.bar_off = static_cast<int32_t>(round_up(off, 8));
   off = p.bar_off + 2 * 8 * S;
   const size_t smem = static_cast<size_t>(off);
 
+  p.split_copy = std::getenv("SC_SPLIT_COPY") ? 1 : 0;
+  p.no_evict_first = std::getenv("SC_NO_EVICT_FIRST") ? 1 : 0;
+  p.blocked = std::getenv("SC_BLOCKED") ? std::atoi(std::getenv("SC_BLOCKED")) : 0;
   const int grid = static_cast<int>(std::min<int64_t>(p.nunits, di.sms));
-  if (cudaError_t e = sc::launch_eval(p, grid, smem, st)) return cuda_fail(e, "eval kernel launch");
+  if (cudaError_t e = sc::launch_eval(p, epl, grid, smem, st)) return cuda_fail(e, "eval kernel launch");
+  g_last_kernel = epl ? "tma_ring_epl" + std::to_string(epl) : "tma_ring_list";
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return SC_OK;
 }
@@ -262,6 +340,21 @@ sc_status sc_context_load(int32_t C, int32_t n_apps, const int32_t* n_lists, con
     for (int32_t c = 0; c < C; ++c)
       if (ca[c] != sc::kCatNone) ent.push_back(static_cast<uint32_t>(c) << 8 | ca[c]);
     ent_off[a + 1] = static_cast<int32_t>(ent.size());
+    for (int dt = 0; dt < 2; ++dt) {
+      const int per_sector = dt == 0 ? 8 : 16;
+      int64_t last = -1, last_line = -1;
+      for (int32_t c = 0; c < C; ++c)
+        if (ca[c] != sc::kCatNone) {
+          if (c / per_sector != last) {
+            last = c / per_sector;
+            ++ctx->touched_sectors[dt];
+          }
+          if (c / (4 * per_sector) != last_line) {
+            last_line = c / (4 * per_sector);
+            ++ctx->touched_lines[dt];
+          }
+        }
+    }
     ctx->n_mapped.push_back(ent_off[a + 1] - ent_off[a]);
     ctx->max_ent = std::max(ctx->max_ent, ent_off[a + 1] - ent_off[a]);
   }
@@ -336,7 +429,7 @@ sc_status sc_decision_hist(sc_context ctx, const sc_batch* b, uint64_t* hist_gt,
   p.gt_mask_out = gt_mask_out;
   const size_t hbytes = static_cast<size_t>(ctx->n_apps) * 256 * 8;
   p.smem_hist = hbytes <= 48 * 1024;
-  const int64_t blocks = std::min<int64_t>((b->rows + 255) / 256, static_cast<int64_t>(di.sms) * 8);
+  const int64_t blocks = std::min<int64_t>((b->rows + 1023) / 1024, static_cast<int64_t>(di.sms) * 8);
   if (cudaError_t e = sc::launch_hist(p, static_cast<int>(blocks), p.smem_hist ? hbytes : 0,
                                       static_cast<cudaStream_t>(stream)))
     return cuda_fail(e, "hist kernel launch");
@@ -355,6 +448,8 @@ sc_status sc_weights_from_hist(sc_context ctx, const uint64_t* hist_gt, float* w
 }
 
 const char* sc_last_error(void) { return g_err.c_str(); }
+
+const char* sc_last_kernel(void) { return g_last_kernel.c_str(); }
 
 uint64_t sc_launch_count(void) { return g_launches.load(); }
 

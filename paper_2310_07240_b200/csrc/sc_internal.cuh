@@ -65,6 +65,12 @@ struct EvalParams {
   int32_t ent_slot;         // entries per warp slot (mode 1)
   int32_t wtab_off;         // byte offset of smem weight table (n_apps==1 && w), or -1
   int32_t bar_off;          // byte offset of the mbarriers
+  int32_t ng;               // consumer groups (stage i is consumed by group i % ng); 1 on the generic path
+  int32_t pmtab_off;        // byte offset of the plus-mask table [2^pmtab_bits][32] (single app), or -1
+  int32_t pmtab_bits;       // D' of the single app
+  int32_t split_copy;       // experiment: one bulk copy per row instead of one per stage
+  int32_t no_evict_first;   // experiment: L2 evict_normal instead of evict_first for the stream
+  int32_t blocked;          // units: one contiguous block per CTA (1) or round-robin over CTAs (0)
 };
 
 struct HistParams {
@@ -79,9 +85,14 @@ struct HistParams {
 };
 
 // Launchers (sc_kernels.cu).  Return cudaError_t of the launch.
-cudaError_t launch_eval(const EvalParams& p, int grid, size_t smem, cudaStream_t st);
+// epl > 0: lane-resident entries (|W| <= 32*epl, whole rows per stage); 0: generic list path.
+cudaError_t launch_eval(const EvalParams& p, int epl, int grid, size_t smem, cudaStream_t st);
+// Sector-sparse variant: epl = entries per lane capacity (1,2,4,8,16,32 -> |W| <= 32*epl).
+cudaError_t launch_gather(const EvalParams& p, int epl, int sms, cudaStream_t st);
 cudaError_t launch_hist(const HistParams& p, int grid, size_t smem, cudaStream_t st);
 cudaError_t launch_weights(const unsigned long long* hist, float* w, int n_apps, cudaStream_t st);
 cudaError_t set_eval_smem_limit(size_t smem);
+// Smallest compiled lane-resident entry capacity for max_ent mapped labels (-1: none fits).
+int eval_epl_for(int max_ent);
 
 }  // namespace sc

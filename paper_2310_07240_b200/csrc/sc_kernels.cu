@@ -100,18 +100,6 @@ __device__ __forceinline__ bool beats(float zo, uint32_t ko, float z, uint32_t k
   return zo > z || (zo == z && ko < k);
 }
 
-__device__ __forceinline__ void warp_lexmax(float& z, uint32_t& k) {
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    const float zo = __shfl_xor_sync(kFull, z, off);
-    const uint32_t ko = __shfl_xor_sync(kFull, k, off);
-    if (beats(zo, ko, z, k)) {
-      z = zo;
-      k = ko;
-    }
-  }
-}
-
 __device__ __forceinline__ float load_logit(const uint8_t* rowp, uint32_t col, int bf16) {
   if (bf16) return __uint_as_float(static_cast<uint32_t>(*reinterpret_cast<const uint16_t*>(rowp + 2u * col)) << 16);
   return *reinterpret_cast<const float*>(rowp + 4u * col);
@@ -258,8 +246,210 @@ __device__ __forceinline__ void deposit(RowBatch& b, int lane, float zp, uint32_
   ++b.n;
 }
 
+// Shared-memory loads by 32-bit shared address (no generic-to-shared conversion per load).
+// volatile keeps them after the mbarrier wait that makes the TMA bytes visible.
+template <bool BF16>
+__device__ __forceinline__ float lds_z(uint32_t a) {
+  if constexpr (BF16) {
+    unsigned short v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+    return __uint_as_float(static_cast<uint32_t>(v) << 16);
+  } else {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+    return v;
+  }
+}
+__device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
+  unsigned short v;
+  asm volatile("ld.shared.u8 %0, [%1];" : "=h"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
+  unsigned short v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+
+// ------------------------------------------------------------------ warp arg max (REDUX)
+
+// Order-preserving map float -> uint32 (negative: ~bits, positive: bits | sign).
+// -0.0 is first canonicalised to +0.0: the two compare equal, so they must tie (A4).
+__device__ __forceinline__ uint32_t ord_f32(float z) {
+  const uint32_t u = __float_as_uint(z + 0.0f);
+  return u ^ (static_cast<uint32_t>(static_cast<int32_t>(u) >> 31) | 0x80000000u);
+}
+__device__ __forceinline__ float unord_f32(uint32_t o) {
+  return __uint_as_float((o & 0x80000000u) ? (o ^ 0x80000000u) : ~o);
+}
+
+// Warp-wide lexicographic max of (z, -label) with two redux.sync instructions: the max of
+// the ordered logits, then the min key among the lanes holding it.  Keys are
+// label << 8 | cat (ordered like the label); kNone marks an empty lane.
+__device__ __forceinline__ void warp_argmax(float& z, uint32_t& k) {
+  const uint32_t o = (k == kNone) ? 0u : ord_f32(z);
+  const uint32_t om = __reduce_max_sync(kFull, o);
+  k = __reduce_min_sync(kFull, (o == om) ? k : kNone);
+  z = om ? unord_f32(om) : -CUDART_INF_F;
+}
+
+// ------------------------------------------------------------------ lane-resident context entries
+
+// The mapped labels of one application, spread over the warp: entry t of lane l is
+// mapped label number t*32 + l (ascending label ids within a lane, so a strict '>'
+// keeps the smaller id on ties).  Kept in registers across rows.
+template <int EPL>
+struct LaneEnt {
+  static constexpr bool kKeepOff = EPL <= 8;  // byte offsets cached in registers only when they fit
+  uint32_t key[EPL];   // label << 8 | cat
+  uint32_t off_[kKeepOff ? EPL : 1];  // byte offset of the label in a row (0 for absent entries)
+  __device__ __forceinline__ uint32_t off(int t, uint32_t elt) const {
+    if constexpr (kKeepOff) return off_[t];
+    else return key[t] == kNone ? 0u : (key[t] >> 8) * elt;
+  }
+  uint32_t catm[8];    // bit t set iff entry t is in list j
+  uint32_t valid;      // bit t set iff entry t exists
+  int32_t app;
+  int tc;              // warp-uniform: entry slots in use, ceil(n / 32)
+};
+
+template <int EPL>
+__device__ __forceinline__ void lane_ent_load(LaneEnt<EPL>& le, const uint32_t* ents, int n, int32_t app, int lane,
+                                              uint32_t elt) {
+  le.valid = 0;
+  le.app = app;
+  le.tc = (n + 31) >> 5;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) le.catm[j] = 0;
+#pragma unroll
+  for (int t = 0; t < EPL; ++t) {
+    const int e = t * 32 + lane;
+    const uint32_t k = e < n ? ents[e] : kNone;
+    le.key[t] = k;
+    if constexpr (LaneEnt<EPL>::kKeepOff) le.off_[t] = e < n ? (k >> 8) * elt : 0u;
+    if (e < n) {
+      le.valid |= 1u << t;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) le.catm[j] |= ((k & 0xFFu) == static_cast<uint32_t>(j) ? 1u : 0u) << t;
+    }
+  }
+}
+
+// Bit t of the result: entry t of this lane belongs to a list in G (i.e. to 𝒲_i).
+template <int EPL>
+__device__ __forceinline__ uint32_t plus_mask(const LaneEnt<EPL>& le, uint32_t G) {
+  uint32_t pm = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) pm |= (G & (1u << j)) ? le.catm[j] : 0u;
+  return pm;
+}
+
+// a3/a4 for one row, branch-free: zs[t] = the row's logit of the lane's entry t (all
+// loads issued before this is called); pm = plus_mask(G); tc = warp-uniform number of
+// entry slots in use.  Split maxima over 𝒲_i and 𝕎∖𝒲_i, reduced over the warp.
+// One entry of the split-maxima scan, in PTX so it stays at ~6 instructions:
+// the plus/minus class comes from one mask bit, each class keeps (max, key) with a
+// strict '>' (ascending ids within a lane keep the smaller id on ties).
+template <uint32_t BIT>
+__device__ __forceinline__ void scan_entry(float z, uint32_t key, uint32_t pm, float& zp, uint32_t& kp, float& zm,
+                                           uint32_t& km) {
+  asm("{\n\t"
+      ".reg .pred bp, gp, gm;\n\t"
+      ".reg .b32 t;\n\t"
+      "and.b32 t, %6, %7;\n\t"
+      "setp.ne.u32 bp, t, 0;\n\t"
+      "setp.gt.and.f32 gp, %4, %0, bp;\n\t"
+      "setp.gt.and.f32 gm, %4, %2, !bp;\n\t"
+      "@gp mov.f32 %0, %4;\n\t"
+      "@gp mov.b32 %1, %5;\n\t"
+      "@gm mov.f32 %2, %4;\n\t"
+      "@gm mov.b32 %3, %5;\n\t"
+      "}"
+      : "+f"(zp), "+r"(kp), "+f"(zm), "+r"(km)
+      : "f"(z), "r"(key), "r"(pm), "n"(BIT));
+}
+
+// The lane's last slot may be empty (lanes >= n mod 32): separate plus / minus masks.
+template <uint32_t BIT>
+__device__ __forceinline__ void scan_entry_masked(float z, uint32_t key, uint32_t vp, uint32_t vm, float& zp,
+                                                  uint32_t& kp, float& zm, uint32_t& km) {
+  asm("{\n\t"
+      ".reg .pred bp, bm, gp, gm;\n\t"
+      ".reg .b32 t, u;\n\t"
+      "and.b32 t, %6, %8;\n\t"
+      "and.b32 u, %7, %8;\n\t"
+      "setp.ne.u32 bp, t, 0;\n\t"
+      "setp.ne.u32 bm, u, 0;\n\t"
+      "setp.gt.and.f32 gp, %4, %0, bp;\n\t"
+      "setp.gt.and.f32 gm, %4, %2, bm;\n\t"
+      "@gp mov.f32 %0, %4;\n\t"
+      "@gp mov.b32 %1, %5;\n\t"
+      "@gm mov.f32 %2, %4;\n\t"
+      "@gm mov.b32 %3, %5;\n\t"
+      "}"
+      : "+f"(zp), "+r"(kp), "+f"(zm), "+r"(km)
+      : "f"(z), "r"(key), "r"(vp), "r"(vm), "n"(BIT));
+}
+
+// FULL: every slot before the last is populated in every lane (n > (EPL-1)*32), so
+// only the last slot needs the validity mask.
+template <int EPL, bool FULL, int T = 0>
+__device__ __forceinline__ void scan_all(const LaneEnt<EPL>& le, uint32_t pm, uint32_t vp, uint32_t vm,
+                                         const float (&zs)[EPL], float& zp, uint32_t& kp, float& zm, uint32_t& km) {
+  if constexpr (T < EPL - 1 && FULL) {
+    scan_entry<(1u << T)>(zs[T], le.key[T], pm, zp, kp, zm, km);
+  } else {
+    scan_entry_masked<(1u << T)>(zs[T], le.key[T], vp, vm, zp, kp, zm, km);
+  }
+  if constexpr (T + 1 < EPL) scan_all<EPL, FULL, T + 1>(le, pm, vp, vm, zs, zp, kp, zm, km);
+}
+
+// a3/a4 for one row: zs[t] = the row's logit of the lane's entry t (all loads issued
+// before this is called); pm = plus_mask(G).  Split maxima over 𝒲_i and 𝕎∖𝒲_i,
+// reduced over the warp.
+template <int EPL>
+__device__ __forceinline__ void scan_vals(const LaneEnt<EPL>& le, uint32_t pm, const float (&zs)[EPL], float& zp,
+                                          uint32_t& kp, float& zm, uint32_t& km) {
+  zp = zm = -CUDART_INF_F;
+  kp = km = kNone;
+  if (le.tc == EPL)  // warp-uniform
+    scan_all<EPL, true>(le, pm, le.valid & pm, le.valid & ~pm, zs, zp, kp, zm, km);
+  else
+    scan_all<EPL, false>(le, pm, le.valid & pm, le.valid & ~pm, zs, zp, kp, zm, km);
+  warp_argmax(zp, kp);
+  warp_argmax(zm, km);
+}
+
 // ------------------------------------------------------------------ fused evaluation kernel
 
+// The CTA's units: round-robin (u = blockIdx + i*grid) or one contiguous block per CTA.
+struct UnitSched {
+  int64_t base, stride, count;
+  __device__ __forceinline__ UnitSched(const EvalParams& p) {
+    if (p.blocked) {
+      const int64_t per = (p.nunits + gridDim.x - 1) / gridDim.x;
+      base = static_cast<int64_t>(blockIdx.x) * per;
+      stride = 1;
+      count = p.nunits - base < per ? p.nunits - base : per;
+      if (count < 0) count = 0;
+    } else {
+      base = blockIdx.x;
+      stride = gridDim.x;
+      count = (p.nunits - blockIdx.x + gridDim.x - 1) / gridDim.x;
+    }
+  }
+  __device__ __forceinline__ int64_t unit(int64_t i) const { return base + i * stride; }
+};
+
+// EPL > 0: whole rows per stage, mapped labels held in registers (|𝕎| <= 32*EPL).
+// EPL == 0: generic path — entries read from a shared/global list, rows may be split
+// into column chunks across stages (large C).
+template <int EPL, bool BF16>
 __global__ void __launch_bounds__(kThreads, 1) eval_kernel(const EvalParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.bar_off);
@@ -270,12 +460,12 @@ __global__ void __launch_bounds__(kThreads, 1) eval_kernel(const EvalParams p) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.stages; ++s) {
       mbar_init(full + s, 1);
-      mbar_init(empty + s, kConsumerWarps);
+      mbar_init(empty + s, kConsumerWarps / p.ng);
     }
     fence_mbar_init();
   }
   uint32_t* ent_smem = reinterpret_cast<uint32_t*>(smem + p.ent_smem_off);
-  if (p.ent_mode == 0) {
+  if (EPL == 0 && p.ent_mode == 0) {
     const int n = p.ctx.ent_off[1];
     for (int e = threadIdx.x; e < n; e += blockDim.x) ent_smem[e] = __ldg(p.ctx.ent + e);
   }
@@ -287,10 +477,13 @@ __global__ void __launch_bounds__(kThreads, 1) eval_kernel(const EvalParams p) {
   if (warp == 0) {
     // ================= TMA producer (one lane) =================
     if (lane == 0) {
-      const uint64_t pol = evict_first_policy();
+      uint64_t pol = evict_first_policy();
+      if (p.no_evict_first) asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
       int s = 0;
       uint32_t phase = 0;
-      for (int64_t u = blockIdx.x; u < p.nunits; u += gridDim.x) {
+      const UnitSched us(p);
+      for (int64_t i = 0; i < us.count; ++i) {
+        const int64_t u = us.unit(i);
         const int64_t r0 = u * p.R;
         const int nr = static_cast<int>((p.rows - r0 < p.R ? p.rows - r0 : (int64_t)p.R));
         for (int kc = 0; kc < p.nchunks; ++kc) {
@@ -322,8 +515,11 @@ __global__ void __launch_bounds__(kThreads, 1) eval_kernel(const EvalParams p) {
             bytes = cb * nr;
           }
           mbar_arrive_expect_tx(full + s, bytes + nb_m + nb_a);
-          if (p.nchunks == 1) {
+          if (p.nchunks == 1 && !p.split_copy) {
             bulk_g2s(st, p.logits + r0 * p.ld_bytes, bytes, full + s, pol);
+          } else if (p.nchunks == 1) {
+            const uint32_t rb = static_cast<uint32_t>(p.ld_bytes);
+            for (int j = 0; j < nr; ++j) bulk_g2s(st + static_cast<size_t>(j) * rb, p.logits + (r0 + j) * p.ld_bytes, rb, full + s, pol);
           } else {
             const uint32_t cb = bytes / nr;
             for (int j = 0; j < nr; ++j)
@@ -344,25 +540,6 @@ __global__ void __launch_bounds__(kThreads, 1) eval_kernel(const EvalParams p) {
   const int cw = warp - 1;
   RowBatch b;
   b.n = 0; b.zp = b.zm = 0.f; b.kp = b.km = kNone; b.G = 0; b.app = 0; b.row = 0;
-  uint32_t* slot = p.ent_mode == 1 ? ent_smem + static_cast<size_t>(cw) * p.ent_slot : nullptr;
-  int32_t cur_app = -1;
-  const uint32_t* ents = p.ent_mode == 0 ? ent_smem : nullptr;
-  int32_t n_ent = p.ent_mode == 0 ? p.ctx.ent_off[1] : 0;
-
-  auto select_app = [&](uint32_t a) {
-    if (p.ent_mode == 0 || static_cast<int32_t>(a) == cur_app) return;
-    const int32_t e0 = __ldg(p.ctx.ent_off + a), e1 = __ldg(p.ctx.ent_off + a + 1);
-    n_ent = e1 - e0;
-    if (p.ent_mode == 1) {
-      __syncwarp();
-      for (int e = lane; e < n_ent; e += 32) slot[e] = __ldg(p.ctx.ent + e0 + e);
-      __syncwarp();
-      ents = slot;
-    } else {
-      ents = p.ctx.ent + e0;
-    }
-    cur_app = static_cast<int32_t>(a);
-  };
 
   auto row_app_mask = [&](const uint8_t* st, int64_t r0, int64_t row, uint32_t& a, uint32_t& G) {
     a = 0;
@@ -381,87 +558,257 @@ __global__ void __launch_bounds__(kThreads, 1) eval_kernel(const EvalParams p) {
 
   int s = 0;
   uint32_t phase = 0;
-  for (int64_t u = blockIdx.x; u < p.nunits; u += gridDim.x) {
-    const int64_t r0 = u * p.R;
-    const int nr = static_cast<int>((p.rows - r0 < p.R ? p.rows - r0 : (int64_t)p.R));
-    if (p.nchunks == 1) {
-      mbar_wait(full + s, phase);
-      const uint8_t* st = smem + static_cast<size_t>(s) * p.stage_bytes;
-      for (int j = cw; j < nr; j += kConsumerWarps) {
+  if constexpr (EPL > 0) {
+    // ---- whole rows, lane-resident entries.  Consumer warps form NG groups of WG warps;
+    // CTA-local unit i lives in stage i % S and is consumed by group i % NG only, so a
+    // stage is released as soon as its WG warps are done (no CTA-wide stage barrier).
+    LaneEnt<EPL> le;
+    constexpr uint32_t kElt = BF16 ? 2u : 4u;
+    lane_ent_load(le, p.ctx.ent + __ldg(p.ctx.ent_off), __ldg(p.ctx.ent_off + 1) - __ldg(p.ctx.ent_off), 0, lane,
+                  kElt);
+    // single app: table of plus-masks per G value (one LDS per row instead of 8 selects)
+    uint32_t* pmtab = p.pmtab_off >= 0 ? reinterpret_cast<uint32_t*>(smem + p.pmtab_off) : nullptr;
+    if (pmtab) {
+      for (int g = cw; g < (1 << p.pmtab_bits); g += kConsumerWarps) pmtab[g * 32 + lane] = plus_mask(le, g);
+      asm volatile("bar.sync 1, %0;" ::"r"(kConsumerWarps * 32) : "memory");
+    }
+    const int ng = p.ng, wg = kConsumerWarps / p.ng;
+    const int grp = cw / wg, wi = cw % wg;
+    const uint32_t sbase = smem_addr(smem);
+    // this group's units are the CTA-local indices grp, grp+ng, ...: stage and phase advance by ng
+    int st_idx = grp;
+    uint32_t ph = 0;
+    const UnitSched us(p);
+    for (int64_t i = grp; i < us.count; i += ng) {
+      const int64_t u = us.unit(i);
+      const int64_t r0 = u * p.R;
+      const int nr = static_cast<int>((p.rows - r0 < p.R ? p.rows - r0 : (int64_t)p.R));
+      mbar_wait(full + st_idx, ph);
+      const uint32_t st_off = static_cast<uint32_t>(st_idx) * p.stage_bytes;
+      // side-band windows start at the 16-B boundary below row r0
+      const uint32_t m_base = st_off + p.mask_off + (p.gt_mask ? (reinterpret_cast<uintptr_t>(p.gt_mask + r0) & 15u) : 0u);
+      const uint32_t a_base = st_off + p.app_off + (p.app ? (reinterpret_cast<uintptr_t>(p.app + r0) & 15u) : 0u);
+      for (int j = wi; j < nr; j += wg) {
         const int64_t row = r0 + j;
-        uint32_t a, G;
-        row_app_mask(st, r0, row, a, G);
-        select_app(a);
-        const uint8_t* rowp = st + static_cast<int64_t>(j) * p.ld_bytes;
-        float zp = -CUDART_INF_F, zm = -CUDART_INF_F;
-        uint32_t kp = kNone, km = kNone;
-        // a3/a4: scan only the mapped labels, ascending ids per lane
-        for (int e = lane; e < n_ent; e += 32) {
-          const uint32_t key = ents[e];
-          const float z = load_logit(rowp, key >> 8, p.bf16);
-          if ((G >> (key & 0xFFu)) & 1u) {
-            if (z > zp) { zp = z; kp = key; }
-          } else {
-            if (z > zm) { zm = z; km = key; }
-          }
+        const uint32_t a = p.app ? lds_u16(sbase + a_base + 2u * j) : 0u;
+        uint32_t G = 0;
+        if (p.gt_mask) G = lds_u8(sbase + m_base + j);
+        else if (p.has_gt) G = warp_gt_mask(p, row, a, lane);
+        if (static_cast<int32_t>(a) != le.app) {
+          const int32_t e0 = __ldg(p.ctx.ent_off + a);
+          lane_ent_load(le, p.ctx.ent + e0, __ldg(p.ctx.ent_off + a + 1) - e0, static_cast<int32_t>(a), lane, kElt);
         }
-        warp_lexmax(zp, kp);
-        warp_lexmax(zm, km);
+        const uint32_t srow = sbase + st_off + static_cast<uint32_t>(j) * static_cast<uint32_t>(p.ld_bytes);
+        float zs[EPL];
+#pragma unroll
+        for (int t = 0; t < EPL; ++t) zs[t] = lds_z<BF16>(srow + le.off(t, kElt));
+        const uint32_t pm = pmtab ? lds_u32(sbase + p.pmtab_off + (G * 32 + lane) * 4) : plus_mask(le, G);
+        float zp, zm;
+        uint32_t kp, km;
+        scan_vals<EPL>(le, pm, zs, zp, kp, zm, km);
         deposit(b, lane, zp, kp, zm, km, G, a, row);
         if (b.n == 32) finish_batch(p, b, wtab, lane);
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(empty + s);
-      if (++s == p.stages) { s = 0; phase ^= 1u; }
-    } else {
-      // split rows: R == W, warp cw owns row r0 + cw across all chunks
-      const bool mine = cw < nr;
-      const int64_t row = r0 + cw;
-      uint32_t a = 0, G = 0;
-      float zp = -CUDART_INF_F, zm = -CUDART_INF_F;
-      uint32_t kp = kNone, km = kNone;
-      int pos = 0;
-      for (int kc = 0; kc < p.nchunks; ++kc) {
+      if (lane == 0) mbar_arrive(empty + st_idx);
+      st_idx += ng;
+      if (st_idx >= p.stages) { st_idx -= p.stages; ph ^= 1u; }
+    }
+  } else {
+    // ---- generic: entries from a list, rows possibly split into column chunks
+    uint32_t* slot = p.ent_mode == 1 ? ent_smem + static_cast<size_t>(cw) * p.ent_slot : nullptr;
+    int32_t cur_app = -1;
+    const uint32_t* ents = p.ent_mode == 0 ? ent_smem : nullptr;
+    int32_t n_ent = p.ent_mode == 0 ? p.ctx.ent_off[1] : 0;
+    auto select_app = [&](uint32_t a) {
+      if (p.ent_mode == 0 || static_cast<int32_t>(a) == cur_app) return;
+      const int32_t e0 = __ldg(p.ctx.ent_off + a), e1 = __ldg(p.ctx.ent_off + a + 1);
+      n_ent = e1 - e0;
+      if (p.ent_mode == 1) {
+        __syncwarp();
+        for (int e = lane; e < n_ent; e += 32) slot[e] = __ldg(p.ctx.ent + e0 + e);
+        __syncwarp();
+        ents = slot;
+      } else {
+        ents = p.ctx.ent + e0;
+      }
+      cur_app = static_cast<int32_t>(a);
+    };
+    const UnitSched us(p);
+    for (int64_t i = 0; i < us.count; ++i) {
+      const int64_t u = us.unit(i);
+      const int64_t r0 = u * p.R;
+      const int nr = static_cast<int>((p.rows - r0 < p.R ? p.rows - r0 : (int64_t)p.R));
+      // rows of this warp: one per stage pass when chunked (R == W), else j = cw + W*t
+      const int rows_here = p.nchunks == 1 ? (nr > cw ? (nr - cw + kConsumerWarps - 1) / kConsumerWarps : 0)
+                                           : (cw < nr ? 1 : 0);
+      if (p.nchunks == 1) {
         mbar_wait(full + s, phase);
         const uint8_t* st = smem + static_cast<size_t>(s) * p.stage_bytes;
-        if (mine) {
-          if (kc == 0) {
-            row_app_mask(st, r0, row, a, G);
-            select_app(a);
-          }
-          const uint8_t* rowp = st + static_cast<int64_t>(cw) * p.chunk_bytes;
-          const uint32_t c_lo = static_cast<uint32_t>(kc) * p.chunk_elems;
-          const uint32_t c_hi = c_lo + p.chunk_elems;
-          int stop = n_ent;
-          for (int e = pos + lane; e < n_ent; e += 32) {
+        for (int j = cw; j < nr; j += kConsumerWarps) {
+          const int64_t row = r0 + j;
+          uint32_t a, G;
+          row_app_mask(st, r0, row, a, G);
+          select_app(a);
+          const uint8_t* rowp = st + static_cast<int64_t>(j) * p.ld_bytes;
+          float zp = -CUDART_INF_F, zm = -CUDART_INF_F;
+          uint32_t kp = kNone, km = kNone;
+          for (int e = lane; e < n_ent; e += 32) {
             const uint32_t key = ents[e];
-            const uint32_t col = key >> 8;
-            if (col >= c_hi) { stop = e; break; }
-            const float z = load_logit(rowp, col - c_lo, p.bf16);
+            const float z = load_logit(rowp, key >> 8, BF16);
             if ((G >> (key & 0xFFu)) & 1u) {
               if (z > zp) { zp = z; kp = key; }
             } else {
               if (z > zm) { zm = z; km = key; }
             }
           }
-          pos = static_cast<int>(__reduce_min_sync(kFull, static_cast<uint32_t>(stop)));
+          warp_argmax(zp, kp);
+          warp_argmax(zm, km);
+          deposit(b, lane, zp, kp, zm, km, G, a, row);
+          if (b.n == 32) finish_batch(p, b, wtab, lane);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(empty + s);
         if (++s == p.stages) { s = 0; phase ^= 1u; }
-      }
-      if (mine) {
-        warp_lexmax(zp, kp);
-        warp_lexmax(zm, km);
-        deposit(b, lane, zp, kp, zm, km, G, a, row);
-        if (b.n == 32) finish_batch(p, b, wtab, lane);
+      } else {
+        const bool mine = rows_here > 0;
+        const int64_t row = r0 + cw;
+        uint32_t a = 0, G = 0;
+        float zp = -CUDART_INF_F, zm = -CUDART_INF_F;
+        uint32_t kp = kNone, km = kNone;
+        int pos = 0;
+        for (int kc = 0; kc < p.nchunks; ++kc) {
+          mbar_wait(full + s, phase);
+          const uint8_t* st = smem + static_cast<size_t>(s) * p.stage_bytes;
+          if (mine) {
+            if (kc == 0) {
+              row_app_mask(st, r0, row, a, G);
+              select_app(a);
+            }
+            const uint8_t* rowp = st + static_cast<int64_t>(cw) * p.chunk_bytes;
+            const uint32_t c_lo = static_cast<uint32_t>(kc) * p.chunk_elems;
+            const uint32_t c_hi = c_lo + p.chunk_elems;
+            int stop = n_ent;
+            for (int e = pos + lane; e < n_ent; e += 32) {
+              const uint32_t key = ents[e];
+              const uint32_t col = key >> 8;
+              if (col >= c_hi) { stop = e; break; }
+              const float z = load_logit(rowp, col - c_lo, BF16);
+              if ((G >> (key & 0xFFu)) & 1u) {
+                if (z > zp) { zp = z; kp = key; }
+              } else {
+                if (z > zm) { zm = z; km = key; }
+              }
+            }
+            pos = static_cast<int>(__reduce_min_sync(kFull, static_cast<uint32_t>(stop)));
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(empty + s);
+          if (++s == p.stages) { s = 0; phase ^= 1u; }
+        }
+        if (mine) {
+          warp_argmax(zp, kp);
+          warp_argmax(zm, km);
+          deposit(b, lane, zp, kp, zm, km, G, a, row);
+          if (b.n == 32) finish_batch(p, b, wtab, lane);
+        }
       }
     }
   }
   if (b.n > 0) finish_batch(p, b, wtab, lane);
 }
 
+// ------------------------------------------------------------------ sector-sparse gather kernel
+
+__device__ __forceinline__ float ldg_stream_f32(const float* p) {
+  float v;
+  asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ float ldg_stream_bf16(const uint16_t* p) {
+  unsigned short v;
+  asm volatile("ld.global.nc.L1::no_allocate.u16 %0, [%1];" : "=h"(v) : "l"(p));
+  return __uint_as_float(static_cast<uint32_t>(v) << 16);
+}
+
+// The same computation as eval_kernel, but each lane loads only its mapped labels'
+// logits straight from HBM (no shared-memory staging), so DRAM traffic is the 32-B
+// sectors that hold mapped labels instead of whole rows.  A warp issues the loads of
+// G rows (EPL per lane per row) before reducing any of them.
+template <int EPL, int G, bool BF16>
+__global__ void __launch_bounds__(256) gather_kernel(const EvalParams p) {
+  __shared__ float wtab_s[256];
+  const int lane = threadIdx.x & 31;
+  const bool wtab = p.wtab_off >= 0;
+  if (wtab)
+    for (int m = threadIdx.x; m < 256; m += blockDim.x) wtab_s[m] = __ldg(p.w + m);
+  __syncthreads();
+  const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int64_t ngroups = (p.rows + G - 1) / G;
+
+  LaneEnt<EPL> le;
+  le.app = -1;
+  RowBatch b;
+  b.n = 0; b.zp = b.zm = 0.f; b.kp = b.km = kNone; b.G = 0; b.app = 0; b.row = 0;
+  for (int64_t grp = gw; grp < ngroups; grp += nw) {
+    const int64_t r0 = grp * G;
+    const int nr = static_cast<int>(p.rows - r0 < G ? p.rows - r0 : G);
+    int j = 0;
+    while (j < nr) {
+      // a run of rows [j, j+run) sharing one application
+      const uint32_t a = p.app ? static_cast<uint32_t>(__ldg(p.app + r0 + j)) : 0u;
+      int run = 1;
+      if (p.app) {
+        while (j + run < nr && __ldg(p.app + r0 + j + run) == a) ++run;
+      } else {
+        run = nr - j;
+      }
+      if (static_cast<int32_t>(a) != le.app) {
+        const int32_t e0 = __ldg(p.ctx.ent_off + a);
+        lane_ent_load(le, p.ctx.ent + e0, __ldg(p.ctx.ent_off + a + 1) - e0, static_cast<int32_t>(a), lane,
+                      BF16 ? 2u : 4u);
+      }
+      // issue every load of the run first (memory-level parallelism), then reduce
+      float z[G][EPL];
+      uint32_t gm[G];
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const int64_t row = r0 + j + g;
+        const uint8_t* rowp = p.logits + row * p.ld_bytes;
+#pragma unroll
+        for (int t = 0; t < EPL; ++t) {
+          const bool ok = g < run && ((le.valid >> t) & 1u);
+          if (BF16) z[g][t] = ok ? ldg_stream_bf16(reinterpret_cast<const uint16_t*>(rowp + le.off(t, 2u))) : -CUDART_INF_F;
+          else      z[g][t] = ok ? ldg_stream_f32(reinterpret_cast<const float*>(rowp + le.off(t, 4u))) : -CUDART_INF_F;
+        }
+        gm[g] = (g < run && p.gt_mask) ? static_cast<uint32_t>(__ldg(p.gt_mask + row)) : 0u;
+      }
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        if (g < run) {  // warp-uniform
+          const int64_t row = r0 + j + g;
+          uint32_t Gi = gm[g];
+          if (!p.gt_mask && p.has_gt) Gi = warp_gt_mask(p, row, a, lane);
+          float zp, zm;
+          uint32_t kp, km;
+          scan_vals<EPL>(le, plus_mask(le, Gi), z[g], zp, kp, zm, km);
+          deposit(b, lane, zp, kp, zm, km, Gi, a, row);
+          if (b.n == 32) finish_batch(p, b, wtab ? wtab_s : nullptr, lane);
+        }
+      }
+      j += run;
+    }
+  }
+  if (b.n > 0) finish_batch(p, b, wtab ? wtab_s : nullptr, lane);
+}
+
 // ------------------------------------------------------------------ GT-only pre-pass
+
+// Thread-per-row with instruction-level parallelism: each thread walks kHR rows at
+// once so the three dependent loads (offsets -> labels -> cat) of kHR rows overlap.
+constexpr int kHR = 4, kHL = 4;
 
 __global__ void __launch_bounds__(256) hist_kernel(const HistParams p) {
   extern __shared__ unsigned long long sh_hist[];
@@ -473,29 +820,54 @@ __global__ void __launch_bounds__(256) hist_kernel(const HistParams p) {
   }
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   const int64_t start = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t iters = (p.rows + stride - 1) / stride;  // uniform trip count for warp-wide intrinsics
+  const int64_t per_iter = stride * kHR;
+  const int64_t iters = (p.rows + per_iter - 1) / per_iter;  // uniform trip count for warp-wide intrinsics
   for (int64_t it = 0; it < iters; ++it) {
-    const int64_t row = start + it * stride;
-    const bool active = row < p.rows;
-    uint32_t key = 0;
-    if (active) {
-      const uint32_t a = p.app ? __ldg(p.app + row) : 0u;
-      const uint8_t* cat = p.ctx.cat + static_cast<int64_t>(a) * p.ctx.C;
+    int64_t row[kHR], o0[kHR], o1[kHR];
+    uint32_t a[kHR];
+#pragma unroll
+    for (int k = 0; k < kHR; ++k) {
+      row[k] = it * per_iter + k * stride + start;
+      const bool act = row[k] < p.rows;
+      o0[k] = act ? __ldg(p.gt_off + row[k]) : 0;
+      o1[k] = act ? __ldg(p.gt_off + row[k] + 1) : 0;
+      a[k] = (act && p.app) ? static_cast<uint32_t>(__ldg(p.app + row[k])) : 0u;
+    }
+    int32_t lab[kHR][kHL];
+#pragma unroll
+    for (int k = 0; k < kHR; ++k)
+#pragma unroll
+      for (int t = 0; t < kHL; ++t) lab[k][t] = (o0[k] + t < o1[k]) ? __ldg(p.gt_lab + o0[k] + t) : -1;
+    uint32_t key[kHR];
+#pragma unroll
+    for (int k = 0; k < kHR; ++k) {
+      const uint8_t* cat = p.ctx.cat + static_cast<int64_t>(a[k]) * p.ctx.C;
       uint32_t G = 0;
-      for (int64_t t = __ldg(p.gt_off + row), e = __ldg(p.gt_off + row + 1); t < e; ++t) {
+#pragma unroll
+      for (int t = 0; t < kHL; ++t) {
+        if (lab[k][t] >= 0) {
+          const uint8_t v = __ldg(cat + lab[k][t]);
+          if (v != kCatNone) G |= 1u << v;
+        }
+      }
+      for (int64_t t = o0[k] + kHL; t < o1[k]; ++t) {  // rows with more than kHL labels
         const uint8_t v = __ldg(cat + __ldg(p.gt_lab + t));
         if (v != kCatNone) G |= 1u << v;
       }
-      if (p.gt_mask_out) p.gt_mask_out[row] = static_cast<uint8_t>(G);
-      key = a * 256u + G;
+      if (p.gt_mask_out && row[k] < p.rows) p.gt_mask_out[row[k]] = static_cast<uint8_t>(G);
+      key[k] = a[k] * 256u + G;
     }
     if (p.hist_gt) {
-      const unsigned act = __ballot_sync(kFull, active);
-      if (active) {
-        const unsigned peers = __match_any_sync(act, key);
-        if (lane == __ffs(peers) - 1) {
-          if (p.smem_hist) atomicAdd(sh_hist + key, static_cast<unsigned long long>(__popc(peers)));
-          else atomicAdd(p.hist_gt + key, static_cast<unsigned long long>(__popc(peers)));
+#pragma unroll
+      for (int k = 0; k < kHR; ++k) {
+        const bool active = row[k] < p.rows;
+        const unsigned act = __ballot_sync(kFull, active);
+        if (active) {
+          const unsigned peers = __match_any_sync(act, key[k]);
+          if (lane == __ffs(peers) - 1) {
+            if (p.smem_hist) atomicAdd(sh_hist + key[k], static_cast<unsigned long long>(__popc(peers)));
+            else atomicAdd(p.hist_gt + key[k], static_cast<unsigned long long>(__popc(peers)));
+          }
         }
       }
     }
@@ -534,13 +906,80 @@ __global__ void __launch_bounds__(256) weights_kernel(const unsigned long long* 
 
 }  // namespace
 
-cudaError_t set_eval_smem_limit(size_t smem) {
-  return cudaFuncSetAttribute(eval_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+template <int EPL>
+static cudaError_t set_limit_t(size_t smem) {
+  cudaError_t e = cudaFuncSetAttribute(eval_kernel<EPL, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e) return e;
+  return cudaFuncSetAttribute(eval_kernel<EPL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>(smem));
 }
 
-cudaError_t launch_eval(const EvalParams& p, int grid, size_t smem, cudaStream_t st) {
-  eval_kernel<<<grid, kThreads, smem, st>>>(p);
+#define SC_EVAL_EPLS(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(12) X(16) X(24) X(32)
+
+cudaError_t set_eval_smem_limit(size_t smem) {
+  cudaError_t e = set_limit_t<0>(smem);
+#define SC_SET(N) if (!e) e = set_limit_t<N>(smem);
+  SC_EVAL_EPLS(SC_SET)
+#undef SC_SET
+  return e;
+}
+
+int eval_epl_for(int max_ent) {
+  const int need = (max_ent + 31) / 32;
+#define SC_PICK(N) if (need <= N) return N;
+  SC_EVAL_EPLS(SC_PICK)
+#undef SC_PICK
+  return -1;
+}
+
+template <bool BF16>
+static void launch_eval_dt(const EvalParams& p, int epl, int grid, size_t smem, cudaStream_t st) {
+  switch (epl) {
+    case 0: eval_kernel<0, BF16><<<grid, kThreads, smem, st>>>(p); break;
+#define SC_CASE(N) case N: eval_kernel<N, BF16><<<grid, kThreads, smem, st>>>(p); break;
+    SC_EVAL_EPLS(SC_CASE)
+#undef SC_CASE
+    default: break;
+  }
+}
+
+cudaError_t launch_eval(const EvalParams& p, int epl, int grid, size_t smem, cudaStream_t st) {
+  if (p.bf16) launch_eval_dt<true>(p, epl, grid, smem, st);
+  else launch_eval_dt<false>(p, epl, grid, smem, st);
   return cudaGetLastError();
+}
+
+template <int EPL, int G, bool BF16>
+static cudaError_t launch_gather_t(const EvalParams& p, int sms, cudaStream_t st) {
+  static int blocks_per_sm = 0;
+  if (blocks_per_sm == 0) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, gather_kernel<EPL, G, BF16>, 256, 0);
+    if (blocks_per_sm < 1) blocks_per_sm = 1;
+  }
+  const int64_t warps_needed = (p.rows + G - 1) / G;
+  int64_t grid = static_cast<int64_t>(sms) * blocks_per_sm;
+  const int64_t max_grid = (warps_needed + 7) / 8;
+  if (grid > max_grid) grid = max_grid;
+  if (grid < 1) grid = 1;
+  gather_kernel<EPL, G, BF16><<<static_cast<int>(grid), 256, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+template <bool BF16>
+static cudaError_t launch_gather_dt(const EvalParams& p, int epl, int sms, cudaStream_t st) {
+  switch (epl) {
+    case 1: return launch_gather_t<1, 8, BF16>(p, sms, st);
+    case 2: return launch_gather_t<2, 8, BF16>(p, sms, st);
+    case 4: return launch_gather_t<4, 4, BF16>(p, sms, st);
+    case 8: return launch_gather_t<8, 4, BF16>(p, sms, st);
+    case 16: return launch_gather_t<16, 2, BF16>(p, sms, st);
+    default: return launch_gather_t<32, 1, BF16>(p, sms, st);
+  }
+}
+
+cudaError_t launch_gather(const EvalParams& p, int epl, int sms, cudaStream_t st) {
+  return p.bf16 ? launch_gather_dt<true>(p, epl, sms, st) : launch_gather_dt<false>(p, epl, sms, st);
 }
 
 cudaError_t launch_hist(const HistParams& p, int grid, size_t smem, cudaStream_t st) {

@@ -39,6 +39,22 @@ def allreduce_(t: torch.Tensor, group=None):
     return t
 
 
+def allreduce_many_(tensors, group=None):
+    """Several sum-allreduces issued as one NCCL group when the backend supports coalescing."""
+    if not _pg_active(group):
+        return tensors
+    import torch.distributed as dist
+    cm = getattr(dist, "_coalescing_manager", None)
+    if cm is not None and tensors[0].is_cuda:
+        with cm(group=group, device=tensors[0].device):
+            for t in tensors:
+                dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    else:
+        for t in tensors:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return tensors
+
+
 @dataclass
 class StepOutputs:
     decision: torch.Tensor     # uint8 [rows]       (this rank's rows)
@@ -68,14 +84,17 @@ class Evaluator:
         na = ctx.n_apps
         dev = torch.device(device)
         r = max(int(max_rows), 1)
+        # every accumulator in one buffer so a step clears them with a single memset:
+        # [hist_gt n_apps*256 | n_incorrect n_apps | hist_pred n_apps*16 | loss_sum n_apps (f64 bits)]
+        self._acc = torch.zeros(na * 256 + na * 17 + na, dtype=torch.int64, device=dev)
         self.out = StepOutputs(
             decision=torch.empty(r, dtype=torch.uint8, device=dev),
             gt_mask=torch.empty(r + 16, dtype=torch.uint8, device=dev),
             grad_idx=torch.empty(2 * r, dtype=torch.int32, device=dev),
             grad_val=torch.empty(2 * r, dtype=torch.float32, device=dev),
-            hist_gt=torch.zeros(na * 256, dtype=torch.int64, device=dev),
-            counts=torch.zeros(na * 17, dtype=torch.int64, device=dev),
-            loss_sum=torch.zeros(na, dtype=torch.float64, device=dev),
+            hist_gt=self._acc[:na * 256],
+            counts=self._acc[na * 256:na * 273],
+            loss_sum=self._acc[na * 273:].view(torch.float64),
             w=torch.empty(na * 256, dtype=torch.float32, device=dev),
             loss_row=torch.empty(r, dtype=torch.float32, device=dev) if want_loss_row else None,
             grad_dense=torch.empty(r * dense_ld, dtype=torch.float32, device=dev) if dense_ld else None,
@@ -86,9 +105,7 @@ class Evaluator:
         rows = logits.shape[0]
         if grad_scale is None:
             grad_scale = 1.0 / max(1, global_rows if global_rows is not None else rows)
-        o.hist_gt.zero_()
-        o.counts.zero_()
-        o.loss_sum.zero_()
+        self._acc.zero_()
         gt_batch = Batch(logits=None, gt_off=gt_off, gt_lab=gt_lab, app=app, rows=rows)
         sc_decision_hist(ctx, gt_batch, hist_gt=o.hist_gt, gt_mask_out=o.gt_mask)
         allreduce_(o.hist_gt, self.group)
@@ -97,8 +114,7 @@ class Evaluator:
                         loss_sum=o.loss_sum, loss_row=o.loss_row, grad_idx=o.grad_idx, grad_val=o.grad_val,
                         grad_dense=o.grad_dense, decision=o.decision, n_incorrect=o.counts[:na],
                         hist_pred=o.counts[na:])
-        allreduce_(o.counts, self.group)
-        allreduce_(o.loss_sum, self.group)
+        allreduce_many_([o.counts, o.loss_sum], self.group)
         return o
 
     # ---------------------------------------------------------------- end to end (host buffers)
@@ -145,9 +161,7 @@ class Evaluator:
         if h_app is not None:
             d_app = self._d_app[:rows]
             d_app.copy_(h_app, non_blocking=True)
-        o.hist_gt.zero_()
-        o.counts.zero_()
-        o.loss_sum.zero_()
+        self._acc.zero_()
         sc_decision_hist(ctx, Batch(gt_off=d_off, gt_lab=d_lab, app=d_app, rows=rows), hist_gt=o.hist_gt,
                          gt_mask_out=o.gt_mask)
         allreduce_(o.hist_gt, self.group)
@@ -170,8 +184,7 @@ class Evaluator:
                             grad_val=o.grad_val[2 * lo:2 * hi], decision=o.decision[lo:hi],
                             n_incorrect=o.counts[:na], hist_pred=o.counts[na:])
             free[ci & 1].record(comp)
-        allreduce_(o.counts, self.group)
-        allreduce_(o.loss_sum, self.group)
+        allreduce_many_([o.counts, o.loss_sum], self.group)
         host_out["decision"][:rows].copy_(o.decision[:rows], non_blocking=True)
         host_out["grad_idx"][:2 * rows].copy_(o.grad_idx[:2 * rows], non_blocking=True)
         host_out["grad_val"][:2 * rows].copy_(o.grad_val[:2 * rows], non_blocking=True)

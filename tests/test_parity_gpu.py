@@ -126,8 +126,15 @@ CASES = [
 ]
 
 
+@pytest.fixture(params=["tma", "gather"])
+def kernel(request, monkeypatch):
+    """Both eval kernels (dense TMA ring / sector-sparse gather) must meet the same bar."""
+    monkeypatch.setenv("SC_KERNEL", request.param)
+    return request.param
+
+
 @pytest.mark.parametrize("cfg,dtype,row0,rows,mode,ld_extra,layout", CASES)
-def test_parity_configs(cfg, dtype, row0, rows, mode, ld_extra, layout):
+def test_parity_configs(cfg, dtype, row0, rows, mode, ld_extra, layout, kernel):
     torch, sc, synth, _ = _mods()
     spec = synth.config_context(cfg)
     ld = synth.default_ld(spec.C, dtype) + ld_extra
@@ -154,7 +161,7 @@ def tie_heavy_batch(rng, C, rows, ld, lists, tau):
 
 @pytest.mark.parametrize("C,ld,rows", [(1, 4, 100), (4, 4, 333), (37, 40, 1000), (64, 64, 4097), (300, 300, 777),
                                        (4097, 4100, 97), (12000, 12000, 40)])
-def test_parity_tie_heavy_overlapping(C, ld, rows):
+def test_parity_tie_heavy_overlapping(C, ld, rows, kernel):
     _, _, synth, _ = _mods()
     rng = np.random.default_rng(C * 7 + rows)
     for tau in (0.0, -1.0):
@@ -167,7 +174,7 @@ def test_parity_tie_heavy_overlapping(C, ld, rows):
         compare(g, o, w, rows)
 
 
-def test_hand_cases_through_gpu(golden_dir):
+def test_hand_cases_through_gpu(golden_dir, kernel):
     import json, os
     torch, sc, synth, Oracle = _mods()
     cases = json.load(open(os.path.join(golden_dir, "hand_cases.json")))
@@ -196,7 +203,7 @@ def test_hand_cases_through_gpu(golden_dir):
             assert got[c] == pytest.approx(want[c], rel=2e-6), case["id"]
 
 
-def test_accumulate_and_chunking():
+def test_accumulate_and_chunking(kernel):
     """Outputs accumulate (+=): two half-batches equal one whole batch (the shard algebra)."""
     torch, sc, synth, _ = _mods()
     spec = synth.config_context(2)
@@ -270,3 +277,34 @@ def test_evaluator_step_matches_oracle():
     np.testing.assert_array_equal(o.hist_pred(1).cpu().numpy().reshape(-1).astype(np.uint64), ref["hist_pred"])
     np.testing.assert_allclose(o.loss_sum.cpu().numpy(), ref["loss_sum"], rtol=RTOL)
     np.testing.assert_allclose(o.grad_val[:8000].cpu().numpy(), ref["grad_val"], rtol=RTOL, atol=0)
+
+
+def test_step_host_matches_device_step():
+    """The end-to-end API (pinned host buffers, chunked H2D overlapped with the kernel)
+    returns exactly what the device-resident step returns."""
+    torch, sc, synth, _ = _mods()
+    from paper_2310_07240_b200.step import Evaluator
+    spec = synth.config_context(4)
+    wl = synth.Workload(spec, seed=4, layout=1)
+    rows = 20000
+    b = wl.host_batch(0, rows)
+    d = to_dev(b, "f32")
+    ctx = sc.Context(spec.C, spec.lists, multi_app=True)
+    ev = Evaluator(ctx, rows)
+    o = ev.step(d["logits"], d["gt_off"], d["gt_lab"], app=d["app"])
+    torch.cuda.synchronize()
+    ref = {k: getattr(o, k)[: (2 * rows if k.startswith("grad") else rows)].clone()
+           for k in ("decision", "grad_idx", "grad_val")}
+    ref_counts, ref_hist, ref_loss = o.counts.clone(), o.hist_gt.clone(), o.loss_sum.clone()
+    h_logits = torch.from_numpy(b["logits"]).pin_memory()
+    h_off = torch.from_numpy(b["gt_off"]).pin_memory()
+    h_lab = torch.from_numpy(b["gt_lab"]).pin_memory()
+    h_app = torch.from_numpy(b["app"].view(np.int16)).pin_memory()
+    out = ev.host_outputs(rows)
+    ev.step_host(h_logits, h_off, h_lab, out, h_app=h_app, chunk_rows=3000)
+    assert torch.equal(out["decision"][:rows], ref["decision"].cpu())
+    assert torch.equal(out["grad_idx"][: 2 * rows], ref["grad_idx"].cpu())
+    assert torch.equal(out["grad_val"][: 2 * rows], ref["grad_val"].cpu())
+    assert torch.equal(out["counts"], ref_counts.cpu())
+    assert torch.equal(out["hist_gt"], ref_hist.cpu())
+    np.testing.assert_allclose(out["loss_sum"].numpy(), ref_loss.cpu().numpy(), rtol=1e-12)
