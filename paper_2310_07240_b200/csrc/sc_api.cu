@@ -170,6 +170,7 @@ sc_status run_eval(const sc_context_s* ctx, const sc_batch* b, const float* w, f
     if (kenv && std::string(kenv) == "tma") gather = false;
     if (kenv && std::string(kenv) == "gather" && ctx->max_ent <= 1024) gather = true;
     if (gather) {
+      p.ld_flavor = std::getenv("SC_LD_FLAVOR") ? std::atoi(std::getenv("SC_LD_FLAVOR")) : 0;
       if (const char* g = std::getenv("SC_L2_FETCH")) {  // experiment: L2 fetch granularity hint (bytes)
         static int applied = -1;
         const int v = std::atoi(g);
@@ -199,13 +200,15 @@ sc_status run_eval(const sc_context_s* ctx, const sc_batch* b, const float* w, f
   int64_t logits_region;
   p.ng = 1;
   if (epl > 0) {
-    // NG groups of W/NG warps, small stages (~16 KB) so a group releases its stage early
-    const char* ng_env = std::getenv("SC_NG");
-    p.ng = ng_env ? std::atoi(ng_env) : 4;
-    if (p.ng != 1 && p.ng != 2 && p.ng != 4 && p.ng != 8 && p.ng != 16) p.ng = 4;
+    // ~16 rows per stage: rpw rows per warp (about 4 KB of logits per warp), NG = min(4, rpw)
+    // groups of W/NG warps; a group releases its stage as soon as its own warps are done.
+    int64_t rpw = 1;
+    while (rpw < 32 && 2 * rpw * p.ld_bytes <= 4096) rpw *= 2;
+    p.ng = static_cast<int32_t>(std::min<int64_t>(4, rpw));
+    if (const char* ng_env = std::getenv("SC_NG")) p.ng = std::atoi(ng_env);
+    if (p.ng != 1 && p.ng != 2 && p.ng != 4 && p.ng != 8 && p.ng != 16) p.ng = 1;
     const int wg = W / p.ng;
-    const int64_t target = (stage_kb_override() ? stage_kb_override() : 16) * 1024;
-    const int64_t rpw = std::max<int64_t>(1, std::min<int64_t>(32, target / (wg * p.ld_bytes)));
+    if (stage_kb_override()) rpw = std::max<int64_t>(1, std::min<int64_t>(32, stage_kb_override() * 1024 / (wg * p.ld_bytes)));
     p.R = static_cast<int32_t>(wg * rpw);
     p.nchunks = 1;
     p.chunk_bytes = static_cast<int32_t>(p.ld_bytes);

@@ -71,6 +71,7 @@ struct EvalParams {
   int32_t split_copy;       // experiment: one bulk copy per row instead of one per stage
   int32_t no_evict_first;   // experiment: L2 evict_normal instead of evict_first for the stream
   int32_t blocked;          // units: one contiguous block per CTA (1) or round-robin over CTAs (0)
+  int32_t ld_flavor;        // gather kernel global-load cache flavour (see ldg_stream_f32)
 };
 
 struct HistParams {

@@ -720,15 +720,22 @@ __global__ void __launch_bounds__(kThreads, 1) eval_kernel(const EvalParams p) {
 
 // ------------------------------------------------------------------ sector-sparse gather kernel
 
-__device__ __forceinline__ float ldg_stream_f32(const float* p) {
+// Load flavours (experiment, EvalParams::ld_flavor): 0 nc+L1::no_allocate, 1 .cg, 2 default, 3 .cs
+__device__ __forceinline__ float ldg_stream_f32(const float* p, int fl) {
   float v;
-  asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  if (fl == 1) asm volatile("ld.global.cg.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  else if (fl == 2) asm volatile("ld.global.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  else if (fl == 3) asm volatile("ld.global.cs.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  else asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
   return v;
 }
 
-__device__ __forceinline__ float ldg_stream_bf16(const uint16_t* p) {
+__device__ __forceinline__ float ldg_stream_bf16(const uint16_t* p, int fl) {
   unsigned short v;
-  asm volatile("ld.global.nc.L1::no_allocate.u16 %0, [%1];" : "=h"(v) : "l"(p));
+  if (fl == 1) asm volatile("ld.global.cg.u16 %0, [%1];" : "=h"(v) : "l"(p));
+  else if (fl == 2) asm volatile("ld.global.u16 %0, [%1];" : "=h"(v) : "l"(p));
+  else if (fl == 3) asm volatile("ld.global.cs.u16 %0, [%1];" : "=h"(v) : "l"(p));
+  else asm volatile("ld.global.nc.L1::no_allocate.u16 %0, [%1];" : "=h"(v) : "l"(p));
   return __uint_as_float(static_cast<uint32_t>(v) << 16);
 }
 
@@ -780,8 +787,8 @@ __global__ void __launch_bounds__(256) gather_kernel(const EvalParams p) {
 #pragma unroll
         for (int t = 0; t < EPL; ++t) {
           const bool ok = g < run && ((le.valid >> t) & 1u);
-          if (BF16) z[g][t] = ok ? ldg_stream_bf16(reinterpret_cast<const uint16_t*>(rowp + le.off(t, 2u))) : -CUDART_INF_F;
-          else      z[g][t] = ok ? ldg_stream_f32(reinterpret_cast<const float*>(rowp + le.off(t, 4u))) : -CUDART_INF_F;
+          if (BF16) z[g][t] = ok ? ldg_stream_bf16(reinterpret_cast<const uint16_t*>(rowp + le.off(t, 2u)), p.ld_flavor) : -CUDART_INF_F;
+          else      z[g][t] = ok ? ldg_stream_f32(reinterpret_cast<const float*>(rowp + le.off(t, 4u)), p.ld_flavor) : -CUDART_INF_F;
         }
         gm[g] = (g < run && p.gt_mask) ? static_cast<uint32_t>(__ldg(p.gt_mask + row)) : 0u;
       }
