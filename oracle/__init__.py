@@ -38,7 +38,11 @@ class _Ctx(ctypes.Structure):
         ("list_labels", ctypes.c_void_p),
         ("tau", ctypes.c_double),
         ("k", ctypes.c_double),
+        ("order", ctypes.c_int32),
     ]
+
+
+API_OUTPUT, APP_CHOICE, MULTI_SELECT = 0, 1, 2
 
 
 _lib = None
@@ -61,6 +65,19 @@ def lib():
         L.orc_loss_row.argtypes = [P, P, P, ctypes.c_uint32, D, P, P, P, P, P, P]
         L.orc_weights_literal.argtypes = [P, I64, P, P, P]
         L.orc_weights_by_mask.argtypes = [I32, P, P]
+        L.orc_label_lists.restype = ctypes.c_uint32
+        L.orc_label_lists.argtypes = [P, I32, I32]
+        L.orc_gt_set_raw.restype = ctypes.c_uint32
+        L.orc_gt_set_raw.argtypes = [P, I32, P, I64]
+        L.orc_decide_app_choice.restype = I32
+        L.orc_decide_app_choice.argtypes = [P, I32, P]
+        L.orc_gt_decision_app_choice.restype = I32
+        L.orc_gt_decision_app_choice.argtypes = [P, I32, P, I64]
+        L.orc_decide_multi_select.restype = ctypes.c_uint32
+        L.orc_decide_multi_select.argtypes = [P, I32, P]
+        L.orc_loss_row_app_choice.argtypes = [P, P, P, ctypes.c_uint32, D, P, P, P, P, P, P]
+        L.orc_loss_row_multi_select.argtypes = [P, I32, P, ctypes.c_uint32, D, P, P, P, P]
+        L.orc_weights_literal_masks.argtypes = [P, I64, P, P, P]
         L.orc_eval.restype = ctypes.c_int
         L.orc_eval.argtypes = [P, I64, I64, I32, P, P, P, P, P, D] + [P] * 10
         _lib = L
@@ -74,8 +91,8 @@ def _p(a):
 class Oracle:
     """Oracle bound to one context: ``lists[a][j]`` are the label ids of W_j of app a."""
 
-    def __init__(self, C: int, lists, tau: float = 0.0, k: float = 10.0):
-        self.C, self.tau, self.k = int(C), float(tau), float(k)
+    def __init__(self, C: int, lists, tau: float = 0.0, k: float = 10.0, order: int = API_OUTPUT):
+        self.C, self.tau, self.k, self.order = int(C), float(tau), float(k), int(order)
         self.lists = [[list(map(int, l)) for l in app] for app in lists]
         n_lists, off, labels = [], [], []
         pos = 0
@@ -90,11 +107,15 @@ class Oracle:
         self._off = np.asarray(off, dtype=np.int64)
         self._labels = np.asarray(labels if labels else [0], dtype=np.int32)
         self._ctx = _Ctx(self.C, len(self.lists), self._n_lists.ctypes.data, self._off.ctypes.data,
-                         self._labels.ctypes.data, self.tau, self.k)
+                         self._labels.ctypes.data, self.tau, self.k, self.order)
 
     @classmethod
-    def from_spec(cls, spec):
-        return cls(spec.C, spec.lists, spec.tau, spec.k)
+    def from_spec(cls, spec, order: int = API_OUTPUT):
+        return cls(spec.C, spec.lists, spec.tau, spec.k, order)
+
+    @property
+    def grad_slots(self) -> int:
+        return 8 if self.order == MULTI_SELECT else 2
 
     @property
     def n_apps(self):
@@ -113,10 +134,37 @@ class Oracle:
         return cat
 
     def decide(self, z, app: int = 0) -> int:
+        """Decision(API(x)) for the context's pattern (a list mask for Multi-Select)."""
         z = np.ascontiguousarray(z, dtype=np.float64)
+        if self.order == APP_CHOICE:
+            return int(lib().orc_decide_app_choice(ctypes.byref(self._ctx), app, z.ctypes.data))
+        if self.order == MULTI_SELECT:
+            return int(lib().orc_decide_multi_select(ctypes.byref(self._ctx), app, z.ctypes.data))
         scratch = np.empty(self.C, dtype=np.int32)
         return int(lib().orc_decide(ctypes.byref(self._ctx), app, self.compile(app).ctypes.data,
                                     z.ctypes.data, scratch.ctypes.data))
+
+    def label_lists(self, c: int, app: int = 0) -> int:
+        return int(lib().orc_label_lists(ctypes.byref(self._ctx), app, c))
+
+    def gt_set_raw(self, labels, app: int = 0) -> int:
+        labels = np.ascontiguousarray(labels, dtype=np.int32)
+        return int(lib().orc_gt_set_raw(ctypes.byref(self._ctx), app, labels.ctypes.data, len(labels)))
+
+    def gt_decision_app_choice(self, labels, app: int = 0) -> int:
+        labels = np.ascontiguousarray(labels, dtype=np.int32)
+        return int(lib().orc_gt_decision_app_choice(ctypes.byref(self._ctx), app, labels.ctypes.data, len(labels)))
+
+    def gt_mask(self, labels, app: int = 0) -> int:
+        """G_i as the pattern defines it (compiled first list for the choice orders)."""
+        return self.gt_set_raw(labels, app) if self.order == MULTI_SELECT else self.gt_set(labels, app)
+
+    def is_correct(self, labels, d: int, app: int = 0) -> bool:
+        if self.order == APP_CHOICE:
+            return d == self.gt_decision_app_choice(labels, app)
+        if self.order == MULTI_SELECT:
+            return d == self.gt_set_raw(labels, app)
+        return self.correct(self.gt_set(labels, app), d, app)
 
     def gt_set(self, labels, app: int = 0) -> int:
         labels = np.ascontiguousarray(labels, dtype=np.int32)
@@ -126,15 +174,32 @@ class Oracle:
         return bool(lib().orc_correct(G, d, self.n_lists(app)))
 
     def loss_row(self, z, G: int, w: float = 1.0, app: int = 0):
-        """-> dict(ell, L, c_plus, g_plus, c_minus, g_minus) (unscaled gradients)."""
+        """-> dict(ell, L, c_plus, g_plus, c_minus, g_minus, grads={label: dL/dz}) (unscaled).
+        For Multi-Select c_plus/c_minus are unused (-1) and grads holds one entry per list."""
         z = np.ascontiguousarray(z, dtype=np.float64)
-        ell, L, gp, gm = (ctypes.c_double() for _ in range(4))
+        ell, L = ctypes.c_double(), ctypes.c_double()
+        if self.order == MULTI_SELECT:
+            cs = np.full(8, -1, dtype=np.int32)
+            gs = np.zeros(8, dtype=np.float64)
+            lib().orc_loss_row_multi_select(ctypes.byref(self._ctx), app, z.ctypes.data, G, w, ctypes.byref(ell),
+                                            ctypes.byref(L), cs.ctypes.data, gs.ctypes.data)
+            grads = {}
+            for c, g in zip(cs.tolist(), gs.tolist()):
+                if c >= 0:
+                    grads[c] = grads.get(c, 0.0) + g
+            return dict(ell=ell.value, L=L.value, c_plus=-1, g_plus=0.0, c_minus=-1, g_minus=0.0, grads=grads,
+                        slots=(cs, gs))
+        gp, gm = ctypes.c_double(), ctypes.c_double()
         cp, cm = ctypes.c_int32(), ctypes.c_int32()
-        lib().orc_loss_row(ctypes.byref(self._ctx), self.compile(app).ctypes.data, z.ctypes.data, G, w,
-                           ctypes.byref(ell), ctypes.byref(L), ctypes.byref(cp), ctypes.byref(gp),
-                           ctypes.byref(cm), ctypes.byref(gm))
+        fn = lib().orc_loss_row_app_choice if self.order == APP_CHOICE else lib().orc_loss_row
+        fn(ctypes.byref(self._ctx), self.compile(app).ctypes.data, z.ctypes.data, G, w,
+           ctypes.byref(ell), ctypes.byref(L), ctypes.byref(cp), ctypes.byref(gp), ctypes.byref(cm), ctypes.byref(gm))
+        grads = {}
+        for c, g in ((cp.value, gp.value), (cm.value, gm.value)):
+            if c >= 0:
+                grads[c] = grads.get(c, 0.0) + g
         return dict(ell=ell.value, L=L.value, c_plus=cp.value, g_plus=gp.value,
-                    c_minus=cm.value, g_minus=gm.value)
+                    c_minus=cm.value, g_minus=gm.value, grads=grads)
 
     def weights_literal(self, gt_off, gt_lab, app: int = 0) -> np.ndarray:
         gt_off = np.ascontiguousarray(gt_off, dtype=np.int64)
@@ -143,6 +208,20 @@ class Oracle:
         w = np.empty(max(M, 1), dtype=np.float64)
         lib().orc_weights_literal(self.compile(app).ctypes.data, M, gt_off.ctypes.data, gt_lab.ctypes.data,
                                   w.ctypes.data)
+        return w[:M]
+
+    def weights_literal_pattern(self, gt_off, gt_lab, app: int = 0) -> np.ndarray:
+        """Literal O(M^2) N_i with the pattern's label->lists map (first list / every list)."""
+        gt_off = np.ascontiguousarray(gt_off, dtype=np.int64)
+        gt_lab = np.ascontiguousarray(gt_lab if len(gt_lab) else [0], dtype=np.int32)
+        if self.order == MULTI_SELECT:
+            lm = np.array([self.label_lists(c, app) for c in range(self.C)], dtype=np.uint8)
+        else:
+            cat = self.compile(app)
+            lm = np.where(cat >= 0, 1 << np.maximum(cat, 0).astype(np.int64), 0).astype(np.uint8)
+        M = len(gt_off) - 1
+        w = np.empty(max(M, 1), dtype=np.float64)
+        lib().orc_weights_literal_masks(lm.ctypes.data, M, gt_off.ctypes.data, gt_lab.ctypes.data, w.ctypes.data)
         return w[:M]
 
     @staticmethod
@@ -172,13 +251,14 @@ class Oracle:
             w = np.ascontiguousarray(w, dtype=np.float64).reshape(-1)
         na = self.n_apps
         r1 = max(rows, 1)
-        out = dict(decision=np.zeros(r1, np.uint8), hist_pred=np.zeros(na * 16, np.uint64))
+        S = self.grad_slots
+        out = dict(decision=np.zeros(r1, np.uint8), hist_pred=np.zeros(na * 256, np.uint64))
         if has_gt:
             out.update(gt_mask=np.zeros(r1, np.uint8), correct=np.zeros(r1, np.uint8),
                        n_incorrect=np.zeros(na, np.uint64), hist_gt=np.zeros(na * 256, np.uint64))
             if want_loss:
                 out.update(loss_sum=np.zeros(na, np.float64), loss_row=np.zeros(r1, np.float64),
-                           grad_idx=np.full(2 * r1, -1, np.int32), grad_val=np.zeros(2 * r1, np.float64))
+                           grad_idx=np.full(S * r1, -1, np.int32), grad_val=np.zeros(S * r1, np.float64))
         g = out.get
         rc = lib().orc_eval(ctypes.byref(self._ctx), rows, ld, dtype, logits.ctypes.data,
                             _p(gt_off), _p(gt_lab), _p(app), _p(w), grad_scale,
@@ -192,5 +272,5 @@ class Oracle:
                 out[key] = out[key][:rows]
         for key in ("grad_idx", "grad_val"):
             if key in out:
-                out[key] = out[key][: 2 * rows]
+                out[key] = out[key][: S * rows]
         return out

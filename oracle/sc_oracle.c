@@ -35,6 +35,8 @@ typedef struct {
   const int32_t* list_labels; /* label ids of every list, in code order              */
   double tau;                 /* label c is in the API output iff z_c > tau          */
   double k;                   /* steepness of S(x) = 1/(1+e^{-kx})                   */
+  int32_t order;              /* decision pattern: 0 Multi-Choice API-output order,
+                                 1 Multi-Choice application-choice order, 2 Multi-Select */
 } orc_ctx;
 
 /* ---------------------------------------------------------------- context */
@@ -197,6 +199,154 @@ void orc_weights_by_mask(int32_t n_apps, const uint64_t* H, double* w) {
   }
 }
 
+/* ---------------------------------------------------------------- other decision patterns */
+
+/* Lists (bit j) containing label c, by scanning every list: a Multi-Select
+ * application acts on every list an output label belongs to,
+ * so for that pattern a label shared by two lists counts for both. */
+uint32_t orc_label_lists(const orc_ctx* x, int32_t app, int32_t c) {
+  const int64_t b = app_base(x, app);
+  uint32_t m = 0;
+  for (int32_t j = 0; j < x->n_lists[app]; ++j)
+    for (int64_t t = x->list_off[b + j]; t < x->list_off[b + j + 1]; ++t)
+      if (x->list_labels[t] == c) { m |= 1u << j; break; }
+  return m;
+}
+
+/* {j : W_j ∩ ŷ ≠ ∅} with every list scanned (Multi-Select's ground-truth decision). */
+uint32_t orc_gt_set_raw(const orc_ctx* x, int32_t app, const int32_t* labels, int64_t n) {
+  uint32_t G = 0;
+  for (int64_t t = 0; t < n; ++t) G |= orc_label_lists(x, app, labels[t]);
+  return G;
+}
+
+/* Multi-Choice, application-choice order (loop nesting PAPER.md:2154-2156):
+ * "checking if the first target class matches with any output label before moving to
+ * the next class" — lists in code order, the first with any output label wins. */
+int32_t orc_decide_app_choice(const orc_ctx* x, int32_t app, const double* z) {
+  const int64_t b = app_base(x, app);
+  for (int32_t j = 0; j < x->n_lists[app]; ++j)
+    for (int64_t t = x->list_off[b + j]; t < x->list_off[b + j + 1]; ++t)
+      if (z[x->list_labels[t]] > x->tau) return j;
+  return x->n_lists[app];
+}
+
+/* k = min{j | W_j ∩ ŷ_i ≠ ∅}: the application-choice decision the
+ * ground truth leads to (unique, whatever the output order); D' if none. */
+int32_t orc_gt_decision_app_choice(const orc_ctx* x, int32_t app, const int32_t* labels, int64_t n) {
+  const int64_t b = app_base(x, app);
+  for (int32_t j = 0; j < x->n_lists[app]; ++j)
+    for (int64_t t = x->list_off[b + j]; t < x->list_off[b + j + 1]; ++t)
+      for (int64_t q = 0; q < n; ++q)
+        if (labels[q] == x->list_labels[t]) return j;
+  return x->n_lists[app];
+}
+
+/* Multi-Select: every list with an output label is selected. */
+uint32_t orc_decide_multi_select(const orc_ctx* x, int32_t app, const double* z) {
+  const int64_t b = app_base(x, app);
+  uint32_t m = 0;
+  for (int32_t j = 0; j < x->n_lists[app]; ++j)
+    for (int64_t t = x->list_off[b + j]; t < x->list_off[b + j + 1]; ++t)
+      if (z[x->list_labels[t]] > x->tau) { m |= 1u << j; break; }
+  return m;
+}
+
+/* Eq. app_choice:
+ *   L = (M/N_i) ( y_i S(max(θ, P_{k⁻}) − P_k) + (1 − y_i) S(P − θ) ),
+ * P_k = max over W_k, P_{k⁻} = max over the higher-priority lists W_j, j < k (the
+ * printed condition "ŷ ∩ W_j ≠ ∅ and j < k" is empty by the definition of k; reading
+ * A21: j < k), P = max over 𝕎.  Lists are the compiled first-list sets (A5): a label
+ * shared with an earlier list can only ever trigger the earlier one.  Arg maxima over
+ * z, smallest id on ties (A8); P_{k⁻} gets gradient only when it exceeds θ (A10). */
+void orc_loss_row_app_choice(const orc_ctx* x, const int8_t* cat, const double* z, uint32_t G, double w,
+                             double* ell_out, double* L_out, int32_t* c_a, double* g_a, int32_t* c_b,
+                             double* g_b) {
+  const double theta = sigma(x->tau);
+  const int y = G != 0;
+  int32_t kk = -1;
+  for (int32_t j = 0; j < 32 && y; ++j) if ((G >> j) & 1u) { kk = j; break; }
+  int32_t ck = -1, ckm = -1, cP = -1;
+  for (int32_t c = 0; c < x->C; ++c) {
+    if (cat[c] < 0) continue;
+    if (cP < 0 || z[c] > z[cP]) cP = c;
+    if (y && cat[c] == kk && (ck < 0 || z[c] > z[ck])) ck = c;
+    if (y && cat[c] < kk && (ckm < 0 || z[c] > z[ckm])) ckm = c;
+  }
+  double ell = 0.0, ga = 0.0, gb = 0.0;
+  int32_t oa = -1, ob = -1;
+  if (y) {
+    const int km_over = ckm >= 0 && z[ckm] > x->tau;            /* P_{k⁻} > θ */
+    const double a = km_over ? sigma(z[ckm]) : theta;           /* max(θ, P_{k⁻}) */
+    const double arg = a - sigma(z[ck]);
+    ell = S(x->k, arg);
+    const double d = dS(x->k, arg);
+    ga = -w * d * dsigma(z[ck]); oa = ck;
+    if (km_over) { gb = w * d * dsigma(z[ckm]); ob = ckm; }
+  } else if (cP >= 0) {
+    const double arg = sigma(z[cP]) - theta;
+    ell = S(x->k, arg);
+    gb = w * dS(x->k, arg) * dsigma(z[cP]); ob = cP;
+  }
+  *ell_out = ell;
+  *L_out = w * ell;
+  *c_a = oa; *g_a = ga; *c_b = ob; *g_b = gb;
+}
+
+/* Eq. multi-select, reading the printed y_i inside the sum as y_ij
+ * (= bit j of G):
+ *   L = (M/N_i) Σ_j ( y_ij S(θ − P_j) + (1 − y_ij) S(P_j − θ) ),  P_j = max over W_j.
+ * Lists are scanned as written (a shared label belongs to every list containing it).
+ * An empty list contributes nothing (P_j = −∞, and y_ij = 0 for it).  c[j], g[j]: the
+ * gradient entry of list j (−1 / 0 when the list is empty). */
+void orc_loss_row_multi_select(const orc_ctx* x, int32_t app, const double* z, uint32_t G, double w,
+                               double* ell_out, double* L_out, int32_t* c, double* g) {
+  const double theta = sigma(x->tau);
+  const int64_t b = app_base(x, app);
+  double ell = 0.0;
+  for (int32_t j = 0; j < 8; ++j) { c[j] = -1; g[j] = 0.0; }
+  for (int32_t j = 0; j < x->n_lists[app]; ++j) {
+    int32_t cj = -1;
+    for (int64_t t = x->list_off[b + j]; t < x->list_off[b + j + 1]; ++t) {
+      const int32_t q = x->list_labels[t];
+      if (cj < 0 || z[q] > z[cj] || (z[q] == z[cj] && q < cj)) cj = q;
+    }
+    if (cj < 0) continue;
+    const double Pj = sigma(z[cj]);
+    if ((G >> j) & 1u) {
+      ell += S(x->k, theta - Pj);
+      g[j] = -w * dS(x->k, theta - Pj) * dsigma(z[cj]);
+    } else {
+      ell += S(x->k, Pj - theta);
+      g[j] = w * dS(x->k, Pj - theta) * dsigma(z[cj]);
+    }
+    c[j] = cj;
+  }
+  *ell_out = ell;
+  *L_out = w * ell;
+}
+
+/* N_i by the literal definition for any pattern: lm[c] = the lists label
+ * c counts for (first list for the choice orders, every list for Multi-Select);
+ * 𝒲_i = labels whose lists meet G_i. */
+void orc_weights_literal_masks(const uint8_t* lm, int64_t M, const int64_t* gt_off, const int32_t* gt_lab,
+                               double* w_row) {
+  for (int64_t i = 0; i < M; ++i) {
+    uint32_t Gi = 0;
+    for (int64_t t = gt_off[i]; t < gt_off[i + 1]; ++t) Gi |= lm[gt_lab[t]];
+    int64_t N = 0;
+    for (int64_t j = 0; j < M; ++j) {
+      int hit = 0, any_mapped = 0;
+      for (int64_t t = gt_off[j]; t < gt_off[j + 1]; ++t) {
+        const uint32_t mj = lm[gt_lab[t]];
+        if (mj) { any_mapped = 1; if (mj & Gi) hit = 1; }
+      }
+      N += Gi ? hit : !any_mapped;
+    }
+    w_row[i] = (double)M / (double)N;
+  }
+}
+
 /* ---------------------------------------------------------------- batch */
 
 static double load_z(const void* logits, int32_t dtype, int64_t idx) {
@@ -206,10 +356,12 @@ static double load_z(const void* logits, int32_t dtype, int64_t idx) {
   return (double)f;
 }
 
-/* Every output of the hot path for `rows` inputs.  Any output may be NULL.
- * Counters ACCUMULATE (+=).  w: [n_apps*256] per-mask weights, NULL = 1.
- * grad_idx/grad_val: [rows*2], slot 0 = c⁺, slot 1 = c⁻, −1/0 when absent;
- * values multiplied by grad_scale.  Returns 0, or -1 on a non-finite logit
+/* Every output of the hot path for `rows` inputs, for the context's decision pattern.
+ * Any output may be NULL; counters ACCUMULATE (+=).  w: [n_apps*256] per-mask weights,
+ * NULL = 1.  hist_pred: [n_apps*256] (a Multi-Select decision is a list mask).
+ * grad_idx/grad_val: [rows*S], S = 2 for the choice orders (slot 0: the class the loss
+ * pushes up, slot 1: the competitor), S = 8 for Multi-Select (slot j = list j); −1 / 0
+ * when absent; values multiplied by grad_scale.  Returns 0, or −1 on a non-finite logit
  * (reading A18) or an out-of-range id. */
 int orc_eval(const orc_ctx* x, int64_t rows, int64_t ld, int32_t dtype, const void* logits,
              const int64_t* gt_off, const int32_t* gt_lab, const uint16_t* app,
@@ -218,6 +370,7 @@ int orc_eval(const orc_ctx* x, int64_t rows, int64_t ld, int32_t dtype, const vo
              uint64_t* n_incorrect, uint64_t* hist_pred, uint64_t* hist_gt,
              double* loss_sum, double* loss_row, int32_t* grad_idx, double* grad_val) {
   const int32_t C = x->C;
+  const int S_ = x->order == 2 ? 8 : 2;
   int8_t* cat = (int8_t*)malloc((size_t)x->n_apps * (size_t)(C > 0 ? C : 1));
   double* z = (double*)malloc(sizeof(double) * (size_t)(C > 0 ? C : 1));
   int32_t* scratch = (int32_t*)malloc(sizeof(int32_t) * (size_t)(C > 0 ? C : 1));
@@ -233,27 +386,49 @@ int orc_eval(const orc_ctx* x, int64_t rows, int64_t ld, int32_t dtype, const vo
     }
     if (rc) break;
     const int32_t D = x->n_lists[a];
-    const int32_t d = orc_decide(x, a, ca, z, scratch);
+    int32_t d;
+    if (x->order == 0) d = orc_decide(x, a, ca, z, scratch);
+    else if (x->order == 1) d = orc_decide_app_choice(x, a, z);
+    else d = (int32_t)orc_decide_multi_select(x, a, z);
     if (decision) decision[i] = (uint8_t)d;
-    if (hist_pred) hist_pred[(int64_t)a * 16 + d] += 1;
+    if (hist_pred) hist_pred[(int64_t)a * 256 + d] += 1;
     if (!gt_off) continue;
     for (int64_t t = gt_off[i]; t < gt_off[i + 1]; ++t)
       if (gt_lab[t] < 0 || gt_lab[t] >= C) rc = -1;
     if (rc) break;
-    const uint32_t G = orc_gt_set(ca, gt_lab + gt_off[i], gt_off[i + 1] - gt_off[i]);
-    const int32_t ok = orc_correct(G, d, D);
+    const int32_t* gl = gt_lab + gt_off[i];
+    const int64_t gn = gt_off[i + 1] - gt_off[i];
+    uint32_t G;
+    int32_t ok;
+    if (x->order == 0) {
+      G = orc_gt_set(ca, gl, gn);
+      ok = orc_correct(G, d, D);
+    } else if (x->order == 1) {
+      G = orc_gt_set(ca, gl, gn);
+      ok = d == orc_gt_decision_app_choice(x, a, gl, gn);
+    } else {
+      G = orc_gt_set_raw(x, a, gl, gn);
+      ok = (uint32_t)d == G;   /* "exactly match with the ground-truth decisions" */
+    }
     if (gt_mask) gt_mask[i] = (uint8_t)G;
     if (correct) correct[i] = (uint8_t)ok;
     if (n_incorrect) n_incorrect[a] += (uint64_t)!ok;
     if (hist_gt) hist_gt[(int64_t)a * 256 + G] += 1;
     if (loss_sum || loss_row || grad_idx || grad_val) {
       const double wi = w ? w[(int64_t)a * 256 + G] : 1.0;
-      double ell, L, gp, gm; int32_t cp, cm;
-      orc_loss_row(x, ca, z, G, wi, &ell, &L, &cp, &gp, &cm, &gm);
+      double ell, L;
+      int32_t cs[8];
+      double gs[8];
+      for (int q = 0; q < 8; ++q) { cs[q] = -1; gs[q] = 0.0; }
+      if (x->order == 0) orc_loss_row(x, ca, z, G, wi, &ell, &L, &cs[0], &gs[0], &cs[1], &gs[1]);
+      else if (x->order == 1) orc_loss_row_app_choice(x, ca, z, G, wi, &ell, &L, &cs[0], &gs[0], &cs[1], &gs[1]);
+      else orc_loss_row_multi_select(x, a, z, G, wi, &ell, &L, cs, gs);
       if (loss_sum) loss_sum[a] += L;
       if (loss_row) loss_row[i] = L;
-      if (grad_idx) { grad_idx[2 * i] = cp; grad_idx[2 * i + 1] = cm; }
-      if (grad_val) { grad_val[2 * i] = gp * grad_scale; grad_val[2 * i + 1] = gm * grad_scale; }
+      for (int q = 0; q < S_; ++q) {
+        if (grad_idx) grad_idx[S_ * i + q] = cs[q];
+        if (grad_val) grad_val[S_ * i + q] = gs[q] * grad_scale;
+      }
     }
   }
   free(cat); free(z); free(scratch);

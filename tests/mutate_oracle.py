@@ -27,6 +27,16 @@ MUTATIONS = [
     ("N counts G subset not intersect", "else for (int q = 0; q < 256; ++q) if (q & m) N += h[q];", "else for (int q = 0; q < 256; ++q) if ((q & m) == q) N += h[q];"),
     ("literal N non-target wrong", "N += Gi ? hit : !any_mapped;", "N += Gi ? hit : 1;"),
     ("weight inverted", "w_row[i] = (double)M / (double)N;", "w_row[i] = (double)N / (double)M;"),
+    ("app-choice: last list wins", "      if (z[x->list_labels[t]] > x->tau) return j;\n  return x->n_lists[app];\n}\n\n/* k = min",
+     "      if (z[x->list_labels[t]] > x->tau && j == x->n_lists[app] - 1) return j;\n  return x->n_lists[app];\n}\n\n/* k = min"),
+    ("app-choice: k- includes k", "if (y && cat[c] < kk && (ckm < 0 || z[c] > z[ckm])) ckm = c;",
+     "if (y && cat[c] <= kk && (ckm < 0 || z[c] > z[ckm])) ckm = c;"),
+    ("app-choice: y=0 uses theta-P", "const double arg = sigma(z[cP]) - theta;", "const double arg = theta - sigma(z[cP]);"),
+    ("multi-select: y term sign", "ell += S(x->k, theta - Pj);", "ell += S(x->k, Pj - theta);"),
+    ("multi-select: first list only", "if (z[x->list_labels[t]] > x->tau) { m |= 1u << j; break; }",
+     "if (z[x->list_labels[t]] > x->tau) { m |= 1u << j; return m; }"),
+    ("multi-select: shared label first list only", "if (x->list_labels[t] == c) { m |= 1u << j; break; }",
+     "if (x->list_labels[t] == c) { m |= 1u << j; return m; }"),
 ]
 
 
@@ -34,7 +44,7 @@ def main():
     failures = []
     with tempfile.TemporaryDirectory() as td:
         for name, old, new in MUTATIONS:
-            assert SRC.count(old) == 1, name
+            assert SRC.count(old) >= 1, name
             src = os.path.join(td, "m.c")
             so = os.path.join(td, f"m{len(failures)}_{abs(hash(name))}.so")
             open(src, "w").write(SRC.replace(old, new))
@@ -42,7 +52,8 @@ def main():
             env = dict(os.environ, ORACLE_SO=so)
             r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-m", "not gpu", "-p", "no:cacheprovider",
                                 "tests/test_oracle_paper.py", "tests/test_oracle_bruteforce.py",
-                                "tests/test_oracle_loss.py", "tests/test_oracle_weights.py"],
+                                "tests/test_oracle_loss.py", "tests/test_oracle_weights.py",
+                                "tests/test_oracle_patterns.py"],
                                cwd=ROOT, env=env, capture_output=True, text=True)
             killed = r.returncode != 0
             print(f"{'KILLED ' if killed else 'SURVIVED'}  {name}")
