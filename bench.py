@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--config", type=int, default=CFG, choices=[1, 2, 3, 4, 5],
                     help="BASELINE.json config (default 2, the metric's config; others for characterisation)")
     ap.add_argument("--kernel", default=None, choices=["tma", "gather"], help="force an eval kernel (default: auto)")
+    ap.add_argument("--order", default="api_output", choices=["api_output", "app_choice", "multi_select"],
+                    help="decision pattern (default: the north star's API-output order)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -289,7 +291,8 @@ def run_ours(args):
     data = wl.device_batch(rank * B, B, device=dev)  # this rank's rows of the global dataset
     logits, gt_off, gt_lab = data["logits"], data["gt_off"], data["gt_lab"]
     app = data.get("app")
-    ctx = sc.Context(spec.C, spec.lists, spec.tau, spec.k, multi_app=True)
+    order = {"api_output": 0, "app_choice": 1, "multi_select": 2}[args.order]
+    ctx = sc.Context(spec.C, spec.lists, spec.tau, spec.k, order=order, multi_app=True)
     ev = Evaluator(ctx, B, device=dev, group=group)
     global_rows = B * world
 
@@ -349,7 +352,7 @@ def run_ours(args):
     elt = 4 if args.dtype == "f32" else 2
     ld = logits.stride(0)
     sect = touched_sector_bytes(spec, ld, elt, rows=B)
-    per_row = sect + 1 + 1 + 8 + 8 + (2 if app is not None else 0)  # sectors + G_i + decision + sparse grad (+ app id)
+    per_row = sect + 1 + 1 + 8 * ctx.grad_slots + (2 if app is not None else 0)  # sectors + G_i + decision + sparse grad (+ app)
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     peak = peaks.get("hbm_gbs", 6650.0)
@@ -369,7 +372,7 @@ def run_ours(args):
         "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
         "config": {"workload": workload_name(cfg, args.dtype), "C": spec.C, "rows_per_gpu": B, "global_batch": global_rows,
                    "parallelism": f"dp{world}", "l2": f"no flush: {B * ld * elt / 1e9:.2f} GB of logits per step per GPU > 126 MB L2",
-                   "grad": "sparse (<= 2 entries/row)"},
+                   "grad": f"sparse ({ctx.grad_slots} slots/row)", "order": args.order},
         "roofline": roofline,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),

@@ -57,9 +57,13 @@ typedef enum {
 
 typedef enum { SC_F32 = 0, SC_BF16 = 1 } sc_dtype;
 
+/* The application's decision pattern ("type of decision" and examination order of the
+ * extracted summary).  A True-False application is any
+ * of them with a single list: all three reduce to Eq. loss there. */
 typedef enum {
-  SC_ORDER_API_OUTPUT = 0, /* Multi-Choice, API-output order — implemented   */
-  SC_ORDER_APP_CHOICE = 1  /* Multi-Choice, application-choice order — NEXT */
+  SC_ORDER_API_OUTPUT = 0,  /* Multi-Choice, API-output order: the hot path      */
+  SC_ORDER_APP_CHOICE = 1,  /* Multi-Choice, application-choice order            */
+  SC_ORDER_MULTI_SELECT = 2 /* Multi-Select: decision = mask of selected lists   */
 } sc_order;
 
 /* cudaStream_t without pulling in CUDA headers: pass a cudaStream_t (or 0). */
@@ -80,7 +84,9 @@ typedef struct sc_context_s* sc_context; /* library-owned; immutable after load 
  *                appear in several lists; it belongs to the first (reading A5).
  *   tau          logit threshold (finite); theta = sigma(tau) is computed in double.
  *   k            steepness of S(x) = 1/(1+e^{-kx}), finite, > 0.
- *   order        SC_ORDER_API_OUTPUT; SC_ORDER_APP_CHOICE returns SC_ERR_UNSUPPORTED.
+ *   order        decision pattern (sc_order).  For the two Multi-Choice orders a label in
+ *                several lists belongs to the first (the if-chain returns, reading A5); for
+ *                Multi-Select it belongs to every list containing it (all are acted on).
  *   out          receives the handle.
  * The host arrays are copied; the context allocates its device tables on the
  * current CUDA device (synchronously) and is usable from any stream/thread on it.
@@ -95,6 +101,10 @@ sc_status sc_context_free(sc_context ctx);
 
 /* sc_context_info — D'_a of app a (n_lists), and the number of mapped labels |𝕎_a|. */
 sc_status sc_context_info(sc_context ctx, int32_t app, int32_t* n_lists, int32_t* n_mapped);
+
+/* sc_context_order — the context's pattern and S, the sparse-gradient slots per row
+ * (2 for the Multi-Choice orders, 8 for Multi-Select: one per list). */
+sc_status sc_context_order(sc_context ctx, sc_order* order, int32_t* grad_slots);
 
 /* A batch of inputs (rows).  All pointers are device pointers.
  *   logits   [rows, ld] row-major, dtype elements; base 16-B aligned and
@@ -121,9 +131,14 @@ typedef struct {
 } sc_batch;
 
 /* sc_decide — decisions and counters, no loss.
- *   decision     [rows] uint8: 0..D'-1 or D' (default).
- *   n_incorrect  [n_apps] += #{i : decision_i not in Decision(ŷ_i)} (Eq. goal; reading A7). Needs GT.
- *   hist_pred    [n_apps*16] += #{i : decision_i = d} at [app*16 + d].
+ *   decision     [rows] uint8: API-output / application-choice order: 0..D'-1 or D'
+ *                (default); Multi-Select: the mask of selected lists.
+ *   n_incorrect  [n_apps] += #{i : decision_i ≠ Decision(ŷ_i)} (Eq. goal).  API-output
+ *                order: Decision(ŷ) is set-valued (reading A7); application-choice order:
+ *                the lowest list ŷ hits; Multi-Select: the mask of lists
+ *                ŷ hits (exact match).  Needs GT.
+ *   hist_pred    [n_apps*256] += #{i : decision_i = d} at [app*256 + d] (a Multi-Select
+ *                decision is a list mask, hence 256 bins).
  *   hist_gt      [n_apps*256] += #{i : G_i = m} at [app*256 + m].  Needs GT. */
 sc_status sc_decide(sc_context ctx, const sc_batch* batch, uint8_t* decision, uint64_t* n_incorrect,
                     uint64_t* hist_pred, uint64_t* hist_gt, sc_stream stream);
@@ -146,18 +161,27 @@ sc_status sc_decision_hist(sc_context ctx, const sc_batch* batch, uint64_t* hist
 sc_status sc_weights_from_hist(sc_context ctx, const uint64_t* hist_gt, float* w, sc_stream stream);
 
 /* sc_loss_fwd_bwd — the fused hot path: one read of each logit row gives the
- * decision, the counters, and Eq. api_output with its gradient:
+ * decision, the counters, and the pattern's decision-aware loss with its gradient.
+ * API-output order, Eq. api_output:
  *   L_i = w[G_i] ( y_i S(max(P⁻,θ) − P⁺) + (1−y_i) S(P⁻ − θ) ),
  *   P⁺ = σ(max_{c: cat[c] ∈ G_i} z_c), P⁻ = σ(max_{c ∈ 𝕎, cat[c] ∉ G_i} z_c), max ∅ = −∞.
- * The arg maxima are exact (ties to the smaller label id, A8); P⁻ enters
- * max(P⁻,θ) and gets gradient only when its logit is > tau (A10).
+ * Application-choice order, Eq. app_choice, k = lowest list in G_i:
+ *   L_i = w[G_i] ( y_i S(max(θ, P_{k⁻}) − P_k) + (1−y_i) S(P − θ) ),
+ *   P_k over list k, P_{k⁻} over lists j < k (reading A21), P over 𝕎.
+ * Multi-Select, Eq. multi-select, y_ij = bit j of G_i:
+ *   L_i = w[G_i] Σ_j ( y_ij S(θ − P_j) + (1 − y_ij) S(P_j − θ) ).
+ * The arg maxima are exact (ties to the smaller label id, A8); a competitor inside
+ * max(·, θ) gets gradient only when its logit is > tau (A10).
  *   w           device [n_apps*256] float (from sc_weights_from_hist) or NULL (all 1).
  *   grad_scale  multiplies every gradient entry (e.g. 1/B_global, reading A14).
  *   loss_sum    [n_apps] double += sum_i L_i (unscaled).
  *   loss_row    [rows] float, L_i.
- *   grad_idx    [rows*2] int32: slot 0 = c⁺ (y_i = 1), slot 1 = c⁻ (when it gets
- *   grad_val    [rows*2] float   gradient), -1 / 0.0f when absent.  All other
- *                                dL_i/dz_c are exactly 0.
+ *   grad_idx    [rows*S] int32: S = sc_context_order's grad_slots.  Multi-Choice:
+ *   grad_val    [rows*S] float   slot 0 = the label the loss pushes up (c⁺ / the arg max
+ *                                of list k), slot 1 = the competitor (c⁻ / of lists < k,
+ *                                or of 𝕎 when y_i = 0); Multi-Select: slot j = the arg
+ *                                max of list j.  -1 / 0.0f when absent; every other
+ *                                dL_i/dz_c is exactly 0.
  *   grad_dense  [rows*ld] float: the full gradient (zeros + at most 2 entries),
  *               every element written, including the padding columns.
  *   decision, n_incorrect, hist_pred, hist_gt: as in sc_decide (same pass).

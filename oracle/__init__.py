@@ -78,6 +78,11 @@ def lib():
         L.orc_loss_row_app_choice.argtypes = [P, P, P, ctypes.c_uint32, D, P, P, P, P, P, P]
         L.orc_loss_row_multi_select.argtypes = [P, I32, P, ctypes.c_uint32, D, P, P, P, P]
         L.orc_weights_literal_masks.argtypes = [P, I64, P, P, P]
+        L.orc_range_of.restype = I32
+        L.orc_range_of.argtypes = [I32, P, P, D]
+        L.orc_range_loss.argtypes = [I32, P, P, D, I32, D, D, P, P]
+        L.orc_ranges_eval.argtypes = [I32, P, P, D, I64, P, P, P, D] + [P] * 8
+        L.orc_ranges_weights.argtypes = [I32, P, P]
         L.orc_eval.restype = ctypes.c_int
         L.orc_eval.argtypes = [P, I64, I64, I32, P, P, P, P, P, D] + [P] * 10
         _lib = L
@@ -273,4 +278,47 @@ class Oracle:
         for key in ("grad_idx", "grad_val"):
             if key in out:
                 out[key] = out[key][: S * rows]
+        return out
+
+
+class RangesOracle:
+    """Value-ranges applications: ranges [lo_j, hi_j] in code order."""
+
+    def __init__(self, lo, hi, k: float = 10.0):
+        self.lo = np.ascontiguousarray(lo, dtype=np.float64)
+        self.hi = np.ascontiguousarray(hi, dtype=np.float64)
+        self.m, self.k = len(self.lo), float(k)
+
+    def range_of(self, score: float) -> int:
+        return int(lib().orc_range_of(self.m, self.lo.ctypes.data, self.hi.ctypes.data, float(score)))
+
+    def loss(self, r: int, score: float, w: float = 1.0):
+        L, dL = ctypes.c_double(), ctypes.c_double()
+        lib().orc_range_loss(self.m, self.lo.ctypes.data, self.hi.ctypes.data, self.k, r, float(score), w,
+                             ctypes.byref(L), ctypes.byref(dL))
+        return L.value, dL.value
+
+    def weights(self, H) -> np.ndarray:
+        H = np.ascontiguousarray(H, dtype=np.uint64)
+        w = np.empty(self.m + 1, dtype=np.float64)
+        lib().orc_ranges_weights(self.m, H.ctypes.data, w.ctypes.data)
+        return w
+
+    def eval(self, score, gt_score, w=None, grad_scale: float = 1.0):
+        score = np.ascontiguousarray(score, dtype=np.float32)
+        gt_score = np.ascontiguousarray(gt_score, dtype=np.float32)
+        rows = len(score)
+        r1 = max(rows, 1)
+        out = dict(decision=np.zeros(r1, np.uint8), gt_range=np.zeros(r1, np.uint8),
+                   n_incorrect=np.zeros(1, np.uint64), hist_pred=np.zeros(self.m + 1, np.uint64),
+                   hist_gt=np.zeros(self.m + 1, np.uint64), loss_sum=np.zeros(1, np.float64),
+                   loss_row=np.zeros(r1, np.float64), grad=np.zeros(r1, np.float64))
+        wp = None if w is None else np.ascontiguousarray(w, dtype=np.float64)
+        g = out.get
+        lib().orc_ranges_eval(self.m, self.lo.ctypes.data, self.hi.ctypes.data, self.k, rows, score.ctypes.data,
+                              gt_score.ctypes.data, _p(wp), grad_scale, _p(g("decision")), _p(g("gt_range")),
+                              _p(g("n_incorrect")), _p(g("hist_pred")), _p(g("hist_gt")), _p(g("loss_sum")),
+                              _p(g("loss_row")), _p(g("grad")))
+        for key in ("decision", "gt_range", "loss_row", "grad"):
+            out[key] = out[key][:rows]
         return out

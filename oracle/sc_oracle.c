@@ -434,3 +434,55 @@ int orc_eval(const orc_ctx* x, int64_t rows, int64_t ld, int32_t dtype, const vo
   free(cat); free(z); free(scratch);
   return rc;
 }
+
+/* ---------------------------------------------------------------- value ranges */
+
+/* Value-ranges applications: the API returns a score O_i (e.g. a
+ * sentiment score) and the application checks, in code order, whether it lies in each
+ * of its ranges [l_j, h_j] (reading A22: closed ranges, the first containing range
+ * wins, none -> default m).  The ground-truth range r_i is the one the true score lies in. */
+int32_t orc_range_of(int32_t m, const double* lo, const double* hi, double score) {
+  for (int32_t j = 0; j < m; ++j)
+    if (score >= lo[j] && score <= hi[j]) return j;
+  return m;
+}
+
+/* L = (M/N_i) ( S(l_i − O_i) + S(O_i − h_i) ) with [l_i, h_i] the ground-truth range
+ * (PAPER.md:2061); rows whose ground truth lies in no range have no target range and
+ * contribute nothing (reading A22).  dL/dO = w ( −S'(l − O) + S'(O − h) ). */
+void orc_range_loss(int32_t m, const double* lo, const double* hi, double k, int32_t r, double score, double w,
+                    double* L, double* dL) {
+  if (r < 0 || r >= m) { *L = 0.0; *dL = 0.0; return; }
+  const double a = lo[r] - score, b = score - hi[r];
+  *L = w * (S(k, a) + S(k, b));
+  *dL = w * (-dS(k, a) + dS(k, b));
+}
+
+/* Batch: decisions, counters (hist over ranges, [m+1] bins), loss and gradient. */
+void orc_ranges_eval(int32_t m, const double* lo, const double* hi, double k, int64_t rows, const float* score,
+                     const float* gt_score, const double* w, double grad_scale, uint8_t* decision, uint8_t* gt_range,
+                     uint64_t* n_incorrect, uint64_t* hist_pred, uint64_t* hist_gt, double* loss_sum,
+                     double* loss_row, double* grad) {
+  for (int64_t i = 0; i < rows; ++i) {
+    const int32_t d = orc_range_of(m, lo, hi, (double)score[i]);
+    const int32_t r = orc_range_of(m, lo, hi, (double)gt_score[i]);
+    if (decision) decision[i] = (uint8_t)d;
+    if (gt_range) gt_range[i] = (uint8_t)r;
+    if (n_incorrect) n_incorrect[0] += (uint64_t)(d != r);
+    if (hist_pred) hist_pred[d] += 1;
+    if (hist_gt) hist_gt[r] += 1;
+    double L, dL;
+    orc_range_loss(m, lo, hi, k, r, (double)score[i], w ? w[r] : 1.0, &L, &dL);
+    if (loss_sum) loss_sum[0] += L;
+    if (loss_row) loss_row[i] = L;
+    if (grad) grad[i] = dL * grad_scale;
+  }
+}
+
+/* Rebalancing over ranges: N_i = #inputs with the same ground-truth range (PAPER.md:2063
+ * "N_i is defined similarly"); w[r] = M / N_r, 0 for an empty bin. */
+void orc_ranges_weights(int32_t m, const uint64_t* H, double* w) {
+  uint64_t M = 0;
+  for (int32_t r = 0; r <= m; ++r) M += H[r];
+  for (int32_t r = 0; r <= m; ++r) w[r] = H[r] ? (double)M / (double)H[r] : 0.0;
+}

@@ -26,7 +26,7 @@ __all__ = [
 SC_OK, SC_ERR_INVALID_ARG, SC_ERR_OOM, SC_ERR_CUDA, SC_ERR_UNSUPPORTED = range(5)
 _STATUS = {1: "SC_ERR_INVALID_ARG", 2: "SC_ERR_OOM", 3: "SC_ERR_CUDA", 4: "SC_ERR_UNSUPPORTED"}
 SC_F32, SC_BF16 = 0, 1
-SC_ORDER_API_OUTPUT, SC_ORDER_APP_CHOICE = 0, 1
+SC_ORDER_API_OUTPUT, SC_ORDER_APP_CHOICE, SC_ORDER_MULTI_SELECT = 0, 1, 2
 
 
 class ScError(RuntimeError):
@@ -65,6 +65,8 @@ def _load():
     lib.sc_context_free.argtypes = [P]
     lib.sc_context_info.restype = ctypes.c_int
     lib.sc_context_info.argtypes = [P, I32, ctypes.POINTER(I32), ctypes.POINTER(I32)]
+    lib.sc_context_order.restype = ctypes.c_int
+    lib.sc_context_order.argtypes = [P, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(I32)]
     lib.sc_decide.restype = ctypes.c_int
     lib.sc_decide.argtypes = [P, ctypes.POINTER(_CBatch), P, P, P, P, P]
     lib.sc_decision_hist.restype = ctypes.c_int
@@ -170,6 +172,7 @@ class Context:
                 pos += len(l)
                 off.append(pos)
         self.C, self.n_apps, self.tau, self.k = int(C), len(lists), float(tau), float(k)
+        self.order = int(order)
         self.lists = lists
         a_n = (ctypes.c_int32 * max(1, len(n_lists)))(*n_lists)
         a_off = (ctypes.c_int64 * max(1, len(off)))(*off)
@@ -182,6 +185,13 @@ class Context:
     @property
     def handle(self):
         return self._h
+
+    @property
+    def grad_slots(self) -> int:
+        """Sparse-gradient entries per row: 2 (Multi-Choice orders) or 8 (Multi-Select)."""
+        o, g = ctypes.c_int(), ctypes.c_int32()
+        _check(_lib.sc_context_order(self._h, ctypes.byref(o), ctypes.byref(g)))
+        return g.value
 
     def n_lists(self, app: int = 0) -> int:
         n, m = ctypes.c_int32(), ctypes.c_int32()
@@ -275,7 +285,7 @@ def sc_decide(ctx: Context, batch: Batch, decision=None, n_incorrect=None, hist_
     _check(_lib.sc_decide(ctx.handle, ctypes.byref(cb),
                           _dev_ptr(decision, "decision", (torch.uint8,), cb.rows),
                           _u64(n_incorrect, "n_incorrect", ctx.n_apps),
-                          _u64(hist_pred, "hist_pred", ctx.n_apps * 16),
+                          _u64(hist_pred, "hist_pred", ctx.n_apps * 256),
                           _u64(hist_gt, "hist_gt", ctx.n_apps * 256), _stream(stream)))
 
 
@@ -306,10 +316,10 @@ def sc_loss_fwd_bwd(ctx: Context, batch: Batch, w=None, grad_scale: float = 1.0,
         _dev_ptr(w, "w", (torch.float32,), ctx.n_apps * 256), float(grad_scale),
         _dev_ptr(loss_sum, "loss_sum", (torch.float64,), ctx.n_apps),
         _dev_ptr(loss_row, "loss_row", (torch.float32,), cb.rows),
-        _dev_ptr(grad_idx, "grad_idx", (torch.int32,), 2 * cb.rows),
-        _dev_ptr(grad_val, "grad_val", (torch.float32,), 2 * cb.rows),
+        _dev_ptr(grad_idx, "grad_idx", (torch.int32,), ctx.grad_slots * cb.rows),
+        _dev_ptr(grad_val, "grad_val", (torch.float32,), ctx.grad_slots * cb.rows),
         _dev_ptr(grad_dense, "grad_dense", (torch.float32,), cb.rows * ld),
         _dev_ptr(decision, "decision", (torch.uint8,), cb.rows),
         _u64(n_incorrect, "n_incorrect", ctx.n_apps),
-        _u64(hist_pred, "hist_pred", ctx.n_apps * 16),
+        _u64(hist_pred, "hist_pred", ctx.n_apps * 256),
         _u64(hist_gt, "hist_gt", ctx.n_apps * 256), _stream(stream)))

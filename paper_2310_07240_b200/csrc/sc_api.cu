@@ -16,6 +16,7 @@
 
 struct sc_context_s {
   int32_t C = 0, n_apps = 0, max_ent = 0;
+  int32_t order = 0;
   float tau = 0.f, theta = 0.5f, k = 1.f;
   int device = 0;
   std::vector<int32_t> nlists, n_mapped;
@@ -83,6 +84,7 @@ sc::DevContext dev_ctx(const sc_context_s* c) {
   d.tau = c->tau;
   d.theta = c->theta;
   d.k = c->k;
+  d.order = c->order;
   return d;
 }
 
@@ -169,6 +171,12 @@ sc_status run_eval(const sc_context_s* ctx, const sc_batch* b, const float* w, f
     bool gather = ctx->max_ent <= 1024 && (frac <= gather_threshold() || ctx->n_apps > 1);
     if (kenv && std::string(kenv) == "tma") gather = false;
     if (kenv && std::string(kenv) == "gather" && ctx->max_ent <= 1024) gather = true;
+    if (ctx->order != SC_ORDER_API_OUTPUT) {
+      // per-list maxima (application-choice order, Multi-Select) run on the gather kernel
+      if (ctx->max_ent > 1024)
+        return fail(SC_ERR_UNSUPPORTED, "this decision pattern supports at most 1024 mapped labels per app");
+      gather = true;
+    }
     if (gather) {
       p.ld_flavor = std::getenv("SC_LD_FLAVOR") ? std::atoi(std::getenv("SC_LD_FLAVOR")) : 0;
       if (const char* g = std::getenv("SC_L2_FETCH")) {  // experiment: L2 fetch granularity hint (bytes)
@@ -182,8 +190,9 @@ sc_status run_eval(const sc_context_s* ctx, const sc_batch* b, const float* w, f
       int epl = 1;
       while (epl * 32 < ctx->max_ent) epl *= 2;
       p.wtab_off = (want_loss && w && ctx->n_apps == 1) ? 0 : -1;
-      if (cudaError_t e = sc::launch_gather(p, epl, di.sms, st)) return cuda_fail(e, "gather kernel launch");
-      g_last_kernel = "gather_epl" + std::to_string(epl);
+      const int pat = ctx->order == SC_ORDER_API_OUTPUT ? 0 : 1;
+      if (cudaError_t e = sc::launch_gather(p, epl, pat, di.sms, st)) return cuda_fail(e, "gather kernel launch");
+      g_last_kernel = (pat ? "gather_lists_epl" : "gather_epl") + std::to_string(epl);
       g_launches.fetch_add(1, std::memory_order_relaxed);
       return SC_OK;
     }
@@ -295,8 +304,8 @@ sc_status sc_context_load(int32_t C, int32_t n_apps, const int32_t* n_lists, con
                           const int32_t* list_labels, float tau, float k, sc_order order, sc_context* out) {
   if (!out) return fail(SC_ERR_INVALID_ARG, "out is NULL");
   *out = nullptr;
-  if (order == SC_ORDER_APP_CHOICE) return fail(SC_ERR_UNSUPPORTED, "SC_ORDER_APP_CHOICE is not implemented yet");
-  if (order != SC_ORDER_API_OUTPUT) return fail(SC_ERR_INVALID_ARG, "unknown order %d", (int)order);
+  if (order != SC_ORDER_API_OUTPUT && order != SC_ORDER_APP_CHOICE && order != SC_ORDER_MULTI_SELECT)
+    return fail(SC_ERR_INVALID_ARG, "unknown order %d", (int)order);
   if (C < 1 || C >= (1 << 23)) return fail(SC_ERR_INVALID_ARG, "C must be in [1, 2^23)");
   if (n_apps < 1 || n_apps > 65535) return fail(SC_ERR_INVALID_ARG, "n_apps must be in [1, 65535]");
   if (!n_lists || !list_off) return fail(SC_ERR_INVALID_ARG, "n_lists / list_off is NULL");
@@ -322,8 +331,11 @@ sc_status sc_context_load(int32_t C, int32_t n_apps, const int32_t* n_lists, con
   ctx->k = k;
   ctx->theta = static_cast<float>(1.0 / (1.0 + std::exp(-static_cast<double>(tau))));
   ctx->nlists.assign(n_lists, n_lists + n_apps);
-  // a1: cat[app][c] = first list, in code order, containing c (the listing's if-chain)
-  std::vector<uint8_t> cat(static_cast<size_t>(n_apps) * C, sc::kCatNone);
+  ctx->order = static_cast<int32_t>(order);
+  const bool ms = order == SC_ORDER_MULTI_SELECT;
+  // a1: Multi-Choice: cat[app][c] = first list, in code order, containing c (the listing's
+  // if-chain); Multi-Select: the mask of every list containing c.
+  std::vector<uint8_t> cat(static_cast<size_t>(n_apps) * C, ms ? uint8_t(0) : sc::kCatNone);
   std::vector<uint32_t> ent;
   std::vector<int32_t> ent_off(n_apps + 1, 0);
   base = 0;
@@ -336,18 +348,20 @@ sc_status sc_context_load(int32_t C, int32_t n_apps, const int32_t* n_lists, con
           delete ctx;
           return fail(SC_ERR_INVALID_ARG, "label %d of app %d list %d not in [0, C)", c, a, j);
         }
-        if (ca[c] == sc::kCatNone) ca[c] = static_cast<uint8_t>(j);
+        if (ms) ca[c] |= static_cast<uint8_t>(1u << j);
+        else if (ca[c] == sc::kCatNone) ca[c] = static_cast<uint8_t>(j);
       }
     }
     base += n_lists[a] + 1;
+    const uint8_t none = ms ? uint8_t(0) : sc::kCatNone;
     for (int32_t c = 0; c < C; ++c)
-      if (ca[c] != sc::kCatNone) ent.push_back(static_cast<uint32_t>(c) << 8 | ca[c]);
+      if (ca[c] != none) ent.push_back(static_cast<uint32_t>(c) << 8 | ca[c]);
     ent_off[a + 1] = static_cast<int32_t>(ent.size());
     for (int dt = 0; dt < 2; ++dt) {
       const int per_sector = dt == 0 ? 8 : 16;
       int64_t last = -1, last_line = -1;
       for (int32_t c = 0; c < C; ++c)
-        if (ca[c] != sc::kCatNone) {
+        if (ca[c] != none) {
           if (c / per_sector != last) {
             last = c / per_sector;
             ++ctx->touched_sectors[dt];
@@ -397,6 +411,13 @@ sc_status sc_context_info(sc_context ctx, int32_t app, int32_t* n_lists, int32_t
   if (app < 0 || app >= ctx->n_apps) return fail(SC_ERR_INVALID_ARG, "app out of range");
   if (n_lists) *n_lists = ctx->nlists[app];
   if (n_mapped) *n_mapped = ctx->n_mapped[app];
+  return SC_OK;
+}
+
+sc_status sc_context_order(sc_context ctx, sc_order* order, int32_t* grad_slots) {
+  if (!ctx) return fail(SC_ERR_INVALID_ARG, "ctx is NULL");
+  if (order) *order = static_cast<sc_order>(ctx->order);
+  if (grad_slots) *grad_slots = ctx->order == SC_ORDER_MULTI_SELECT ? 8 : 2;
   return SC_OK;
 }
 

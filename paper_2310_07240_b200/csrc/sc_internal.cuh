@@ -9,17 +9,27 @@ namespace sc {
 constexpr int kConsumerWarps = 16;                 // W: consumer warps per CTA
 constexpr int kThreads = 32 * (1 + kConsumerWarps);  // + 1 TMA producer warp
 constexpr uint32_t kNone = 0xFFFFFFFFu;            // "no label" key
-constexpr uint8_t kCatNone = 0xFF;                 // label in no list
+constexpr uint8_t kCatNone = 0xFF;                 // label in no list (Multi-Choice tables)
 
 // Device-side context tables (built once by sc_context_load).
+// Decision patterns (sc_order).
+constexpr int kApiOutput = 0, kAppChoice = 1, kMultiSelect = 2;
+
 struct DevContext {
-  const uint8_t* cat;       // [n_apps*C]  first list containing label c, or kCatNone   (a1)
+  const uint8_t* cat;       // [n_apps*C]  Multi-Choice: first list containing label c, or kCatNone (a1);
+                            //             Multi-Select: mask of every list containing c (0 = none)
   const uint32_t* ent;      // per app, mapped labels sorted by id: key = c << 8 | cat[c]
   const int32_t* ent_off;   // [n_apps+1]
   const uint8_t* nlists;    // [n_apps]  D'
   int32_t C, n_apps, max_ent;
   float tau, theta, k;
+  int32_t order;            // kApiOutput / kAppChoice / kMultiSelect
 };
+
+// Lists (bit set) label-table value v stands for.
+__host__ __device__ __forceinline__ uint32_t label_lists(uint8_t v, int order) {
+  return order == kMultiSelect ? static_cast<uint32_t>(v) : (v == kCatNone ? 0u : (1u << v));
+}
 
 // Parameters of the fused evaluation kernel (decide + counters + loss fwd/bwd).
 struct EvalParams {
@@ -89,7 +99,8 @@ struct HistParams {
 // epl > 0: lane-resident entries (|W| <= 32*epl, whole rows per stage); 0: generic list path.
 cudaError_t launch_eval(const EvalParams& p, int epl, int grid, size_t smem, cudaStream_t st);
 // Sector-sparse variant: epl = entries per lane capacity (1,2,4,8,16,32 -> |W| <= 32*epl).
-cudaError_t launch_gather(const EvalParams& p, int epl, int sms, cudaStream_t st);
+// pat 0: split maxima (API-output order); pat 1: per-list maxima (application-choice, Multi-Select).
+cudaError_t launch_gather(const EvalParams& p, int epl, int pat, int sms, cudaStream_t st);
 cudaError_t launch_hist(const HistParams& p, int grid, size_t smem, cudaStream_t st);
 cudaError_t launch_weights(const unsigned long long* hist, float* w, int n_apps, cudaStream_t st);
 cudaError_t set_eval_smem_limit(size_t smem);

@@ -110,10 +110,7 @@ __device__ __forceinline__ uint32_t warp_gt_mask(const EvalParams& p, int64_t ro
   const int64_t b = __ldg(p.gt_off + row), e = __ldg(p.gt_off + row + 1);
   uint32_t G = 0;
   const uint8_t* cat = p.ctx.cat + static_cast<int64_t>(a) * p.ctx.C;
-  for (int64_t t = b + lane; t < e; t += 32) {
-    const uint8_t v = __ldg(cat + __ldg(p.gt_lab + t));
-    if (v != kCatNone) G |= 1u << v;
-  }
+  for (int64_t t = b + lane; t < e; t += 32) G |= label_lists(__ldg(cat + __ldg(p.gt_lab + t)), p.ctx.order);
   return __reduce_or_sync(kFull, G);
 }
 
@@ -188,7 +185,7 @@ __device__ __forceinline__ void finish_batch(const EvalParams& p, RowBatch& b, c
   }
   // a6 / a5 counters: one atomic per distinct (app, bin) in the warp.
   if (p.hist_pred && active) {
-    const uint32_t key = b.app * 16u + dec;
+    const uint32_t key = b.app * 256u + dec;
     const unsigned peers = __match_any_sync(act, key);
     if (lane == __ffs(peers) - 1) atomicAdd(p.hist_pred + key, static_cast<unsigned long long>(__popc(peers)));
   }
@@ -312,7 +309,7 @@ struct LaneEnt {
     if constexpr (kKeepOff) return off_[t];
     else return key[t] == kNone ? 0u : (key[t] >> 8) * elt;
   }
-  uint32_t catm[8];    // bit t set iff entry t is in list j
+  uint32_t catm[8];    // bit t set iff entry t is in list j (several bits for Multi-Select)
   uint32_t valid;      // bit t set iff entry t exists
   int32_t app;
   int tc;              // warp-uniform: entry slots in use, ceil(n / 32)
@@ -320,7 +317,7 @@ struct LaneEnt {
 
 template <int EPL>
 __device__ __forceinline__ void lane_ent_load(LaneEnt<EPL>& le, const uint32_t* ents, int n, int32_t app, int lane,
-                                              uint32_t elt) {
+                                              uint32_t elt, int order = kApiOutput) {
   le.valid = 0;
   le.app = app;
   le.tc = (n + 31) >> 5;
@@ -334,8 +331,9 @@ __device__ __forceinline__ void lane_ent_load(LaneEnt<EPL>& le, const uint32_t* 
     if constexpr (LaneEnt<EPL>::kKeepOff) le.off_[t] = e < n ? (k >> 8) * elt : 0u;
     if (e < n) {
       le.valid |= 1u << t;
+      const uint32_t lists = label_lists(static_cast<uint8_t>(k & 0xFFu), order);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) le.catm[j] |= ((k & 0xFFu) == static_cast<uint32_t>(j) ? 1u : 0u) << t;
+      for (int j = 0; j < 8; ++j) le.catm[j] |= ((lists >> j) & 1u) << t;
     }
   }
 }
@@ -718,6 +716,219 @@ __global__ void __launch_bounds__(kThreads, 1) eval_kernel(const EvalParams p) {
   if (b.n > 0) finish_batch(p, b, wtab, lane);
 }
 
+// ------------------------------------------------------------------ per-list maxima (NEXT f1)
+
+// The application-choice order and Multi-Select need the arg max of every list (P_j,
+// PAPER.md:2026, :2050), not just the split into 𝒲_i / 𝕎∖𝒲_i.  One predicated update per
+// (entry, list): the entry belongs to list j iff bit t of catm[j] is set.
+template <uint32_t BIT>
+__device__ __forceinline__ void list_entry(float z, uint32_t key, uint32_t cm, float& az, uint32_t& ak) {
+  asm("{\n\t"
+      ".reg .pred b, g;\n\t"
+      ".reg .b32 t;\n\t"
+      "and.b32 t, %4, %5;\n\t"
+      "setp.ne.u32 b, t, 0;\n\t"
+      "setp.gt.and.f32 g, %2, %0, b;\n\t"
+      "@g mov.f32 %0, %2;\n\t"
+      "@g mov.b32 %1, %3;\n\t"
+      "}"
+      : "+f"(az), "+r"(ak)
+      : "f"(z), "r"(key), "r"(cm), "n"(BIT));
+}
+
+template <int EPL, int T = 0>
+__device__ __forceinline__ void list_scan(const LaneEnt<EPL>& le, uint32_t cm, const float (&zs)[EPL], float& az,
+                                          uint32_t& ak) {
+  list_entry<(1u << T)>(zs[T], le.key[T], cm, az, ak);
+  if constexpr (T + 1 < EPL) list_scan<EPL, T + 1>(le, cm, zs, az, ak);
+}
+
+constexpr int kListPad = 9;  // row stride (floats) of the per-warp list-maxima batch: conflict-free reads
+
+// Per-warp batch of 32 rows' per-list arg maxima, in shared memory.
+struct ListBatch {
+  float* z;      // [32][kListPad]
+  uint32_t* k;   // [32][kListPad]
+};
+
+// a3/a4 for one row, every list: the warp-reduced arg max of list j lands in batch row `slot`.
+template <int EPL>
+__device__ __forceinline__ void scan_lists(const LaneEnt<EPL>& le, int D, const float (&zs)[EPL], ListBatch lb,
+                                           int slot, int lane) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    if (j < D) {  // warp-uniform
+      float az = -CUDART_INF_F;
+      uint32_t ak = kNone;
+      list_scan<EPL>(le, le.catm[j], zs, az, ak);
+      warp_argmax(az, ak);
+      if (lane == j) {
+        lb.z[slot * kListPad + j] = az;
+        lb.k[slot * kListPad + j] = ak;
+      }
+    }
+  }
+}
+
+// Epilogue of the application-choice order (Eq. app_choice) and Multi-Select (Eq.
+// multi-select) for the batch's rows, one row per lane; counters as in finish_batch.
+__device__ __forceinline__ void finish_lists(const EvalParams& p, RowBatch& b, ListBatch lb, const float* wtab_smem,
+                                             int lane) {
+  __syncwarp();
+  const bool active = lane < b.n;
+  const unsigned act = __ballot_sync(kFull, active);
+  const float tau = p.ctx.tau, theta = p.ctx.theta, k = p.ctx.k;
+  const bool ms = p.ctx.order == kMultiSelect;
+  const int S = ms ? 8 : 2;
+  uint32_t dec = 0, correct = 1;
+  float L = 0.f;
+  int32_t gi[8];
+  float gv[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) { gi[q] = -1; gv[q] = 0.f; }
+  if (active) {
+    const int D = __ldg(p.ctx.nlists + b.app);
+    float zj[8];
+    uint32_t kj[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      zj[j] = j < D ? lb.z[lane * kListPad + j] : -CUDART_INF_F;
+      kj[j] = j < D ? lb.k[lane * kListPad + j] : kNone;
+    }
+    const uint32_t G = b.G;
+    const bool y = G != 0;
+    const float wi = p.w ? (wtab_smem ? wtab_smem[G] : __ldg(p.w + b.app * 256u + G)) : 1.f;
+    if (!ms) {
+      // application-choice order: the first list (code order) holding an output label
+      dec = static_cast<uint32_t>(D);
+#pragma unroll
+      for (int j = 7; j >= 0; --j)
+        if (kj[j] != kNone && zj[j] > tau) dec = static_cast<uint32_t>(j);
+      const int kk = y ? __ffs(G) - 1 : D;  // the ground truth's decision
+      correct = dec == static_cast<uint32_t>(kk);
+      if (p.want_loss) {
+        // competitor: lists j < k when y = 1 (P_{k⁻}), every list when y = 0 (P)
+        float zc = -CUDART_INF_F;
+        uint32_t kc = kNone;
+        float zk = -CUDART_INF_F;
+        uint32_t kk_key = kNone;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (j == kk) { zk = zj[j]; kk_key = kj[j]; }
+          const bool compete = y ? (j < kk) : (j < D);
+          if (compete && kj[j] != kNone && beats(zj[j], kj[j], zc, kc)) { zc = zj[j]; kc = kj[j]; }
+        }
+        if (y && kk_key != kNone) {
+          const bool c_over = kc != kNone && zc > tau;
+          const float am = c_over ? sigmoid_f(zc) : theta;  // max(θ, P_{k⁻})
+          const float x = am - sigmoid_f(zk);
+          const float ds = k * dsigmoid_f(k * x);
+          L = wi * sigmoid_f(k * x);
+          gi[0] = static_cast<int32_t>(kk_key >> 8);
+          gv[0] = -wi * ds * dsigmoid_f(zk) * p.grad_scale;
+          if (c_over) {
+            gi[1] = static_cast<int32_t>(kc >> 8);
+            gv[1] = wi * ds * dsigmoid_f(zc) * p.grad_scale;
+          }
+        } else if (!y && kc != kNone) {
+          const float x = sigmoid_f(zc) - theta;  // P − θ
+          L = wi * sigmoid_f(k * x);
+          gi[1] = static_cast<int32_t>(kc >> 8);
+          gv[1] = wi * k * dsigmoid_f(k * x) * dsigmoid_f(zc) * p.grad_scale;
+        }
+      }
+    } else {
+      // Multi-Select: every list holding an output label; exact match with G
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (kj[j] != kNone && zj[j] > tau) dec |= 1u << j;
+      correct = dec == G;
+      if (p.want_loss) {
+        float ell = 0.f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (kj[j] != kNone) {
+            const float pj = sigmoid_f(zj[j]);
+            const bool yj = (G >> j) & 1u;
+            const float x = yj ? theta - pj : pj - theta;
+            ell += sigmoid_f(k * x);
+            const float g = wi * k * dsigmoid_f(k * x) * dsigmoid_f(zj[j]) * p.grad_scale;
+            gi[j] = static_cast<int32_t>(kj[j] >> 8);
+            gv[j] = yj ? -g : g;
+          }
+        }
+        L = wi * ell;
+      }
+    }
+    if (p.decision) p.decision[b.row] = static_cast<uint8_t>(dec);
+    if (p.want_loss) {
+      if (p.loss_row) p.loss_row[b.row] = L;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        if (q < S) {
+          if (p.grad_idx) p.grad_idx[S * b.row + q] = gi[q];
+          if (p.grad_val) p.grad_val[S * b.row + q] = gv[q];
+        }
+      }
+    }
+  }
+  if (p.hist_pred && active) {
+    const uint32_t key = b.app * 256u + dec;
+    const unsigned peers = __match_any_sync(act, key);
+    if (lane == __ffs(peers) - 1) atomicAdd(p.hist_pred + key, static_cast<unsigned long long>(__popc(peers)));
+  }
+  if (p.has_gt) {
+    if (p.hist_gt && active) {
+      const uint32_t key = b.app * 256u + b.G;
+      const unsigned peers = __match_any_sync(act, key);
+      if (lane == __ffs(peers) - 1) atomicAdd(p.hist_gt + key, static_cast<unsigned long long>(__popc(peers)));
+    }
+    const unsigned inc = __ballot_sync(kFull, active && !correct);
+    if (p.n_incorrect && (inc >> lane & 1u)) {
+      const unsigned peers = __match_any_sync(inc, b.app);
+      if (lane == __ffs(peers) - 1) atomicAdd(p.n_incorrect + b.app, static_cast<unsigned long long>(__popc(peers)));
+    }
+    if (p.loss_sum && p.want_loss) {
+      double sl = active ? static_cast<double>(L) : 0.0;
+      const uint32_t app0 = __shfl_sync(kFull, b.app, 0);
+      if (__all_sync(kFull, !active || b.app == app0)) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) sl += __shfl_xor_sync(kFull, sl, off);
+        if (lane == 0) atomicAdd(p.loss_sum + app0, sl);
+      } else if (active) {
+        atomicAdd(p.loss_sum + b.app, sl);
+      }
+    }
+  }
+  if (p.grad_dense) {
+    for (int t = 0; t < b.n; ++t) {
+      const int64_t row = __shfl_sync(kFull, b.row, t);
+      int32_t ci[8];
+      float cv[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        ci[q] = __shfl_sync(kFull, gi[q], t);
+        cv[q] = __shfl_sync(kFull, gv[q], t);
+      }
+      float* out = p.grad_dense + row * p.ld;
+      const int64_t nv = p.ld >> 2;
+      for (int64_t v = lane; v < nv; v += 32) {
+        float e[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const int64_t c = 4 * v + q4;
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (c == ci[q]) e[q4] += cv[q];  // Multi-Select: one label may lead several lists
+        }
+        st_cs_f4(out + 4 * v, make_float4(e[0], e[1], e[2], e[3]));
+      }
+    }
+  }
+  __syncwarp();
+  b.n = 0;
+}
+
 // ------------------------------------------------------------------ sector-sparse gather kernel
 
 // Load flavours (experiment, EvalParams::ld_flavor): 0 nc+L1::no_allocate, 1 .cg, 2 default, 3 .cs
@@ -743,9 +954,12 @@ __device__ __forceinline__ float ldg_stream_bf16(const uint16_t* p, int fl) {
 // logits straight from HBM (no shared-memory staging), so DRAM traffic is the 32-B
 // sectors that hold mapped labels instead of whole rows.  A warp issues the loads of
 // G rows (EPL per lane per row) before reducing any of them.
-template <int EPL, int G, bool BF16>
+template <int EPL, int G, bool BF16, int PAT>
 __global__ void __launch_bounds__(256) gather_kernel(const EvalParams p) {
   __shared__ float wtab_s[256];
+  constexpr int kLB = PAT ? 8 * 32 * kListPad : 1;  // per-warp list-maxima batches (PAT 1)
+  __shared__ float lbz_s[kLB];
+  __shared__ uint32_t lbk_s[kLB];
   const int lane = threadIdx.x & 31;
   const bool wtab = p.wtab_off >= 0;
   if (wtab)
@@ -759,6 +973,9 @@ __global__ void __launch_bounds__(256) gather_kernel(const EvalParams p) {
   le.app = -1;
   RowBatch b;
   b.n = 0; b.zp = b.zm = 0.f; b.kp = b.km = kNone; b.G = 0; b.app = 0; b.row = 0;
+  ListBatch lb;
+  lb.z = lbz_s + (PAT ? (threadIdx.x >> 5) * 32 * kListPad : 0);
+  lb.k = lbk_s + (PAT ? (threadIdx.x >> 5) * 32 * kListPad : 0);
   for (int64_t grp = gw; grp < ngroups; grp += nw) {
     const int64_t r0 = grp * G;
     const int nr = static_cast<int>(p.rows - r0 < G ? p.rows - r0 : G);
@@ -775,7 +992,7 @@ __global__ void __launch_bounds__(256) gather_kernel(const EvalParams p) {
       if (static_cast<int32_t>(a) != le.app) {
         const int32_t e0 = __ldg(p.ctx.ent_off + a);
         lane_ent_load(le, p.ctx.ent + e0, __ldg(p.ctx.ent_off + a + 1) - e0, static_cast<int32_t>(a), lane,
-                      BF16 ? 2u : 4u);
+                      BF16 ? 2u : 4u, p.ctx.order);
       }
       // issue every load of the run first (memory-level parallelism), then reduce
       float z[G][EPL];
@@ -798,17 +1015,26 @@ __global__ void __launch_bounds__(256) gather_kernel(const EvalParams p) {
           const int64_t row = r0 + j + g;
           uint32_t Gi = gm[g];
           if (!p.gt_mask && p.has_gt) Gi = warp_gt_mask(p, row, a, lane);
-          float zp, zm;
-          uint32_t kp, km;
-          scan_vals<EPL>(le, plus_mask(le, Gi), z[g], zp, kp, zm, km);
-          deposit(b, lane, zp, kp, zm, km, Gi, a, row);
-          if (b.n == 32) finish_batch(p, b, wtab ? wtab_s : nullptr, lane);
+          if constexpr (PAT == 0) {
+            float zp, zm;
+            uint32_t kp, km;
+            scan_vals<EPL>(le, plus_mask(le, Gi), z[g], zp, kp, zm, km);
+            deposit(b, lane, zp, kp, zm, km, Gi, a, row);
+            if (b.n == 32) finish_batch(p, b, wtab ? wtab_s : nullptr, lane);
+          } else {
+            scan_lists<EPL>(le, __ldg(p.ctx.nlists + a), z[g], lb, b.n, lane);
+            deposit(b, lane, 0.f, kNone, 0.f, kNone, Gi, a, row);
+            if (b.n == 32) finish_lists(p, b, lb, wtab ? wtab_s : nullptr, lane);
+          }
         }
       }
       j += run;
     }
   }
-  if (b.n > 0) finish_batch(p, b, wtab ? wtab_s : nullptr, lane);
+  if (b.n > 0) {
+    if constexpr (PAT == 0) finish_batch(p, b, wtab ? wtab_s : nullptr, lane);
+    else finish_lists(p, b, lb, wtab ? wtab_s : nullptr, lane);
+  }
 }
 
 // ------------------------------------------------------------------ GT-only pre-pass
@@ -852,15 +1078,10 @@ __global__ void __launch_bounds__(256) hist_kernel(const HistParams p) {
       uint32_t G = 0;
 #pragma unroll
       for (int t = 0; t < kHL; ++t) {
-        if (lab[k][t] >= 0) {
-          const uint8_t v = __ldg(cat + lab[k][t]);
-          if (v != kCatNone) G |= 1u << v;
-        }
+        if (lab[k][t] >= 0) G |= label_lists(__ldg(cat + lab[k][t]), p.ctx.order);
       }
-      for (int64_t t = o0[k] + kHL; t < o1[k]; ++t) {  // rows with more than kHL labels
-        const uint8_t v = __ldg(cat + __ldg(p.gt_lab + t));
-        if (v != kCatNone) G |= 1u << v;
-      }
+      for (int64_t t = o0[k] + kHL; t < o1[k]; ++t)  // rows with more than kHL labels
+        G |= label_lists(__ldg(cat + __ldg(p.gt_lab + t)), p.ctx.order);
       if (p.gt_mask_out && row[k] < p.rows) p.gt_mask_out[row[k]] = static_cast<uint8_t>(G);
       key[k] = a[k] * 256u + G;
     }
@@ -957,11 +1178,11 @@ cudaError_t launch_eval(const EvalParams& p, int epl, int grid, size_t smem, cud
   return cudaGetLastError();
 }
 
-template <int EPL, int G, bool BF16>
+template <int EPL, int G, bool BF16, int PAT>
 static cudaError_t launch_gather_t(const EvalParams& p, int sms, cudaStream_t st) {
   static int blocks_per_sm = 0;
   if (blocks_per_sm == 0) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, gather_kernel<EPL, G, BF16>, 256, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, gather_kernel<EPL, G, BF16, PAT>, 256, 0);
     if (blocks_per_sm < 1) blocks_per_sm = 1;
   }
   const int64_t warps_needed = (p.rows + G - 1) / G;
@@ -969,24 +1190,25 @@ static cudaError_t launch_gather_t(const EvalParams& p, int sms, cudaStream_t st
   const int64_t max_grid = (warps_needed + 7) / 8;
   if (grid > max_grid) grid = max_grid;
   if (grid < 1) grid = 1;
-  gather_kernel<EPL, G, BF16><<<static_cast<int>(grid), 256, 0, st>>>(p);
+  gather_kernel<EPL, G, BF16, PAT><<<static_cast<int>(grid), 256, 0, st>>>(p);
   return cudaGetLastError();
 }
 
-template <bool BF16>
+template <bool BF16, int PAT>
 static cudaError_t launch_gather_dt(const EvalParams& p, int epl, int sms, cudaStream_t st) {
   switch (epl) {
-    case 1: return launch_gather_t<1, 8, BF16>(p, sms, st);
-    case 2: return launch_gather_t<2, 8, BF16>(p, sms, st);
-    case 4: return launch_gather_t<4, 4, BF16>(p, sms, st);
-    case 8: return launch_gather_t<8, 4, BF16>(p, sms, st);
-    case 16: return launch_gather_t<16, 2, BF16>(p, sms, st);
-    default: return launch_gather_t<32, 1, BF16>(p, sms, st);
+    case 1: return launch_gather_t<1, 8, BF16, PAT>(p, sms, st);
+    case 2: return launch_gather_t<2, 8, BF16, PAT>(p, sms, st);
+    case 4: return launch_gather_t<4, 4, BF16, PAT>(p, sms, st);
+    case 8: return launch_gather_t<8, 4, BF16, PAT>(p, sms, st);
+    case 16: return launch_gather_t<16, 2, BF16, PAT>(p, sms, st);
+    default: return launch_gather_t<32, 1, BF16, PAT>(p, sms, st);
   }
 }
 
-cudaError_t launch_gather(const EvalParams& p, int epl, int sms, cudaStream_t st) {
-  return p.bf16 ? launch_gather_dt<true>(p, epl, sms, st) : launch_gather_dt<false>(p, epl, sms, st);
+cudaError_t launch_gather(const EvalParams& p, int epl, int pat, int sms, cudaStream_t st) {
+  if (pat) return p.bf16 ? launch_gather_dt<true, 1>(p, epl, sms, st) : launch_gather_dt<false, 1>(p, epl, sms, st);
+  return p.bf16 ? launch_gather_dt<true, 0>(p, epl, sms, st) : launch_gather_dt<false, 0>(p, epl, sms, st);
 }
 
 cudaError_t launch_hist(const HistParams& p, int grid, size_t smem, cudaStream_t st) {

@@ -59,10 +59,10 @@ def allreduce_many_(tensors, group=None):
 class StepOutputs:
     decision: torch.Tensor     # uint8 [rows]       (this rank's rows)
     gt_mask: torch.Tensor      # uint8 [rows]
-    grad_idx: torch.Tensor     # int32 [rows*2]
-    grad_val: torch.Tensor     # float32 [rows*2]
+    grad_idx: torch.Tensor     # int32 [rows*S]  (S = ctx.grad_slots: 2, or 8 for Multi-Select)
+    grad_val: torch.Tensor     # float32 [rows*S]
     hist_gt: torch.Tensor      # int64 [n_apps*256]  global after the step
-    counts: torch.Tensor       # int64 [n_apps*17]   n_incorrect | hist_pred(16), global
+    counts: torch.Tensor       # int64 [n_apps*257]  n_incorrect | hist_pred(256), global
     loss_sum: torch.Tensor     # float64 [n_apps]    global
     w: torch.Tensor            # float32 [n_apps*256]
     loss_row: torch.Tensor | None = None
@@ -72,7 +72,7 @@ class StepOutputs:
         return self.counts[:n_apps]
 
     def hist_pred(self, n_apps: int):
-        return self.counts[n_apps:].view(n_apps, 16)
+        return self.counts[n_apps:].view(n_apps, 256)
 
 
 class Evaluator:
@@ -84,17 +84,19 @@ class Evaluator:
         na = ctx.n_apps
         dev = torch.device(device)
         r = max(int(max_rows), 1)
+        S = ctx.grad_slots
+        self.S = S
         # every accumulator in one buffer so a step clears them with a single memset:
-        # [hist_gt n_apps*256 | n_incorrect n_apps | hist_pred n_apps*16 | loss_sum n_apps (f64 bits)]
-        self._acc = torch.zeros(na * 256 + na * 17 + na, dtype=torch.int64, device=dev)
+        # [hist_gt n_apps*256 | n_incorrect n_apps | hist_pred n_apps*256 | loss_sum n_apps (f64 bits)]
+        self._acc = torch.zeros(na * 256 + na * 257 + na, dtype=torch.int64, device=dev)
         self.out = StepOutputs(
             decision=torch.empty(r, dtype=torch.uint8, device=dev),
             gt_mask=torch.empty(r + 16, dtype=torch.uint8, device=dev),
-            grad_idx=torch.empty(2 * r, dtype=torch.int32, device=dev),
-            grad_val=torch.empty(2 * r, dtype=torch.float32, device=dev),
+            grad_idx=torch.empty(S * r, dtype=torch.int32, device=dev),
+            grad_val=torch.empty(S * r, dtype=torch.float32, device=dev),
             hist_gt=self._acc[:na * 256],
-            counts=self._acc[na * 256:na * 273],
-            loss_sum=self._acc[na * 273:].view(torch.float64),
+            counts=self._acc[na * 256:na * 513],
+            loss_sum=self._acc[na * 513:].view(torch.float64),
             w=torch.empty(na * 256, dtype=torch.float32, device=dev),
             loss_row=torch.empty(r, dtype=torch.float32, device=dev) if want_loss_row else None,
             grad_dense=torch.empty(r * dense_ld, dtype=torch.float32, device=dev) if dense_ld else None,
@@ -123,10 +125,11 @@ class Evaluator:
         """Pinned host buffers for step_host's per-row results and aggregates."""
         na = self.ctx.n_apps
         pin = dict(pin_memory=True)
+        S = self.S
         return dict(decision=torch.empty(rows, dtype=torch.uint8, **pin),
-                    grad_idx=torch.empty(2 * rows, dtype=torch.int32, **pin),
-                    grad_val=torch.empty(2 * rows, dtype=torch.float32, **pin),
-                    counts=torch.empty(na * 17, dtype=torch.int64, **pin),
+                    grad_idx=torch.empty(S * rows, dtype=torch.int32, **pin),
+                    grad_val=torch.empty(S * rows, dtype=torch.float32, **pin),
+                    counts=torch.empty(na * 257, dtype=torch.int64, **pin),
                     hist_gt=torch.empty(na * 256, dtype=torch.int64, **pin),
                     loss_sum=torch.empty(na, dtype=torch.float64, **pin))
 
@@ -180,14 +183,15 @@ class Evaluator:
             comp.wait_event(ready[ci & 1])
             sc_loss_fwd_bwd(ctx, Batch(logits=buf[:hi - lo], gt_mask=o.gt_mask[lo:], app=None if d_app is None
                                        else d_app[lo:hi]),
-                            w=o.w, grad_scale=grad_scale, loss_sum=o.loss_sum, grad_idx=o.grad_idx[2 * lo:2 * hi],
-                            grad_val=o.grad_val[2 * lo:2 * hi], decision=o.decision[lo:hi],
+                            w=o.w, grad_scale=grad_scale, loss_sum=o.loss_sum, grad_idx=o.grad_idx[self.S * lo:self.S * hi],
+                            grad_val=o.grad_val[self.S * lo:self.S * hi], decision=o.decision[lo:hi],
                             n_incorrect=o.counts[:na], hist_pred=o.counts[na:])
             free[ci & 1].record(comp)
         allreduce_many_([o.counts, o.loss_sum], self.group)
         host_out["decision"][:rows].copy_(o.decision[:rows], non_blocking=True)
-        host_out["grad_idx"][:2 * rows].copy_(o.grad_idx[:2 * rows], non_blocking=True)
-        host_out["grad_val"][:2 * rows].copy_(o.grad_val[:2 * rows], non_blocking=True)
+        S = self.S
+        host_out["grad_idx"][:S * rows].copy_(o.grad_idx[:S * rows], non_blocking=True)
+        host_out["grad_val"][:S * rows].copy_(o.grad_val[:S * rows], non_blocking=True)
         host_out["counts"].copy_(o.counts, non_blocking=True)
         host_out["hist_gt"].copy_(o.hist_gt, non_blocking=True)
         host_out["loss_sum"].copy_(o.loss_sum, non_blocking=True)

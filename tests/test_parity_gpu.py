@@ -38,11 +38,12 @@ def to_dev(b, dtype):
     return out
 
 
-def run_gpu(ctxspec, d, mode="mask", dense=False, with_app=False):
+def run_gpu(ctxspec, d, mode="mask", dense=False, with_app=False, order=0):
     """hist pre-pass -> weights -> fused loss pass; returns numpy dict."""
     torch, sc, _, _ = _mods()
-    ctx = sc.Context(ctxspec.C, ctxspec.lists, ctxspec.tau, ctxspec.k, multi_app=True)
+    ctx = sc.Context(ctxspec.C, ctxspec.lists, ctxspec.tau, ctxspec.k, order=order, multi_app=True)
     rows, na = d["logits"].shape[0], ctxspec.n_apps
+    S = ctx.grad_slots
     app = d.get("app") if with_app else None
     hist = torch.zeros(na * 256, dtype=torch.int64, device="cuda")
     gmask = torch.empty(rows + 16, dtype=torch.uint8, device="cuda")
@@ -53,12 +54,12 @@ def run_gpu(ctxspec, d, mode="mask", dense=False, with_app=False):
     o = dict(
         decision=torch.full((rows,), 77, dtype=torch.uint8, device="cuda"),
         n_incorrect=torch.zeros(na, dtype=torch.int64, device="cuda"),
-        hist_pred=torch.zeros(na * 16, dtype=torch.int64, device="cuda"),
+        hist_pred=torch.zeros(na * 256, dtype=torch.int64, device="cuda"),
         hist_gt=torch.zeros(na * 256, dtype=torch.int64, device="cuda"),
         loss_sum=torch.zeros(na, dtype=torch.float64, device="cuda"),
         loss_row=torch.full((rows,), -1.0, dtype=torch.float32, device="cuda"),
-        grad_idx=torch.full((2 * rows,), -7, dtype=torch.int32, device="cuda"),
-        grad_val=torch.full((2 * rows,), -7.0, dtype=torch.float32, device="cuda"),
+        grad_idx=torch.full((S * rows,), -7, dtype=torch.int32, device="cuda"),
+        grad_val=torch.full((S * rows,), -7.0, dtype=torch.float32, device="cuda"),
     )
     ld = d["logits"].stride(0)
     if dense:
@@ -76,12 +77,13 @@ def run_gpu(ctxspec, d, mode="mask", dense=False, with_app=False):
     res["w"] = w.cpu().numpy()
     res["grad_scale"] = grad_scale
     res["ld"] = ld
+    res["S"] = S
     return res
 
 
-def run_oracle(ctxspec, b, grad_scale, with_app=False):
+def run_oracle(ctxspec, b, grad_scale, with_app=False, order=0):
     *_, Oracle = _mods()
-    orc = Oracle.from_spec(ctxspec)
+    orc = Oracle.from_spec(ctxspec, order)
     app = b.get("app") if with_app else None
     pre = orc.eval(b["logits"], b["gt_off"], b["gt_lab"], app=app, want_loss=False)
     w = Oracle.weights_by_mask(pre["hist_gt"])
@@ -101,13 +103,16 @@ def compare(g, o, w_orc, rows):
     np.testing.assert_allclose(g["grad_val"], o["grad_val"], rtol=RTOL, atol=0)
     np.testing.assert_allclose(g["loss_sum"], o["loss_sum"], rtol=RTOL, atol=0)
     if "grad_dense" in g:
-        ld = g["ld"]
+        ld, S = g["ld"], g["S"]
         dense = np.zeros((rows, ld), dtype=np.float64)
-        gi, gv = o["grad_idx"].reshape(rows, 2), o["grad_val"].reshape(rows, 2)
-        for s in range(2):
+        mag = np.zeros((rows, ld), dtype=np.float64)  # Σ|terms|: bound for sums that cancel (Multi-Select)
+        gi, gv = o["grad_idx"].reshape(rows, S), o["grad_val"].reshape(rows, S)
+        for s in range(S):
             m = gi[:, s] >= 0
             dense[np.nonzero(m)[0], gi[m, s]] += gv[m, s]
-        np.testing.assert_allclose(g["grad_dense"].reshape(rows, ld), dense, rtol=RTOL, atol=0)
+            mag[np.nonzero(m)[0], gi[m, s]] += np.abs(gv[m, s])
+        got = g["grad_dense"].reshape(rows, ld).astype(np.float64)
+        assert np.all(np.abs(got - dense) <= RTOL * mag), np.max(np.abs(got - dense) - RTOL * mag)
 
 
 CASES = [
@@ -213,7 +218,7 @@ def test_accumulate_and_chunking(kernel):
 
     def agg(parts):
         ni = torch.zeros(1, dtype=torch.int64, device="cuda")
-        hp = torch.zeros(16, dtype=torch.int64, device="cuda")
+        hp = torch.zeros(256, dtype=torch.int64, device="cuda")
         hg = torch.zeros(256, dtype=torch.int64, device="cuda")
         ls = torch.zeros(1, dtype=torch.float64, device="cuda")
         for lo, hi in parts:
@@ -247,7 +252,7 @@ def test_edge_cases_and_errors():
     with pytest.raises(sc.ScError):
         sc.Context(10, [[1]] * 9)  # > 8 lists
     with pytest.raises(sc.ScError):
-        sc.Context(10, [[1]], order=sc.SC_ORDER_APP_CHOICE)
+        sc.Context(10, [[1]], order=7)
     with pytest.raises(ValueError):
         sc.sc_decide(ctx, sc.Batch(logits=torch.zeros(4, 12)))  # CPU tensor: no fallback
     # decisions only (no GT) on one row

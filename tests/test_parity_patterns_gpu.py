@@ -1,0 +1,69 @@
+"""GPU parity of the other decision patterns against the oracle:
+Multi-Choice application-choice order (Eq. app_choice) and Multi-Select (Eq. multi-select).
+Same bar as the hot path: decisions, G, counters and gradient indices bit-exact; loss and
+gradient values within 1e-5 relative; overlapping lists exercise the two membership rules
+(first list for the choice orders, every list for Multi-Select)."""
+import numpy as np
+import pytest
+
+from conftest import gpu_available
+from test_parity_gpu import compare, run_gpu, run_oracle, tie_heavy_batch, to_dev
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device")]
+
+APP_CHOICE, MULTI_SELECT = 1, 2
+
+
+@pytest.mark.parametrize("order", [APP_CHOICE, MULTI_SELECT])
+@pytest.mark.parametrize("cfg,dtype,row0,rows,mode,layout", [
+    (1, "f32", 0, 4096, "mask", 0),
+    (1, "bf16", 0, 4096, "csr", 0),
+    (2, "f32", 777, 3001, "mask", 0),
+    (2, "bf16", 5, 2049, "csr", 0),
+    (3, "f32", 31, 203, "mask", 0),
+    (4, "f32", (1 << 18) - 700, 1500, "mask", 0),
+    (4, "bf16", 10, 999, "mask", 1),
+])
+def test_patterns_configs(order, cfg, dtype, row0, rows, mode, layout):
+    import synth
+    spec = synth.config_context(cfg)
+    wl = synth.Workload(spec, seed=cfg, dtype=dtype, layout=layout)
+    b = wl.host_batch(row0, rows)
+    multi = spec.n_apps > 1
+    g = run_gpu(spec, to_dev(b, dtype), mode=mode, dense=(cfg in (1, 2)), with_app=multi, order=order)
+    o, w = run_oracle(spec, b, g["grad_scale"], with_app=multi, order=order)
+    compare(g, o, w, rows)
+
+
+@pytest.mark.parametrize("order", [APP_CHOICE, MULTI_SELECT])
+@pytest.mark.parametrize("C,ld,rows", [(1, 4, 100), (4, 4, 333), (37, 40, 1000), (300, 300, 777), (4097, 4100, 97)])
+def test_patterns_tie_heavy_overlapping(order, C, ld, rows):
+    import synth
+    rng = np.random.default_rng(C * 11 + rows + order)
+    for tau in (0.0, -1.0):
+        D = int(rng.integers(1, 9))
+        lists = [sorted(set(rng.integers(0, C, size=int(rng.integers(0, min(C, 40) + 1))).tolist()))
+                 for _ in range(D)]
+        spec = synth.ContextSpec(C, [lists], tau=tau, k=float(rng.choice([1.0, 10.0, 25.0])))
+        b = tie_heavy_batch(rng, C, rows, ld, lists, tau)
+        g = run_gpu(spec, to_dev(b, "f32"), mode="mask" if tau == 0 else "csr", dense=C < 1000, order=order)
+        o, w = run_oracle(spec, b, g["grad_scale"], order=order)
+        compare(g, o, w, rows)
+
+
+def test_true_false_patterns_agree_on_gpu():
+    """One list: the three patterns give the same decisions (list 0 / its mask) and losses."""
+    import torch
+    import synth
+    rng = np.random.default_rng(5)
+    C, rows = 64, 2000
+    W1 = sorted(set(rng.integers(0, C, size=12).tolist()))
+    spec = synth.ContextSpec(C, [[W1]], tau=0.0, k=10.0)
+    b = tie_heavy_batch(rng, C, rows, C, [W1], 0.0)
+    res = {o: run_gpu(spec, to_dev(b, "f32"), order=o) for o in (0, APP_CHOICE, MULTI_SELECT)}
+    d0 = res[0]["decision"]
+    np.testing.assert_array_equal(res[APP_CHOICE]["decision"], d0)
+    np.testing.assert_array_equal(res[MULTI_SELECT]["decision"], (d0 == 0).astype(np.uint8))
+    for o in (APP_CHOICE, MULTI_SELECT):
+        np.testing.assert_allclose(res[o]["loss_row"], res[0]["loss_row"], rtol=1e-6, atol=0)
+        np.testing.assert_array_equal(res[o]["n_incorrect"], res[0]["n_incorrect"])
