@@ -191,6 +191,31 @@ sc_status sc_loss_fwd_bwd(sc_context ctx, const sc_batch* batch, const float* w,
                           float* grad_dense, uint8_t* decision, uint64_t* n_incorrect, uint64_t* hist_pred,
                           uint64_t* hist_gt, sc_stream stream);
 
+/* ---- Value-ranges applications, NEXT f1 -------------------------
+ * The API returns a score O_i per input; the application checks, in code order, whether
+ * it lies in each of its ranges [lo_j, hi_j] (reading A22: closed ranges, the first
+ * containing range wins, none -> default m).  Loss:
+ *   L_i = w[r_i] ( S(lo_{r_i} − O_i) + S(O_i − hi_{r_i}) ),  r_i = the range the
+ * ground-truth score lies in (no range -> L_i = 0), w[r] = M / N_r (rebalancing). */
+typedef struct sc_ranges_s* sc_ranges;
+
+/* m in [1, 255] ranges; lo/hi host arrays (copied), lo_j <= hi_j finite; k > 0. */
+sc_status sc_ranges_load(int32_t m, const float* lo, const float* hi, float k, sc_ranges* out);
+sc_status sc_ranges_free(sc_ranges r);
+/* Ground-truth pre-pass: hist_gt [m+1] += #{i : r_i = r}; gt_range_out [rows] = r_i (optional). */
+sc_status sc_ranges_hist(sc_ranges r, const float* gt_score, int64_t rows, uint64_t* hist_gt,
+                         uint8_t* gt_range_out, sc_stream stream);
+/* w [m+1] = M / hist_gt[r] (0 for empty bins), M = sum of hist_gt (the GLOBAL histogram). */
+sc_status sc_ranges_weights(sc_ranges r, const uint64_t* hist_gt, float* w, sc_stream stream);
+/* One pass over the scores: decision [rows] (range id, m = none), n_incorrect [1] += #{d_i ≠ r_i},
+ * hist_pred [m+1] += decision histogram, loss_sum [1] += Σ L_i, loss_row [rows] = L_i,
+ * grad [rows] = dL_i/dO_i · grad_scale.  w NULL = all 1.  Outputs may be NULL. */
+sc_status sc_ranges_loss_fwd_bwd(sc_ranges r, const float* score, const uint8_t* gt_range, int64_t rows,
+                                 const float* w, float grad_scale, double* loss_sum, float* loss_row, float* grad,
+                                 uint8_t* decision, uint64_t* n_incorrect, uint64_t* hist_pred,
+                                 sc_stream stream);
+const char* sc_ranges_last_error(void);
+
 /* Thread-local text for the last non-OK status of this thread ("" if none). */
 const char* sc_last_error(void);
 

@@ -81,6 +81,19 @@ def _load():
     lib.sc_launch_count.argtypes = []
     lib.sc_last_kernel.restype = ctypes.c_char_p
     lib.sc_last_kernel.argtypes = []
+    F32 = ctypes.c_float
+    lib.sc_ranges_load.restype = ctypes.c_int
+    lib.sc_ranges_load.argtypes = [I32, P, P, F32, ctypes.POINTER(P)]
+    lib.sc_ranges_free.restype = ctypes.c_int
+    lib.sc_ranges_free.argtypes = [P]
+    lib.sc_ranges_hist.restype = ctypes.c_int
+    lib.sc_ranges_hist.argtypes = [P, P, I64, P, P, P]
+    lib.sc_ranges_weights.restype = ctypes.c_int
+    lib.sc_ranges_weights.argtypes = [P, P, P, P]
+    lib.sc_ranges_loss_fwd_bwd.restype = ctypes.c_int
+    lib.sc_ranges_loss_fwd_bwd.argtypes = [P, P, P, I64, P, F32, P, P, P, P, P, P, P]
+    lib.sc_ranges_last_error.restype = ctypes.c_char_p
+    lib.sc_ranges_last_error.argtypes = []
     return lib
 
 
@@ -323,3 +336,61 @@ def sc_loss_fwd_bwd(ctx: Context, batch: Batch, w=None, grad_scale: float = 1.0,
         _u64(n_incorrect, "n_incorrect", ctx.n_apps),
         _u64(hist_pred, "hist_pred", ctx.n_apps * 256),
         _u64(hist_gt, "hist_gt", ctx.n_apps * 256), _stream(stream)))
+
+
+# ------------------------------------------------------------------ value ranges
+
+def _rcheck(status: int):
+    if status != SC_OK:
+        raise ScError(status, _lib.sc_ranges_last_error().decode())
+
+
+class Ranges:
+    """Handle to a value-ranges application (sc_ranges): ranges [lo_j, hi_j] in code order."""
+
+    def __init__(self, lo, hi, k: float = 10.0):
+        self.m = len(lo)
+        a_lo = (ctypes.c_float * max(1, self.m))(*[float(x) for x in lo])
+        a_hi = (ctypes.c_float * max(1, len(hi)))(*[float(x) for x in hi])
+        if len(hi) != self.m:
+            raise ValueError("lo and hi must have the same length")
+        h = ctypes.c_void_p()
+        _rcheck(_lib.sc_ranges_load(self.m, a_lo, a_hi, float(k), ctypes.byref(h)))
+        self._h = h
+
+    def free(self):
+        if getattr(self, "_h", None):
+            _lib.sc_ranges_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def sc_ranges_hist(r: Ranges, gt_score, hist_gt=None, gt_range_out=None, stream=None):
+    torch = _torch()
+    n = gt_score.numel()
+    _rcheck(_lib.sc_ranges_hist(r._h, _dev_ptr(gt_score, "gt_score", (torch.float32,)), n,
+                                _u64(hist_gt, "hist_gt", r.m + 1),
+                                _dev_ptr(gt_range_out, "gt_range_out", (torch.uint8,), n), _stream(stream)))
+
+
+def sc_ranges_weights(r: Ranges, hist_gt, w, stream=None):
+    torch = _torch()
+    _rcheck(_lib.sc_ranges_weights(r._h, _u64(hist_gt, "hist_gt", r.m + 1),
+                                   _dev_ptr(w, "w", (torch.float32,), r.m + 1), _stream(stream)))
+
+
+def sc_ranges_loss_fwd_bwd(r: Ranges, score, gt_range, w=None, grad_scale: float = 1.0, loss_sum=None,
+                           loss_row=None, grad=None, decision=None, n_incorrect=None, hist_pred=None, stream=None):
+    torch = _torch()
+    n = score.numel()
+    _rcheck(_lib.sc_ranges_loss_fwd_bwd(
+        r._h, _dev_ptr(score, "score", (torch.float32,)), _dev_ptr(gt_range, "gt_range", (torch.uint8,), n), n,
+        _dev_ptr(w, "w", (torch.float32,), r.m + 1), float(grad_scale),
+        _dev_ptr(loss_sum, "loss_sum", (torch.float64,), 1), _dev_ptr(loss_row, "loss_row", (torch.float32,), n),
+        _dev_ptr(grad, "grad", (torch.float32,), n), _dev_ptr(decision, "decision", (torch.uint8,), n),
+        _u64(n_incorrect, "n_incorrect", 1), _u64(hist_pred, "hist_pred", r.m + 1), _stream(stream)))

@@ -1,0 +1,60 @@
+"""GPU parity of the value-ranges path against the oracle."""
+import numpy as np
+import pytest
+
+from conftest import gpu_available
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device")]
+
+
+@pytest.mark.parametrize("m,rows", [(1, 1), (3, 100003), (7, 5000), (40, 20000)])
+def test_ranges_parity(m, rows):
+    import torch
+    import paper_2310_07240_b200 as sc
+    from oracle import RangesOracle
+    rng = np.random.default_rng(m * 1000 + rows)
+    edges = np.sort(rng.uniform(-1, 1, size=m + 1)).astype(np.float32)
+    lo, hi = edges[:-1].copy(), edges[1:].copy()
+    if m > 3:  # overlapping ranges too: the first containing range wins
+        hi[1] = np.float32(min(1.0, hi[1] + 0.2))
+    k = 10.0
+    score = rng.uniform(-1.2, 1.2, rows).astype(np.float32)
+    score[: rows // 10] = lo[rng.integers(0, m, rows // 10)]  # exactly on a bound
+    gt = rng.uniform(-1.2, 1.2, rows).astype(np.float32)
+    orc = RangesOracle(lo.astype(np.float64), hi.astype(np.float64), k)
+    pre = orc.eval(score, gt)
+    w_ref = orc.weights(pre["hist_gt"])
+    ref = orc.eval(score, gt, w=w_ref, grad_scale=1.0 / rows)
+
+    r = sc.Ranges(lo, hi, k)
+    d_score, d_gt = torch.from_numpy(score).cuda(), torch.from_numpy(gt).cuda()
+    hist = torch.zeros(m + 1, dtype=torch.int64, device="cuda")
+    gtr = torch.empty(rows, dtype=torch.uint8, device="cuda")
+    sc.sc_ranges_hist(r, d_gt, hist_gt=hist, gt_range_out=gtr)
+    w = torch.empty(m + 1, dtype=torch.float32, device="cuda")
+    sc.sc_ranges_weights(r, hist, w)
+    out = dict(loss_sum=torch.zeros(1, dtype=torch.float64, device="cuda"),
+               loss_row=torch.empty(rows, dtype=torch.float32, device="cuda"),
+               grad=torch.empty(rows, dtype=torch.float32, device="cuda"),
+               decision=torch.empty(rows, dtype=torch.uint8, device="cuda"),
+               n_incorrect=torch.zeros(1, dtype=torch.int64, device="cuda"),
+               hist_pred=torch.zeros(m + 1, dtype=torch.int64, device="cuda"))
+    sc.sc_ranges_loss_fwd_bwd(r, d_score, gtr, w=w, grad_scale=1.0 / rows, **out)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(hist.cpu().numpy().astype(np.uint64), pre["hist_gt"])
+    np.testing.assert_array_equal(gtr.cpu().numpy(), ref["gt_range"])
+    np.testing.assert_allclose(w.cpu().numpy(), w_ref, rtol=1e-7)
+    np.testing.assert_array_equal(out["decision"].cpu().numpy(), ref["decision"])
+    np.testing.assert_array_equal(out["n_incorrect"].cpu().numpy().astype(np.uint64), ref["n_incorrect"])
+    np.testing.assert_array_equal(out["hist_pred"].cpu().numpy().astype(np.uint64), ref["hist_pred"])
+    np.testing.assert_allclose(out["loss_row"].cpu().numpy(), ref["loss_row"], rtol=1e-5, atol=0)
+    # dL/dO = w k (σ'(k(O − hi)) − σ'(k(lo − O))): the two terms can cancel, so the bar is
+    # 1e-5 of the terms' magnitude (a tolerance bound only; the reference value is the oracle's)
+    r_i = ref["gt_range"].astype(np.int64)
+    ok = r_i < m
+    dsg = lambda x: np.exp(-np.abs(x)) / (1 + np.exp(-np.abs(x))) ** 2
+    mag = np.zeros(rows)
+    lo64, hi64, s64 = lo.astype(np.float64), hi.astype(np.float64), score.astype(np.float64)
+    mag[ok] = w_ref[r_i[ok]] * k * (dsg(k * (lo64[r_i[ok]] - s64[ok])) + dsg(k * (s64[ok] - hi64[r_i[ok]]))) / rows
+    assert np.all(np.abs(out["grad"].cpu().numpy() - ref["grad"]) <= 1e-5 * mag + 1e-30)
+    np.testing.assert_allclose(out["loss_sum"].cpu().numpy(), ref["loss_sum"], rtol=1e-5)
