@@ -306,21 +306,26 @@ def run_ours(args):
         ev.step(logits, gt_off, gt_lab, app=app, global_rows=global_rows)
     torch.cuda.synchronize(dev)
 
-    k_start = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    k_end = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    # instrumented step: events around the dominant kernel (sc_loss_fwd_bwd) on its stream
+    # instrumented step: CUDA events around each libsc call on the stream it is launched on
     import paper_2310_07240_b200.step as step_mod
-    orig = step_mod.sc_loss_fwd_bwd
+    phases = ("sc_decision_hist", "sc_weights_from_hist", "sc_loss_fwd_bwd")
+    ev_s = {ph: [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)] for ph in phases}
+    ev_e = {ph: [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)] for ph in phases}
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     idx = {"i": -1}
+    origs = {ph: getattr(step_mod, ph) for ph in phases}
 
-    def timed_loss(*a, **kw):
-        i = idx["i"]
-        k_start[i].record(stream)
-        orig(*a, **kw)
-        k_end[i].record(stream)
+    def wrap(ph):
+        def timed(*a, **kw):
+            i = idx["i"]
+            ev_s[ph][i].record(stream)
+            origs[ph](*a, **kw)
+            ev_e[ph][i].record(stream)
+        return timed
 
-    step_mod.sc_loss_fwd_bwd = timed_loss
+    for ph in phases:
+        setattr(step_mod, ph, wrap(ph))
+    k_start, k_end = ev_s["sc_loss_fwd_bwd"], ev_e["sc_loss_fwd_bwd"]
     launches0 = sc.sc_launch_count()
     with ClockSampler(local) as clk:
         barrier()
@@ -332,8 +337,10 @@ def run_ours(args):
         t_end.record(stream)
         torch.cuda.synchronize(dev)
         barrier()
-    step_mod.sc_loss_fwd_bwd = orig
+    for ph in phases:
+        setattr(step_mod, ph, origs[ph])
     launches = sc.sc_launch_count() - launches0
+    phase_us = {ph: 1e3 * sum(a.elapsed_time(b) for a, b in zip(ev_s[ph], ev_e[ph])) / args.steps for ph in phases}
     ms = t_start.elapsed_time(t_end)
     k_ms = sum(a.elapsed_time(b) for a, b in zip(k_start, k_end)) / args.steps
     if world > 1:
@@ -375,6 +382,7 @@ def run_ours(args):
                    "grad": f"sparse ({ctx.grad_slots} slots/row)", "order": args.order},
         "roofline": roofline,
         "gpu_launches": int(launches),
+        "phases_us": {k: round(v, 2) for k, v in phase_us.items()},
         "clocks": clk.summary(),
     }
 

@@ -201,7 +201,8 @@ sc_status run_eval(const sc_context_s* ctx, const sc_batch* b, const float* w, f
   const int W = sc::kConsumerWarps;
   const int64_t stage_cap = 64 * 1024;
   p.copy_row_bytes = static_cast<int32_t>(round_up(static_cast<int64_t>(ctx->C) * elt, 16));
-  const bool whole_rows = W * p.ld_bytes <= stage_cap;
+  const int64_t force_chunk = std::getenv("SC_FORCE_CHUNK") ? std::atoll(std::getenv("SC_FORCE_CHUNK")) : 0;
+  const bool whole_rows = W * p.ld_bytes <= stage_cap && force_chunk == 0;
   // mapped labels in registers when whole rows fit a stage and |W| <= 1024
   int epl = 0;
   if (whole_rows && ctx->max_ent <= 1024 && !(std::getenv("SC_EPL") && std::atoi(std::getenv("SC_EPL")) == 0))
@@ -233,7 +234,7 @@ sc_status run_eval(const sc_context_s* ctx, const sc_batch* b, const float* w, f
     logits_region = p.R * p.ld_bytes;
   } else {
     p.R = W;
-    p.chunk_bytes = static_cast<int32_t>((stage_cap / W) / 16 * 16);
+    p.chunk_bytes = static_cast<int32_t>((force_chunk ? force_chunk : stage_cap / W) / 16 * 16);
     p.chunk_elems = static_cast<int32_t>(p.chunk_bytes / elt);
     p.nchunks = static_cast<int32_t>((p.copy_row_bytes + p.chunk_bytes - 1) / p.chunk_bytes);
     logits_region = static_cast<int64_t>(p.R) * p.chunk_bytes;
