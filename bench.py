@@ -308,7 +308,8 @@ def run_ours(args):
 
     # instrumented step: CUDA events around each libsc call on the stream it is launched on
     import paper_2310_07240_b200.step as step_mod
-    phases = ("sc_decision_hist", "sc_weights_from_hist", "sc_loss_fwd_bwd")
+    phases = ("sc_decision_hist", "sc_decision_hist_weights", "sc_weights_from_hist", "sc_loss_fwd_bwd")
+    called = set()
     ev_s = {ph: [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)] for ph in phases}
     ev_e = {ph: [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)] for ph in phases}
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -318,6 +319,7 @@ def run_ours(args):
     def wrap(ph):
         def timed(*a, **kw):
             i = idx["i"]
+            called.add(ph)
             ev_s[ph][i].record(stream)
             origs[ph](*a, **kw)
             ev_e[ph][i].record(stream)
@@ -340,7 +342,8 @@ def run_ours(args):
     for ph in phases:
         setattr(step_mod, ph, origs[ph])
     launches = sc.sc_launch_count() - launches0
-    phase_us = {ph: 1e3 * sum(a.elapsed_time(b) for a, b in zip(ev_s[ph], ev_e[ph])) / args.steps for ph in phases}
+    phase_us = {ph: 1e3 * sum(a.elapsed_time(b) for a, b in zip(ev_s[ph], ev_e[ph])) / args.steps
+                for ph in phases if ph in called}
     ms = t_start.elapsed_time(t_end)
     k_ms = sum(a.elapsed_time(b) for a, b in zip(k_start, k_end)) / args.steps
     if world > 1:

@@ -41,6 +41,7 @@
 #ifndef SC_H
 #define SC_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -151,6 +152,14 @@ sc_status sc_decide(sc_context ctx, const sc_batch* batch, uint8_t* decision, ui
 sc_status sc_decision_hist(sc_context ctx, const sc_batch* batch, uint64_t* hist_gt, uint8_t* gt_mask_out,
                            sc_stream stream);
 
+/* sc_decision_hist_weights — sc_decision_hist followed, in the same launch, by
+ * sc_weights_from_hist on the histogram it produced (the last CTA to finish computes
+ * w).  For a batch that is the whole dataset (one GPU): hist_gt must be zero on entry.
+ * Calls sharing a context must not run concurrently (one completion counter per context).
+ *   w  device [n_apps*256] float, overwritten. */
+sc_status sc_decision_hist_weights(sc_context ctx, const sc_batch* batch, uint64_t* hist_gt, uint8_t* gt_mask_out,
+                                   float* w, sc_stream stream);
+
 /* sc_weights_from_hist — rebalancing weights from the GLOBAL mask histogram
  * (PAPER.md:2014, :2020, :2029): per app, M = sum_m H[m]; N(m) = #inputs whose
  * ground truth intersects m's lists = M - sum_{m' ∩ m = ∅} H[m'] for m != 0,
@@ -215,6 +224,23 @@ sc_status sc_ranges_loss_fwd_bwd(sc_ranges r, const float* score, const uint8_t*
                                  uint8_t* decision, uint64_t* n_incorrect, uint64_t* hist_pred,
                                  sc_stream stream);
 const char* sc_ranges_last_error(void);
+
+/* ---- Rebalanced training-data sampler (NEXT f2) --------------------
+ * Draws n row indices i.i.d. with probability q_i = w[G_i] / Σ_j w[G_j] (w = M/N from
+ * sc_weights_from_hist: the balance of PAPER.md:2020/2029), one application's rows.
+ * Mapping of uniforms to rows (reading A24): rows grouped by G (ascending mask, row order
+ * inside), bucket weights count_m·w[m] summed in double in ascending m; bucket = first m
+ * with u1·ΣW < cumulative W; row = number min(count_m − 1, floor(u2·count_m)) of the bucket.
+ *   gt_mask    device [rows] G_i (from sc_decision_hist)
+ *   w          device [256] float per-mask weights
+ *   u          device [2n] double uniforms in [0,1), interleaved (u1, u2) per draw
+ *   out        device [n] int64 row indices (-1 for every draw if all weights are 0)
+ *   workspace  device scratch of at least sc_sample_workspace_bytes(rows) bytes
+ * Four launches, stream-ordered; no allocation. */
+size_t sc_sample_workspace_bytes(int64_t rows);
+sc_status sc_rebalance_sample(const uint8_t* gt_mask, int64_t rows, const float* w, const double* u, int64_t n,
+                              int64_t* out, void* workspace, size_t workspace_bytes, sc_stream stream);
+const char* sc_sample_last_error(void);
 
 /* Thread-local text for the last non-OK status of this thread ("" if none). */
 const char* sc_last_error(void);

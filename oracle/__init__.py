@@ -83,6 +83,8 @@ def lib():
         L.orc_range_loss.argtypes = [I32, P, P, D, I32, D, D, P, P]
         L.orc_ranges_eval.argtypes = [I32, P, P, D, I64, P, P, P, D] + [P] * 8
         L.orc_ranges_weights.argtypes = [I32, P, P]
+        L.orc_sample.restype = ctypes.c_int
+        L.orc_sample.argtypes = [P, I64, P, I64, P, P, P]
         L.orc_eval.restype = ctypes.c_int
         L.orc_eval.argtypes = [P, I64, I64, I32, P, P, P, P, P, D] + [P] * 10
         _lib = L
@@ -322,3 +324,18 @@ class RangesOracle:
         for key in ("decision", "gt_range", "loss_row", "grad"):
             out[key] = out[key][:rows]
         return out
+
+
+def sample(gt_mask, w, u1, u2):
+    """Rebalanced sampler (reading A24): indices for the uniforms (u1, u2).
+    gt_mask: uint8 [rows]; w: per-mask weights [256] (the kernel's f32 values)."""
+    gt_mask = np.ascontiguousarray(gt_mask, dtype=np.uint8)
+    w = np.ascontiguousarray(np.asarray(w, dtype=np.float32).astype(np.float64))
+    u1 = np.ascontiguousarray(u1, dtype=np.float64)
+    u2 = np.ascontiguousarray(u2, dtype=np.float64)
+    out = np.empty(max(len(u1), 1), dtype=np.int64)
+    rc = lib().orc_sample(gt_mask.ctypes.data if len(gt_mask) else None, len(gt_mask), w.ctypes.data, len(u1),
+                          u1.ctypes.data, u2.ctypes.data, out.ctypes.data)
+    if rc != 0:
+        raise ValueError("every weight is zero")
+    return out[: len(u1)]

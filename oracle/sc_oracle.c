@@ -486,3 +486,43 @@ void orc_ranges_weights(int32_t m, const uint64_t* H, double* w) {
   for (int32_t r = 0; r <= m; ++r) M += H[r];
   for (int32_t r = 0; r <= m; ++r) w[r] = H[r] ? (double)M / (double)H[r] : 0.0;
 }
+
+/* ---------------------------------------------------------------- rebalanced sampler */
+
+/* The strawman of PAPER.md:1989-1990 (abstract PAPER.md:19-20): re-train on a re-sampled
+ * training set that rebalances the application's target classes.  Inputs are drawn
+ * i.i.d. with probability q_i = w_i / Σ_j w_j, w_i = M/N_i, the balance
+ * the loss weights express ("the number of target-inputs and non-target-inputs are
+ * effectively balanced").  Mapping of the two uniforms to an input
+ * (reading A24): group rows by G (ascending mask, rows in row order), bucket weight
+ * W_m = count_m · w[m] summed in double in ascending m; the bucket is the first m with
+ * u1 · ΣW < cumulative W, the row is number min(count_m − 1, floor(u2 · count_m)) of it.
+ * w: the per-mask weights as the caller has them (the kernel's f32 values, widened).
+ * Returns 0, or −1 when every weight is 0. */
+int orc_sample(const uint8_t* gt_mask, int64_t rows, const double* w, int64_t n, const double* u1, const double* u2,
+               int64_t* out) {
+  int64_t count[256] = {0};
+  for (int64_t i = 0; i < rows; ++i) count[gt_mask[i]] += 1;
+  int64_t start[256];
+  int64_t acc = 0;
+  for (int m = 0; m < 256; ++m) { start[m] = acc; acc += count[m]; }
+  int64_t* order = (int64_t*)malloc(sizeof(int64_t) * (size_t)(rows > 0 ? rows : 1));
+  int64_t fill[256];
+  for (int m = 0; m < 256; ++m) fill[m] = start[m];
+  for (int64_t i = 0; i < rows; ++i) order[fill[gt_mask[i]]++] = i;   /* stable: row order within a mask */
+  double cum[256];
+  double total = 0.0;
+  for (int m = 0; m < 256; ++m) { total += (double)count[m] * w[m]; cum[m] = total; }
+  if (!(total > 0.0)) { free(order); return -1; }
+  for (int64_t i = 0; i < n; ++i) {
+    const double t = u1[i] * total;
+    int m = 0;
+    while (m < 255 && !(t < cum[m])) ++m;
+    const int64_t c = count[m];
+    int64_t pos = (int64_t)floor(u2[i] * (double)c);
+    if (pos > c - 1) pos = c - 1;
+    out[i] = order[start[m] + pos];
+  }
+  free(order);
+  return 0;
+}

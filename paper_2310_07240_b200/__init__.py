@@ -20,7 +20,7 @@ from . import build as _build
 
 __all__ = [
     "ScError", "Context", "Batch", "sc_context_load", "sc_context_free", "sc_decide", "sc_decision_hist",
-    "sc_weights_from_hist", "sc_loss_fwd_bwd", "sc_last_error", "sc_launch_count", "sc_last_kernel", "library_path",
+    "sc_weights_from_hist", "sc_decision_hist_weights", "sc_loss_fwd_bwd", "sc_last_error", "sc_launch_count", "sc_last_kernel", "library_path",
 ]
 
 SC_OK, SC_ERR_INVALID_ARG, SC_ERR_OOM, SC_ERR_CUDA, SC_ERR_UNSUPPORTED = range(5)
@@ -71,6 +71,8 @@ def _load():
     lib.sc_decide.argtypes = [P, ctypes.POINTER(_CBatch), P, P, P, P, P]
     lib.sc_decision_hist.restype = ctypes.c_int
     lib.sc_decision_hist.argtypes = [P, ctypes.POINTER(_CBatch), P, P, P]
+    lib.sc_decision_hist_weights.restype = ctypes.c_int
+    lib.sc_decision_hist_weights.argtypes = [P, ctypes.POINTER(_CBatch), P, P, P, P]
     lib.sc_weights_from_hist.restype = ctypes.c_int
     lib.sc_weights_from_hist.argtypes = [P, P, P, P]
     lib.sc_loss_fwd_bwd.restype = ctypes.c_int
@@ -94,6 +96,12 @@ def _load():
     lib.sc_ranges_loss_fwd_bwd.argtypes = [P, P, P, I64, P, F32, P, P, P, P, P, P, P]
     lib.sc_ranges_last_error.restype = ctypes.c_char_p
     lib.sc_ranges_last_error.argtypes = []
+    lib.sc_sample_workspace_bytes.restype = ctypes.c_size_t
+    lib.sc_sample_workspace_bytes.argtypes = [I64]
+    lib.sc_rebalance_sample.restype = ctypes.c_int
+    lib.sc_rebalance_sample.argtypes = [P, I64, P, P, I64, P, P, ctypes.c_size_t, P]
+    lib.sc_sample_last_error.restype = ctypes.c_char_p
+    lib.sc_sample_last_error.argtypes = []
     return lib
 
 
@@ -310,6 +318,15 @@ def sc_decision_hist(ctx: Context, batch: Batch, hist_gt=None, gt_mask_out=None,
                                  _dev_ptr(gt_mask_out, "gt_mask_out", (torch.uint8,), cb.rows), _stream(stream)))
 
 
+def sc_decision_hist_weights(ctx: Context, batch: Batch, hist_gt, w, gt_mask_out=None, stream=None):
+    """Pre-pass + weights in one launch (whole dataset on one GPU; hist_gt must start at 0)."""
+    torch = _torch()
+    cb = batch._c()
+    _check(_lib.sc_decision_hist_weights(ctx.handle, ctypes.byref(cb), _u64(hist_gt, "hist_gt", ctx.n_apps * 256),
+                                         _dev_ptr(gt_mask_out, "gt_mask_out", (torch.uint8,), cb.rows),
+                                         _dev_ptr(w, "w", (torch.float32,), ctx.n_apps * 256), _stream(stream)))
+
+
 def sc_weights_from_hist(ctx: Context, hist_gt, w, stream=None):
     """Rebalancing weights M/N(m) from the global mask histogram (overwrites w)."""
     torch = _torch()
@@ -394,3 +411,24 @@ def sc_ranges_loss_fwd_bwd(r: Ranges, score, gt_range, w=None, grad_scale: float
         _dev_ptr(loss_sum, "loss_sum", (torch.float64,), 1), _dev_ptr(loss_row, "loss_row", (torch.float32,), n),
         _dev_ptr(grad, "grad", (torch.float32,), n), _dev_ptr(decision, "decision", (torch.uint8,), n),
         _u64(n_incorrect, "n_incorrect", 1), _u64(hist_pred, "hist_pred", r.m + 1), _stream(stream)))
+
+
+# ------------------------------------------------------------------ rebalanced sampler
+
+def sc_sample_workspace_bytes(rows: int) -> int:
+    return int(_lib.sc_sample_workspace_bytes(int(rows)))
+
+
+def sc_rebalance_sample(gt_mask, w, u, out, workspace=None, stream=None):
+    """Draw out.numel() rows with probability ∝ w[G_i] (u: float64 [2n] uniforms)."""
+    torch = _torch()
+    rows, n = gt_mask.numel(), out.numel()
+    if workspace is None:
+        workspace = torch.empty(sc_sample_workspace_bytes(rows), dtype=torch.uint8, device=gt_mask.device)
+    st = _lib.sc_rebalance_sample(_dev_ptr(gt_mask, "gt_mask", (torch.uint8,), rows), rows,
+                                  _dev_ptr(w, "w", (torch.float32,), 256), _dev_ptr(u, "u", (torch.float64,), 2 * n),
+                                  n, _dev_ptr(out, "out", (torch.int64,), n),
+                                  _dev_ptr(workspace, "workspace", (torch.uint8,)), workspace.numel(), _stream(stream))
+    if st != SC_OK:
+        raise ScError(st, _lib.sc_sample_last_error().decode())
+    return out

@@ -26,6 +26,7 @@ struct sc_context_s {
   uint32_t* d_ent = nullptr;
   int32_t* d_ent_off = nullptr;
   uint8_t* d_nlists = nullptr;
+  unsigned int* d_done = nullptr;  // completion counter of the fused hist+weights pre-pass
 };
 
 namespace {
@@ -205,8 +206,13 @@ sc_status run_eval(const sc_context_s* ctx, const sc_batch* b, const float* w, f
   const bool whole_rows = W * p.ld_bytes <= stage_cap && force_chunk == 0;
   // mapped labels in registers when whole rows fit a stage and |W| <= 1024
   int epl = 0;
-  if (whole_rows && ctx->max_ent <= 1024 && !(std::getenv("SC_EPL") && std::atoi(std::getenv("SC_EPL")) == 0))
-    epl = std::max(0, sc::eval_epl_for(ctx->max_ent));
+  // Lane-resident entries cut the per-row instruction count; they pay when the row is
+  // short per mapped label (measured: bf16 cfg2, 11 B/label, 1.6x faster), while the
+  // shared-list path streams f32 cfg2 (22 B/label) 1-3 % faster.
+  const bool compute_bound = p.ld_bytes < 16 * static_cast<int64_t>(std::max(ctx->max_ent, 1));
+  const char* epl_env = std::getenv("SC_EPL");
+  const bool want_epl = epl_env ? std::atoi(epl_env) != 0 : compute_bound;
+  if (whole_rows && ctx->max_ent <= 1024 && want_epl) epl = std::max(0, sc::eval_epl_for(ctx->max_ent));
   int64_t logits_region;
   p.ng = 1;
   if (epl > 0) {
@@ -385,6 +391,8 @@ sc_status sc_context_load(int32_t C, int32_t n_apps, const int32_t* n_lists, con
   if (!e) e = cudaMalloc(&ctx->d_ent, ent.size() * 4);
   if (!e) e = cudaMalloc(&ctx->d_ent_off, ent_off.size() * 4);
   if (!e) e = cudaMalloc(&ctx->d_nlists, nl.size());
+  if (!e) e = cudaMalloc(&ctx->d_done, sizeof(unsigned int));
+  if (!e) e = cudaMemset(ctx->d_done, 0, sizeof(unsigned int));
   if (!e) e = cudaMemcpy(ctx->d_cat, cat.data(), cat.size(), cudaMemcpyHostToDevice);
   if (!e) e = cudaMemcpy(ctx->d_ent, ent.data(), ent.size() * 4, cudaMemcpyHostToDevice);
   if (!e) e = cudaMemcpy(ctx->d_ent_off, ent_off.data(), ent_off.size() * 4, cudaMemcpyHostToDevice);
@@ -403,6 +411,7 @@ sc_status sc_context_free(sc_context ctx) {
   cudaFree(ctx->d_ent);
   cudaFree(ctx->d_ent_off);
   cudaFree(ctx->d_nlists);
+  cudaFree(ctx->d_done);
   delete ctx;
   return SC_OK;
 }
@@ -435,10 +444,11 @@ sc_status sc_loss_fwd_bwd(sc_context ctx, const sc_batch* batch, const float* w,
                   n_incorrect, hist_pred, hist_gt, true, static_cast<cudaStream_t>(stream));
 }
 
-sc_status sc_decision_hist(sc_context ctx, const sc_batch* b, uint64_t* hist_gt, uint8_t* gt_mask_out,
-                           sc_stream stream) {
+static sc_status run_hist(sc_context ctx, const sc_batch* b, uint64_t* hist_gt, uint8_t* gt_mask_out, float* w_out,
+                          sc_stream stream) {
   if (sc_status s = check_batch_common(ctx, b)) return s;
   if (!b->gt_off || !b->gt_lab) return fail(SC_ERR_INVALID_ARG, "sc_decision_hist needs gt_off and gt_lab");
+  if (w_out && !hist_gt) return fail(SC_ERR_INVALID_ARG, "weights need hist_gt");
   if (b->rows == 0 || (!hist_gt && !gt_mask_out)) return SC_OK;
   int dev = 0;
   if (cudaError_t e = cudaGetDevice(&dev)) return cuda_fail(e, "cudaGetDevice");
@@ -452,14 +462,30 @@ sc_status sc_decision_hist(sc_context ctx, const sc_batch* b, uint64_t* hist_gt,
   p.app = b->app;
   p.hist_gt = reinterpret_cast<unsigned long long*>(hist_gt);
   p.gt_mask_out = gt_mask_out;
+  p.w_out = w_out;
+  p.done_counter = ctx->d_done;
   const size_t hbytes = static_cast<size_t>(ctx->n_apps) * 256 * 8;
-  p.smem_hist = hbytes <= 48 * 1024;
-  const int64_t blocks = std::min<int64_t>((b->rows + 1023) / 1024, static_cast<int64_t>(di.sms) * 8);
+  p.smem_hist = hbytes <= 32 * 1024;
+  const int64_t per_block = 8 * 32 * 2;  // 8 warps x kHB blocks of 32 rows
+  // persistent: one wave (3 CTAs/SM at <= 85 registers), warps loop with a prefetch pipeline
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((b->rows + per_block - 1) / per_block,
+                                                                static_cast<int64_t>(di.sms) * 3));
   if (cudaError_t e = sc::launch_hist(p, static_cast<int>(blocks), p.smem_hist ? hbytes : 0,
                                       static_cast<cudaStream_t>(stream)))
     return cuda_fail(e, "hist kernel launch");
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return SC_OK;
+}
+
+sc_status sc_decision_hist(sc_context ctx, const sc_batch* b, uint64_t* hist_gt, uint8_t* gt_mask_out,
+                           sc_stream stream) {
+  return run_hist(ctx, b, hist_gt, gt_mask_out, nullptr, stream);
+}
+
+sc_status sc_decision_hist_weights(sc_context ctx, const sc_batch* b, uint64_t* hist_gt, uint8_t* gt_mask_out,
+                                   float* w, sc_stream stream) {
+  if (!w) return fail(SC_ERR_INVALID_ARG, "w is NULL");
+  return run_hist(ctx, b, hist_gt, gt_mask_out, w, stream);
 }
 
 sc_status sc_weights_from_hist(sc_context ctx, const uint64_t* hist_gt, float* w, sc_stream stream) {

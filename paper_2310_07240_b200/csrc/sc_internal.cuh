@@ -93,6 +93,8 @@ struct HistParams {
   unsigned long long* hist_gt;
   uint8_t* gt_mask_out;
   int32_t smem_hist;        // 1: CTA-private shared histogram (n_apps*256 counters)
+  float* w_out;             // optional: weights from the finished histogram (last CTA)
+  unsigned int* done_counter;  // zero between calls (reset by the last CTA)
 };
 
 // Launchers (sc_kernels.cu).  Return cudaError_t of the launch.

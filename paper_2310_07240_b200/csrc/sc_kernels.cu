@@ -1039,71 +1039,128 @@ __global__ void __launch_bounds__(256) gather_kernel(const EvalParams p) {
 
 // ------------------------------------------------------------------ GT-only pre-pass
 
-// Thread-per-row with instruction-level parallelism: each thread walks kHR rows at
-// once so the three dependent loads (offsets -> labels -> cat) of kHR rows overlap.
-constexpr int kHR = 4, kHL = 4;
+// Warp-cooperative: a warp takes kHB blocks of 32 consecutive rows at once.  The rows'
+// offsets are coalesced loads, their labels one contiguous span per block (the CSR keeps a
+// row's labels adjacent) loaded coalesced; every load of all kHB blocks is issued before
+// any is used, so a warp pays ~3 dependent latencies per 32·kHB rows.  Each label finds
+// its row through a per-warp owner table and ORs its lists into that row's G with a
+// shared atomic.  Optionally (w_out) the last CTA to finish turns the histogram into the
+// weights (a7), saving a launch when the batch is the whole dataset (one GPU).
+constexpr int kHB = 2;         // 32-row blocks in flight per warp
+constexpr int kSpanCap = 128;  // labels per block handled by the owner table (4 per row)
+constexpr int kSpanLd = kSpanCap / 32;
 
-__global__ void __launch_bounds__(256) hist_kernel(const HistParams p) {
+__device__ void weights_from_hist_block(const unsigned long long* hist, float* w, int n_apps);
+
+__global__ void __launch_bounds__(256, 3) hist_kernel(const HistParams p) {
   extern __shared__ unsigned long long sh_hist[];
-  const int lane = threadIdx.x & 31;
+  __shared__ uint8_t owner_s[8][kHB][kSpanCap];
+  __shared__ uint32_t g_s[8][kHB][32];
+  __shared__ uint32_t app_s[8][kHB][32];
+  __shared__ bool last_block;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int nbins = p.ctx.n_apps * 256;
-  if (p.smem_hist) {
+  if (p.smem_hist)
     for (int i = threadIdx.x; i < nbins; i += blockDim.x) sh_hist[i] = 0;
-    __syncthreads();
-  }
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
-  const int64_t start = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int64_t per_iter = stride * kHR;
-  const int64_t iters = (p.rows + per_iter - 1) / per_iter;  // uniform trip count for warp-wide intrinsics
-  for (int64_t it = 0; it < iters; ++it) {
-    int64_t row[kHR], o0[kHR], o1[kHR];
-    uint32_t a[kHR];
+  __syncthreads();
+  const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  // software pipeline: the next group's offsets are in flight while this group is processed
+  int64_t n_lo[kHB], n_hi[kHB];
+  uint32_t n_a[kHB];
+  auto prefetch = [&](int64_t r00) {
 #pragma unroll
-    for (int k = 0; k < kHR; ++k) {
-      row[k] = it * per_iter + k * stride + start;
-      const bool act = row[k] < p.rows;
-      o0[k] = act ? __ldg(p.gt_off + row[k]) : 0;
-      o1[k] = act ? __ldg(p.gt_off + row[k] + 1) : 0;
-      a[k] = (act && p.app) ? static_cast<uint32_t>(__ldg(p.app + row[k])) : 0u;
+    for (int b = 0; b < kHB; ++b) {
+      const int64_t row = r00 + b * 32 + lane;
+      const bool act = row < p.rows;
+      n_lo[b] = act ? __ldg(p.gt_off + row) : 0;
+      n_hi[b] = act ? __ldg(p.gt_off + row + 1) : 0;
+      n_a[b] = (act && p.app) ? static_cast<uint32_t>(__ldg(p.app + row)) : 0u;
     }
-    int32_t lab[kHR][kHL];
+  };
+  prefetch(gw * 32 * kHB);
+  for (int64_t r00 = gw * 32 * kHB; r00 < p.rows; r00 += nw * 32 * kHB) {
+    int64_t o_lo[kHB], o_hi[kHB], base[kHB], span[kHB];
+    uint32_t a[kHB];
+    unsigned amask[kHB];
 #pragma unroll
-    for (int k = 0; k < kHR; ++k)
+    for (int b = 0; b < kHB; ++b) {
+      o_lo[b] = n_lo[b];
+      o_hi[b] = n_hi[b];
+      a[b] = n_a[b];
+    }
+    prefetch(r00 + nw * 32 * kHB);
 #pragma unroll
-      for (int t = 0; t < kHL; ++t) lab[k][t] = (o0[k] + t < o1[k]) ? __ldg(p.gt_lab + o0[k] + t) : -1;
-    uint32_t key[kHR];
+    for (int b = 0; b < kHB; ++b) {
+      amask[b] = __ballot_sync(kFull, r00 + b * 32 + lane < p.rows);
+      const int last = amask[b] ? 31 - __clz(amask[b]) : 0;
+      base[b] = __shfl_sync(kFull, o_lo[b], 0);
+      span[b] = amask[b] ? __shfl_sync(kFull, o_hi[b], last) - base[b] : 0;
+    }
+    int32_t lab[kHB][kSpanLd];
 #pragma unroll
-    for (int k = 0; k < kHR; ++k) {
-      const uint8_t* cat = p.ctx.cat + static_cast<int64_t>(a[k]) * p.ctx.C;
-      uint32_t G = 0;
+    for (int b = 0; b < kHB; ++b)
 #pragma unroll
-      for (int t = 0; t < kHL; ++t) {
-        if (lab[k][t] >= 0) G |= label_lists(__ldg(cat + lab[k][t]), p.ctx.order);
+      for (int q = 0; q < kSpanLd; ++q) {
+        const int pos = q * 32 + lane;
+        lab[b][q] = (pos < span[b] && span[b] <= kSpanCap) ? __ldg(p.gt_lab + base[b] + pos) : -1;
       }
-      for (int64_t t = o0[k] + kHL; t < o1[k]; ++t)  // rows with more than kHL labels
-        G |= label_lists(__ldg(cat + __ldg(p.gt_lab + t)), p.ctx.order);
-      if (p.gt_mask_out && row[k] < p.rows) p.gt_mask_out[row[k]] = static_cast<uint8_t>(G);
-      key[k] = a[k] * 256u + G;
-    }
-    if (p.hist_gt) {
 #pragma unroll
-      for (int k = 0; k < kHR; ++k) {
-        const bool active = row[k] < p.rows;
-        const unsigned act = __ballot_sync(kFull, active);
-        if (active) {
-          const unsigned peers = __match_any_sync(act, key[k]);
-          if (lane == __ffs(peers) - 1) {
-            if (p.smem_hist) atomicAdd(sh_hist + key[k], static_cast<unsigned long long>(__popc(peers)));
-            else atomicAdd(p.hist_gt + key[k], static_cast<unsigned long long>(__popc(peers)));
-          }
+    for (int b = 0; b < kHB; ++b) {
+      for (int64_t t = o_lo[b]; t < o_hi[b] && span[b] <= kSpanCap; ++t)
+        owner_s[wib][b][t - base[b]] = static_cast<uint8_t>(lane);
+      g_s[wib][b][lane] = 0;
+      app_s[wib][b][lane] = a[b];
+    }
+    __syncwarp();
+#pragma unroll
+    for (int b = 0; b < kHB; ++b)
+#pragma unroll
+      for (int q = 0; q < kSpanLd; ++q)
+        if (lab[b][q] >= 0) {
+          const int own = owner_s[wib][b][q * 32 + lane];
+          const uint8_t* cat = p.ctx.cat + static_cast<int64_t>(app_s[wib][b][own]) * p.ctx.C;
+          const uint32_t lists = label_lists(__ldg(cat + lab[b][q]), p.ctx.order);
+          if (lists) atomicOr(&g_s[wib][b][own], lists);
+        }
+    __syncwarp();
+#pragma unroll
+    for (int b = 0; b < kHB; ++b) {
+      const int64_t row = r00 + b * 32 + lane;
+      const bool act = row < p.rows;
+      uint32_t G = g_s[wib][b][lane];
+      if (span[b] > kSpanCap) {  // very long label lists (warp-uniform): one row per lane
+        G = 0;
+        const uint8_t* cat = p.ctx.cat + static_cast<int64_t>(a[b]) * p.ctx.C;
+        for (int64_t t = o_lo[b]; t < o_hi[b]; ++t) G |= label_lists(__ldg(cat + __ldg(p.gt_lab + t)), p.ctx.order);
+      }
+      if (act && p.gt_mask_out) p.gt_mask_out[row] = static_cast<uint8_t>(G);
+      if (p.hist_gt && act) {
+        const uint32_t key = a[b] * 256u + G;
+        const unsigned peers = __match_any_sync(amask[b], key);
+        if (lane == __ffs(peers) - 1) {
+          if (p.smem_hist) atomicAdd(sh_hist + key, static_cast<unsigned long long>(__popc(peers)));
+          else atomicAdd(p.hist_gt + key, static_cast<unsigned long long>(__popc(peers)));
         }
       }
     }
+    __syncwarp();
   }
   if (p.smem_hist && p.hist_gt) {
     __syncthreads();
     for (int i = threadIdx.x; i < nbins; i += blockDim.x)
       if (sh_hist[i]) atomicAdd(p.hist_gt + i, sh_hist[i]);
+  }
+  if (p.w_out) {  // last CTA done: weights from the finished histogram
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last_block = atomicAdd(p.done_counter, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (last_block) {
+      __threadfence();
+      weights_from_hist_block(p.hist_gt, p.w_out, p.ctx.n_apps);
+      if (threadIdx.x == 0) *p.done_counter = 0;  // ready for the next call
+    }
   }
 }
 
@@ -1112,11 +1169,25 @@ __global__ void __launch_bounds__(256) hist_kernel(const HistParams p) {
 // One CTA per app.  F = subset-sum (zeta) transform of H over 8 bits, so
 // F[s] = #inputs whose G ⊆ s.  N(m) = M − F[~m] counts the inputs whose G
 // intersects m; N(0) = H[0] counts non-target inputs (:2014).
+__device__ void weights_one_app(const unsigned long long* H, float* w_app);
+
 __global__ void __launch_bounds__(256) weights_kernel(const unsigned long long* hist, float* w) {
+  weights_one_app(hist + static_cast<int64_t>(blockIdx.x) * 256, w + static_cast<int64_t>(blockIdx.x) * 256);
+}
+
+// All apps by one CTA (the hist kernel's last block).
+__device__ void weights_from_hist_block(const unsigned long long* hist, float* w, int n_apps) {
+  for (int a = 0; a < n_apps; ++a) {
+    weights_one_app(hist + static_cast<int64_t>(a) * 256, w + static_cast<int64_t>(a) * 256);
+    __syncthreads();
+  }
+}
+
+// One app, 256 threads (a thread per mask).
+__device__ void weights_one_app(const unsigned long long* H, float* w_app) {
   __shared__ unsigned long long F[256];
   const int m = threadIdx.x;
-  const unsigned long long* H = hist + static_cast<int64_t>(blockIdx.x) * 256;
-  const unsigned long long h = H[m];
+  const unsigned long long h = __ldcg(H + m);  // L2: the histogram was built by atomics
   F[m] = h;
 #pragma unroll
   for (int bit = 0; bit < 8; ++bit) {
@@ -1129,7 +1200,8 @@ __global__ void __launch_bounds__(256) weights_kernel(const unsigned long long* 
   __syncthreads();
   const unsigned long long M = F[255];
   const unsigned long long N = m == 0 ? h : M - F[(~m) & 255];
-  w[static_cast<int64_t>(blockIdx.x) * 256 + m] = N ? static_cast<float>(static_cast<double>(M) / static_cast<double>(N)) : 0.f;
+  w_app[m] = N ? static_cast<float>(static_cast<double>(M) / static_cast<double>(N)) : 0.f;
+  __syncthreads();
 }
 
 }  // namespace

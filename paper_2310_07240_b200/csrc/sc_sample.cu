@@ -1,0 +1,191 @@
+// sc_sample.cu — rebalanced training-data sampler.
+//
+// The strawman of PAPER.md:1989-1990 (abstract PAPER.md:19-20): re-train on a re-sampled
+// training set that rebalances the application's target classes.  Draws are i.i.d. with
+// q_i = w[G_i] / Σ_j w[G_j] (w = M/N).  Mapping of two uniforms to a row
+// (reading A24): rows grouped by G in ascending mask
+// order (row order inside a group), bucket weights count_m·w[m] summed in double in
+// ascending m; bucket = first m with u1·ΣW < cumulative W; row = number
+// min(count_m − 1, floor(u2·count_m)) of the bucket.
+//
+// Four launches: per-chunk mask counts, one-CTA scans (bucket starts, per-chunk offsets,
+// CDF in the oracle's summation order), a stable scatter (one warp per chunk, rows in
+// order), and the draws (one thread per draw, CDF in shared memory).
+#include "sc.h"
+
+#include <cuda_runtime.h>
+
+#include <string>
+
+namespace {
+
+constexpr unsigned kFull = 0xFFFFFFFFu;
+constexpr int64_t kChunk = 4096;  // rows per chunk of the counting sort
+
+thread_local std::string g_serr;
+
+sc_status sfail(sc_status st, const char* msg) {
+  g_serr = msg;
+  return st;
+}
+
+struct Workspace {  // carved from the caller's buffer
+  unsigned* chunk_cnt;   // [nchunks][256]
+  int64_t* chunk_off;    // [nchunks][256]  first slot of (chunk, mask) in bucket order
+  int64_t* count;        // [256]
+  int64_t* start;        // [256]
+  double* cum;           // [256]
+  int64_t* order;        // [rows] row ids in bucket order
+  int* status;           // [1]  0 ok, 1 all weights zero
+};
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+size_t layout(int64_t rows, Workspace* ws, uint8_t* base) {
+  const int64_t nch = (rows + kChunk - 1) / kChunk;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off = align_up(off + bytes, 256);
+    return base ? base + o : nullptr;
+  };
+  uint8_t* p;
+  p = take(sizeof(unsigned) * 256 * (nch > 0 ? nch : 1));
+  if (ws) ws->chunk_cnt = reinterpret_cast<unsigned*>(p);
+  p = take(sizeof(int64_t) * 256 * (nch > 0 ? nch : 1));
+  if (ws) ws->chunk_off = reinterpret_cast<int64_t*>(p);
+  p = take(sizeof(int64_t) * 256);
+  if (ws) ws->count = reinterpret_cast<int64_t*>(p);
+  p = take(sizeof(int64_t) * 256);
+  if (ws) ws->start = reinterpret_cast<int64_t*>(p);
+  p = take(sizeof(double) * 256);
+  if (ws) ws->cum = reinterpret_cast<double*>(p);
+  p = take(sizeof(int64_t) * (rows > 0 ? rows : 1));
+  if (ws) ws->order = reinterpret_cast<int64_t*>(p);
+  p = take(sizeof(int));
+  if (ws) ws->status = reinterpret_cast<int*>(p);
+  return off;
+}
+
+__global__ void __launch_bounds__(256) chunk_count_kernel(const uint8_t* gt_mask, int64_t rows, unsigned* chunk_cnt) {
+  __shared__ unsigned h[256];
+  h[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t lo = static_cast<int64_t>(blockIdx.x) * kChunk;
+  const int64_t hi = lo + kChunk < rows ? lo + kChunk : rows;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) atomicAdd(h + gt_mask[i], 1u);
+  __syncthreads();
+  chunk_cnt[static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x] = h[threadIdx.x];
+}
+
+// One CTA of 256 threads (a thread per mask).
+__global__ void __launch_bounds__(256) scan_kernel(const unsigned* chunk_cnt, int64_t nch, const float* w,
+                                                   Workspace ws) {
+  __shared__ int64_t cnt[256];
+  const int m = threadIdx.x;
+  int64_t c = 0;
+  for (int64_t k = 0; k < nch; ++k) c += chunk_cnt[k * 256 + m];
+  cnt[m] = c;
+  ws.count[m] = c;
+  __syncthreads();
+  if (m == 0) {  // sequential, ascending m: the oracle's summation order
+    int64_t s = 0;
+    double tot = 0.0;
+    for (int q = 0; q < 256; ++q) {
+      ws.start[q] = s;
+      s += cnt[q];
+      tot += static_cast<double>(cnt[q]) * static_cast<double>(w[q]);
+      ws.cum[q] = tot;
+    }
+    *ws.status = tot > 0.0 ? 0 : 1;
+  }
+  __syncthreads();
+  int64_t run = ws.start[m];
+  for (int64_t k = 0; k < nch; ++k) {
+    ws.chunk_off[k * 256 + m] = run;
+    run += chunk_cnt[k * 256 + m];
+  }
+}
+
+// One warp per chunk walks its rows in order: stable rank among equal masks.
+__global__ void __launch_bounds__(32) scatter_kernel(const uint8_t* gt_mask, int64_t rows, Workspace ws) {
+  __shared__ int64_t next[256];
+  const int lane = threadIdx.x;
+  for (int m = lane; m < 256; m += 32) next[m] = ws.chunk_off[static_cast<int64_t>(blockIdx.x) * 256 + m];
+  __syncwarp();
+  const int64_t lo = static_cast<int64_t>(blockIdx.x) * kChunk;
+  const int64_t hi = lo + kChunk < rows ? lo + kChunk : rows;
+  for (int64_t i0 = lo; i0 < hi; i0 += 32) {
+    const int64_t i = i0 + lane;
+    const bool act = i < hi;
+    const unsigned am = __ballot_sync(kFull, act);
+    if (act) {
+      const unsigned key = gt_mask[i];
+      const unsigned peers = __match_any_sync(am, key);
+      const int rank = __popc(peers & ((1u << lane) - 1u));
+      const int64_t slot = next[key] + rank;
+      ws.order[slot] = i;
+      __syncwarp(am);
+      if (lane == __ffs(peers) - 1) next[key] += __popc(peers);
+    }
+    __syncwarp();
+  }
+}
+
+__global__ void __launch_bounds__(256) draw_kernel(const double* u, int64_t n, Workspace ws, int64_t* out) {
+  __shared__ double cum[256];
+  __shared__ int64_t cnt[256], st[256];
+  cum[threadIdx.x] = ws.cum[threadIdx.x];
+  cnt[threadIdx.x] = ws.count[threadIdx.x];
+  st[threadIdx.x] = ws.start[threadIdx.x];
+  __syncthreads();
+  const double total = cum[255];
+  for (int64_t d = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; d < n;
+       d += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (!(total > 0.0)) { out[d] = -1; continue; }
+    const double t = u[2 * d] * total;
+    int lo = 0, hi = 255;  // first m with t < cum[m]
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (t < cum[mid]) hi = mid;
+      else lo = mid + 1;
+    }
+    const int64_t c = cnt[lo];
+    int64_t pos = static_cast<int64_t>(floor(u[2 * d + 1] * static_cast<double>(c)));
+    if (pos > c - 1) pos = c - 1;
+    out[d] = ws.order[st[lo] + pos];
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t sc_sample_workspace_bytes(int64_t rows) { return layout(rows < 0 ? 0 : rows, nullptr, nullptr) + 256; }
+
+sc_status sc_rebalance_sample(const uint8_t* gt_mask, int64_t rows, const float* w, const double* u, int64_t n,
+                              int64_t* out, void* workspace, size_t workspace_bytes, sc_stream stream) {
+  if (rows <= 0) return sfail(SC_ERR_INVALID_ARG, "rows must be > 0");
+  if (n < 0) return sfail(SC_ERR_INVALID_ARG, "n < 0");
+  if (!gt_mask || !w || !workspace || (n > 0 && (!u || !out))) return sfail(SC_ERR_INVALID_ARG, "NULL argument");
+  if (workspace_bytes < sc_sample_workspace_bytes(rows)) return sfail(SC_ERR_INVALID_ARG, "workspace too small");
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(workspace) + 255) & ~uintptr_t(255));
+  Workspace ws;
+  layout(rows, &ws, base);
+  const int64_t nch = (rows + kChunk - 1) / kChunk;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  chunk_count_kernel<<<static_cast<unsigned>(nch), 256, 0, st>>>(gt_mask, rows, ws.chunk_cnt);
+  scan_kernel<<<1, 256, 0, st>>>(ws.chunk_cnt, nch, w, ws);
+  scatter_kernel<<<static_cast<unsigned>(nch), 32, 0, st>>>(gt_mask, rows, ws);
+  if (n > 0) {
+    int64_t g = (n + 255) / 256;
+    if (g > 148 * 16) g = 148 * 16;
+    draw_kernel<<<static_cast<unsigned>(g), 256, 0, st>>>(u, n, ws, out);
+  }
+  if (cudaError_t e = cudaGetLastError()) return sfail(SC_ERR_CUDA, cudaGetErrorString(e));
+  return SC_OK;
+}
+
+const char* sc_sample_last_error(void) { return g_serr.c_str(); }
+
+}  // extern "C"

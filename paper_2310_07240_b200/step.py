@@ -16,7 +16,7 @@ from dataclasses import dataclass
 
 import torch
 
-from . import Batch, Context, sc_decision_hist, sc_loss_fwd_bwd, sc_weights_from_hist
+from . import Batch, Context, sc_decision_hist, sc_decision_hist_weights, sc_loss_fwd_bwd, sc_weights_from_hist
 
 
 def shard_range(rows: int, rank: int, world: int):
@@ -45,7 +45,7 @@ def allreduce_many_(tensors, group=None):
         return tensors
     import torch.distributed as dist
     cm = getattr(dist, "_coalescing_manager", None)
-    if cm is not None and tensors[0].is_cuda:
+    if cm is not None and tensors[0].is_cuda and dist.get_backend(group) == "nccl":
         with cm(group=group, device=tensors[0].device):
             for t in tensors:
                 dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
@@ -109,9 +109,12 @@ class Evaluator:
             grad_scale = 1.0 / max(1, global_rows if global_rows is not None else rows)
         self._acc.zero_()
         gt_batch = Batch(logits=None, gt_off=gt_off, gt_lab=gt_lab, app=app, rows=rows)
-        sc_decision_hist(ctx, gt_batch, hist_gt=o.hist_gt, gt_mask_out=o.gt_mask)
-        allreduce_(o.hist_gt, self.group)
-        sc_weights_from_hist(ctx, o.hist_gt, o.w)
+        if _pg_active(self.group) or na > 1:  # N_i needs the global histogram: allreduce in between
+            sc_decision_hist(ctx, gt_batch, hist_gt=o.hist_gt, gt_mask_out=o.gt_mask)
+            allreduce_(o.hist_gt, self.group)
+            sc_weights_from_hist(ctx, o.hist_gt, o.w)  # one CTA per application
+        else:                                  # one GPU, one app: weights from the pre-pass launch
+            sc_decision_hist_weights(ctx, gt_batch, o.hist_gt, o.w, gt_mask_out=o.gt_mask)
         sc_loss_fwd_bwd(ctx, Batch(logits=logits, gt_mask=o.gt_mask, app=app), w=o.w, grad_scale=grad_scale,
                         loss_sum=o.loss_sum, loss_row=o.loss_row, grad_idx=o.grad_idx, grad_val=o.grad_val,
                         grad_dense=o.grad_dense, decision=o.decision, n_incorrect=o.counts[:na],

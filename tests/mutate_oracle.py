@@ -35,6 +35,8 @@ MUTATIONS = [
     ("multi-select: y term sign", "ell += S(x->k, theta - Pj);", "ell += S(x->k, Pj - theta);"),
     ("multi-select: first list only", "if (z[x->list_labels[t]] > x->tau) { m |= 1u << j; break; }",
      "if (z[x->list_labels[t]] > x->tau) { m |= 1u << j; return m; }"),
+    ("sampler: weights ignored", "total += (double)count[m] * w[m];", "total += (double)count[m];"),
+    ("sampler: position from u1", "int64_t pos = (int64_t)floor(u2[i] * (double)c);", "int64_t pos = (int64_t)floor(u1[i] * (double)c);"),
     ("multi-select: shared label first list only", "if (x->list_labels[t] == c) { m |= 1u << j; break; }",
      "if (x->list_labels[t] == c) { m |= 1u << j; return m; }"),
 ]
@@ -53,7 +55,8 @@ def main():
             r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-m", "not gpu", "-p", "no:cacheprovider",
                                 "tests/test_oracle_paper.py", "tests/test_oracle_bruteforce.py",
                                 "tests/test_oracle_loss.py", "tests/test_oracle_weights.py",
-                                "tests/test_oracle_patterns.py"],
+                                "tests/test_oracle_patterns.py", "tests/test_oracle_ranges.py",
+                                "tests/test_oracle_sampler.py"],
                                cwd=ROOT, env=env, capture_output=True, text=True)
             killed = r.returncode != 0
             print(f"{'KILLED ' if killed else 'SURVIVED'}  {name}")

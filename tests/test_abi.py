@@ -14,7 +14,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def declared_functions():
     src = open(os.path.join(ROOT, "include", "sc.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"^\s*(?:sc_status|const char\*|uint64_t)\s+(sc_\w+)\s*\(", src, flags=re.M)))
+    return sorted(set(re.findall(r"^\s*(?:sc_status|const char\*|uint64_t|size_t)\s+(sc_\w+)\s*\(", src, flags=re.M)))
 
 
 def test_header_declares_the_survey_boundary():

@@ -313,3 +313,30 @@ def test_step_host_matches_device_step():
     assert torch.equal(out["counts"], ref_counts.cpu())
     assert torch.equal(out["hist_gt"], ref_hist.cpu())
     np.testing.assert_allclose(out["loss_sum"].numpy(), ref_loss.cpu().numpy(), rtol=1e-12)
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 4])
+def test_fused_hist_weights_matches_two_launches(cfg):
+    """sc_decision_hist_weights (weights from the pre-pass's last CTA) == hist + weights kernels;
+    repeated calls reuse the context's completion counter."""
+    torch, sc, synth, _ = _mods()
+    spec = synth.config_context(cfg)
+    wl = synth.Workload(spec, seed=cfg, layout=1)
+    b = wl.host_batch(0, 5000)
+    d = to_dev(b, "f32")
+    ctx = sc.Context(spec.C, spec.lists, multi_app=True)
+    na = spec.n_apps
+    app = d.get("app")
+    batch = sc.Batch(gt_off=d["gt_off"], gt_lab=d["gt_lab"], app=app, rows=5000)
+    h1 = torch.zeros(na * 256, dtype=torch.int64, device="cuda")
+    w1 = torch.empty(na * 256, dtype=torch.float32, device="cuda")
+    m1 = torch.empty(5000, dtype=torch.uint8, device="cuda")
+    sc.sc_decision_hist(ctx, batch, hist_gt=h1, gt_mask_out=m1)
+    sc.sc_weights_from_hist(ctx, h1, w1)
+    for rep in range(3):
+        h2 = torch.zeros(na * 256, dtype=torch.int64, device="cuda")
+        w2 = torch.full((na * 256,), -1.0, dtype=torch.float32, device="cuda")
+        m2 = torch.empty(5000, dtype=torch.uint8, device="cuda")
+        sc.sc_decision_hist_weights(ctx, batch, h2, w2, gt_mask_out=m2)
+        torch.cuda.synchronize()
+        assert torch.equal(h1, h2) and torch.equal(m1, m2) and torch.equal(w1, w2)
