@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--config", type=int, default=CFG, choices=[1, 2, 3, 4, 5],
                     help="BASELINE.json config (default 2, the metric's config; others for characterisation)")
     ap.add_argument("--kernel", default=None, choices=["tma", "gather"], help="force an eval kernel (default: auto)")
+    ap.add_argument("--mode", default="step", choices=["step", "all_apps"],
+                    help="step: the hot path; all_apps: one read, every application (NEXT f3, config 4)")
     ap.add_argument("--order", default="api_output", choices=["api_output", "app_choice", "multi_select"],
                     help="decision pattern (default: the north star's API-output order)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -302,6 +304,8 @@ def run_ours(args):
             dist.barrier()
 
     stream = torch.cuda.current_stream(dev)
+    if args.mode == "all_apps":
+        return run_all_apps(args, sc, ctx, logits, gt_off, gt_lab, B, dev, stream, rank)
     for _ in range(args.warmup):
         ev.step(logits, gt_off, gt_lab, app=app, global_rows=global_rows)
     torch.cuda.synchronize(dev)
@@ -403,6 +407,31 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+    return 0
+
+
+def run_all_apps(args, sc, ctx, logits, gt_off, gt_lab, B, dev, stream, rank):
+    """One read of the logits, every application (sc_decide_all_apps): row-app evaluations/s."""
+    import torch
+    A = ctx.n_apps
+    ni = torch.zeros(A, dtype=torch.int64, device=dev)
+    hp = torch.zeros(A * 256, dtype=torch.int64, device=dev)
+    batch = sc.Batch(logits=logits, gt_off=gt_off, gt_lab=gt_lab)
+    for _ in range(args.warmup):
+        sc.sc_decide_all_apps(ctx, batch, n_incorrect=ni, hist_pred=hp)
+    torch.cuda.synchronize(dev)
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record(stream)
+    for _ in range(args.steps):
+        sc.sc_decide_all_apps(ctx, batch, n_incorrect=ni, hist_pred=hp)
+    e.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = s.elapsed_time(e) / args.steps
+    if rank == 0:
+        print(json.dumps({"metric": "row-application evaluations/s (one read, every application)",
+                          "value": B * A / (ms / 1e3), "unit": "evaluations/s", "ms_per_step": ms, "rows": B,
+                          "apps": A, "dtype": args.dtype, "config": {"workload": workload_name(args.config, args.dtype)},
+                          "reread_equivalent_ms": None}), flush=True)
     return 0
 
 

@@ -200,6 +200,18 @@ sc_status sc_loss_fwd_bwd(sc_context ctx, const sc_batch* batch, const float* w,
                           float* grad_dense, uint8_t* decision, uint64_t* n_incorrect, uint64_t* hist_pred,
                           uint64_t* hist_gt, sc_stream stream);
 
+/* ---- One read, many contexts (NEXT f3) ------------------------------------------------
+ * sc_decide_all_apps — every row is evaluated under EVERY application of the context
+ * (the provider's what-if: which applications would these outputs mislead), reading the
+ * logits once.  API-output order only; batch->app and batch->gt_mask are ignored, the
+ * ground truth comes from gt_off/gt_lab (G differs per application).
+ *   n_incorrect  [n_apps] += per application, rows whose decision is incorrect (Eq. goal)
+ *   hist_pred    [n_apps*256] += per application decision histogram
+ *   decision     [rows*n_apps] uint8 (row-major) or NULL
+ * All applications' mapped labels must fit in shared memory (about 50K entries). */
+sc_status sc_decide_all_apps(sc_context ctx, const sc_batch* batch, uint64_t* n_incorrect, uint64_t* hist_pred,
+                             uint8_t* decision, sc_stream stream);
+
 /* ---- Value-ranges applications, NEXT f1 -------------------------
  * The API returns a score O_i per input; the application checks, in code order, whether
  * it lies in each of its ranges [lo_j, hi_j] (reading A22: closed ranges, the first

@@ -73,6 +73,8 @@ def _load():
     lib.sc_decision_hist.argtypes = [P, ctypes.POINTER(_CBatch), P, P, P]
     lib.sc_decision_hist_weights.restype = ctypes.c_int
     lib.sc_decision_hist_weights.argtypes = [P, ctypes.POINTER(_CBatch), P, P, P, P]
+    lib.sc_decide_all_apps.restype = ctypes.c_int
+    lib.sc_decide_all_apps.argtypes = [P, ctypes.POINTER(_CBatch), P, P, P, P]
     lib.sc_weights_from_hist.restype = ctypes.c_int
     lib.sc_weights_from_hist.argtypes = [P, P, P, P]
     lib.sc_loss_fwd_bwd.restype = ctypes.c_int
@@ -316,6 +318,18 @@ def sc_decision_hist(ctx: Context, batch: Batch, hist_gt=None, gt_mask_out=None,
     cb = batch._c()
     _check(_lib.sc_decision_hist(ctx.handle, ctypes.byref(cb), _u64(hist_gt, "hist_gt", ctx.n_apps * 256),
                                  _dev_ptr(gt_mask_out, "gt_mask_out", (torch.uint8,), cb.rows), _stream(stream)))
+
+
+def sc_decide_all_apps(ctx: Context, batch: Batch, n_incorrect=None, hist_pred=None, decision=None, stream=None):
+    """One read of the logits, every application of the context (provider what-if)."""
+    torch = _torch()
+    cb = batch._c()
+    cb.app = None
+    cb.gt_mask = None
+    _check(_lib.sc_decide_all_apps(ctx.handle, ctypes.byref(cb), _u64(n_incorrect, "n_incorrect", ctx.n_apps),
+                                   _u64(hist_pred, "hist_pred", ctx.n_apps * 256),
+                                   _dev_ptr(decision, "decision", (torch.uint8,), cb.rows * ctx.n_apps),
+                                   _stream(stream)))
 
 
 def sc_decision_hist_weights(ctx: Context, batch: Batch, hist_gt, w, gt_mask_out=None, stream=None):

@@ -1,0 +1,164 @@
+// sc_allapps.cu — "one read, many contexts".
+//
+// The provider's what-if: every row's logits are read from HBM once and evaluated under
+// EVERY application of the context (Multi-Choice, API-output order, PAPER.md:862,
+// :128-134, Eq. goal): per application, the decision, its correctness and
+// the decision histogram.  Reading the batch once per application would cost n_apps full
+// passes; here the bound moves from HBM to the shared-memory / issue rate.
+//
+// A persistent CTA per SM holds every application's mapped labels (sorted per app,
+// key = c << 8 | cat) in shared memory, double-buffers rows with TMA bulk copies, builds
+// G for all applications from the row's ground-truth labels and a label-major copy of
+// the category table (one coalesced 256-B read per label for 256 apps), then its 8 warps
+// take the applications round-robin: split maxima over the app's labels, two REDUX pairs,
+// decision, correctness, shared-memory counters; counters flushed once per CTA.
+#include "sc_internal.cuh"
+
+#include <cuda_runtime.h>
+#include <math_constants.h>
+
+namespace sc {
+namespace {
+
+constexpr unsigned kFull = 0xFFFFFFFFu;
+constexpr int kAAWarps = 8;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init1(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nAA_WAIT_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra AA_WAIT_%=;\n}\n" ::
+          "r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+                   "r"(smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ uint32_t ord_key(float z) {
+  const uint32_t u = __float_as_uint(z + 0.0f);
+  return u ^ (static_cast<uint32_t>(static_cast<int32_t>(u) >> 31) | 0x80000000u);
+}
+
+__device__ __forceinline__ void argmax_warp(float& z, uint32_t& k) {
+  const uint32_t o = (k == kNone) ? 0u : ord_key(z);
+  const uint32_t om = __reduce_max_sync(kFull, o);
+  k = __reduce_min_sync(kFull, (o == om) ? k : kNone);
+  z = om ? __uint_as_float((om & 0x80000000u) ? (om ^ 0x80000000u) : ~om) : -CUDART_INF_F;
+}
+
+__global__ void __launch_bounds__(kAAWarps * 32, 1) all_apps_kernel(const AllAppsParams p) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int A = p.ctx.n_apps;
+  // carve shared memory
+  uint8_t* rowbuf[2] = {sm, sm + p.row_bytes_pad};
+  uint32_t* ents = reinterpret_cast<uint32_t*>(sm + 2 * p.row_bytes_pad);
+  int32_t* eoff = reinterpret_cast<int32_t*>(ents + p.n_ent_total);
+  unsigned* cnt_inc = reinterpret_cast<unsigned*>(eoff + A + 1);
+  unsigned* cnt_pred = cnt_inc + A;                       // [A][16]
+  uint8_t* gs = reinterpret_cast<uint8_t*>(cnt_pred + A * 16);   // [A] G of the current row per app
+  uint8_t* nl = gs + A;                                   // [A] D'
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + p.bar_off);  // [2]
+  for (int i = tid; i < p.n_ent_total; i += blockDim.x) ents[i] = __ldg(p.ctx.ent + i);
+  for (int i = tid; i <= A; i += blockDim.x) eoff[i] = __ldg(p.ctx.ent_off + i);
+  for (int i = tid; i < A; i += blockDim.x) { cnt_inc[i] = 0; nl[i] = __ldg(p.ctx.nlists + i); }
+  for (int i = tid; i < A * 16; i += blockDim.x) cnt_pred[i] = 0;
+  if (tid == 0) { mbar_init1(bar); mbar_init1(bar + 1); }
+  __syncthreads();
+
+  const int64_t first = blockIdx.x, step = gridDim.x;
+  // prefetch the first row
+  if (tid == 0 && first < p.rows) {
+    mbar_expect(bar, p.copy_bytes);
+    bulk_copy(rowbuf[0], p.logits + first * p.ld_bytes, p.copy_bytes, bar);
+  }
+  uint32_t phase[2] = {0, 0};
+  int buf = 0;
+  for (int64_t row = first; row < p.rows; row += step, buf ^= 1) {
+    // next row into the other buffer (its previous row was fully consumed: barrier below)
+    const int64_t nxt = row + step;
+    if (tid == 0 && nxt < p.rows) {
+      mbar_expect(bar + (buf ^ 1), p.copy_bytes);
+      bulk_copy(rowbuf[buf ^ 1], p.logits + nxt * p.ld_bytes, p.copy_bytes, bar + (buf ^ 1));
+    }
+    // G for every app from the row's ground truth (label-major category table)
+    const int64_t g0 = __ldg(p.gt_off + row), g1 = __ldg(p.gt_off + row + 1);
+    for (int a = tid; a < A; a += blockDim.x) {
+      uint32_t G = 0;
+      for (int64_t t = g0; t < g1; ++t) {
+        const int32_t c = __ldg(p.gt_lab + t);
+        G |= label_lists(__ldg(p.catT + static_cast<int64_t>(c) * A + a), kApiOutput);
+      }
+      gs[a] = static_cast<uint8_t>(G);
+    }
+    mbar_wait_parity(bar + buf, phase[buf]);
+    phase[buf] ^= 1u;
+    __syncthreads();
+    const uint8_t* rb = rowbuf[buf];
+    for (int a = warp; a < A; a += kAAWarps) {
+      const uint32_t G = gs[a];
+      float zp = -CUDART_INF_F, zm = -CUDART_INF_F;
+      uint32_t kp = kNone, km = kNone;
+      for (int e = eoff[a] + lane; e < eoff[a + 1]; e += 32) {
+        const uint32_t key = ents[e];
+        const float z = p.bf16 ? __uint_as_float(static_cast<uint32_t>(
+                                     *reinterpret_cast<const uint16_t*>(rb + 2u * (key >> 8))) << 16)
+                               : *reinterpret_cast<const float*>(rb + 4u * (key >> 8));
+        if ((G >> (key & 0xFFu)) & 1u) {
+          if (z > zp) { zp = z; kp = key; }
+        } else {
+          if (z > zm) { zm = z; km = key; }
+        }
+      }
+      argmax_warp(zp, kp);
+      argmax_warp(zm, km);
+      if (lane == 0) {
+        const uint32_t D = nl[a];
+        const bool hp = kp != kNone, hm = km != kNone;
+        const bool take_p = hp && (!hm || zp > zm || (zp == zm && kp < km));
+        const float zs = take_p ? zp : zm;
+        const uint32_t ks = take_p ? kp : km;
+        const uint32_t dec = ((hp || hm) && zs > p.ctx.tau) ? (ks & 0xFFu) : D;
+        const bool ok = G ? (dec < D && ((G >> dec) & 1u)) : (dec == D);
+        if (!ok) atomicAdd(cnt_inc + a, 1u);
+        atomicAdd(cnt_pred + a * 16 + dec, 1u);
+        if (p.decision) p.decision[row * A + a] = static_cast<uint8_t>(dec);
+      }
+    }
+    __syncthreads();  // row buffer and gs are reused
+  }
+  for (int i = tid; i < A; i += blockDim.x)
+    if (cnt_inc[i] && p.n_incorrect) atomicAdd(p.n_incorrect + i, static_cast<unsigned long long>(cnt_inc[i]));
+  for (int i = tid; i < A * 16; i += blockDim.x)
+    if (cnt_pred[i] && p.hist_pred)
+      atomicAdd(p.hist_pred + (i >> 4) * 256 + (i & 15), static_cast<unsigned long long>(cnt_pred[i]));
+}
+
+}  // namespace
+
+cudaError_t launch_all_apps(const AllAppsParams& p, int grid, size_t smem, cudaStream_t st) {
+  cudaError_t e = cudaFuncSetAttribute(all_apps_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e) return e;
+  all_apps_kernel<<<grid, kAAWarps * 32, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace sc

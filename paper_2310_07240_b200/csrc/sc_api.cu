@@ -27,6 +27,8 @@ struct sc_context_s {
   int32_t* d_ent_off = nullptr;
   uint8_t* d_nlists = nullptr;
   unsigned int* d_done = nullptr;  // completion counter of the fused hist+weights pre-pass
+  uint8_t* d_catT = nullptr;       // [C][n_apps] label-major category table (all-apps pass)
+  int32_t n_ent_total = 0;
 };
 
 namespace {
@@ -392,6 +394,12 @@ sc_status sc_context_load(int32_t C, int32_t n_apps, const int32_t* n_lists, con
   if (!e) e = cudaMalloc(&ctx->d_ent_off, ent_off.size() * 4);
   if (!e) e = cudaMalloc(&ctx->d_nlists, nl.size());
   if (!e) e = cudaMalloc(&ctx->d_done, sizeof(unsigned int));
+  std::vector<uint8_t> catT(static_cast<size_t>(n_apps) * C);
+  for (int32_t a = 0; a < n_apps; ++a)
+    for (int32_t c = 0; c < C; ++c) catT[static_cast<size_t>(c) * n_apps + a] = cat[static_cast<size_t>(a) * C + c];
+  ctx->n_ent_total = ent_off[n_apps];
+  if (!e) e = cudaMalloc(&ctx->d_catT, catT.size());
+  if (!e) e = cudaMemcpy(ctx->d_catT, catT.data(), catT.size(), cudaMemcpyHostToDevice);
   if (!e) e = cudaMemset(ctx->d_done, 0, sizeof(unsigned int));
   if (!e) e = cudaMemcpy(ctx->d_cat, cat.data(), cat.size(), cudaMemcpyHostToDevice);
   if (!e) e = cudaMemcpy(ctx->d_ent, ent.data(), ent.size() * 4, cudaMemcpyHostToDevice);
@@ -412,6 +420,7 @@ sc_status sc_context_free(sc_context ctx) {
   cudaFree(ctx->d_ent_off);
   cudaFree(ctx->d_nlists);
   cudaFree(ctx->d_done);
+  cudaFree(ctx->d_catT);
   delete ctx;
   return SC_OK;
 }
@@ -486,6 +495,49 @@ sc_status sc_decision_hist_weights(sc_context ctx, const sc_batch* b, uint64_t* 
                                    float* w, sc_stream stream) {
   if (!w) return fail(SC_ERR_INVALID_ARG, "w is NULL");
   return run_hist(ctx, b, hist_gt, gt_mask_out, w, stream);
+}
+
+sc_status sc_decide_all_apps(sc_context ctx, const sc_batch* b, uint64_t* n_incorrect, uint64_t* hist_pred,
+                             uint8_t* decision, sc_stream stream) {
+  if (sc_status s = check_batch_common(ctx, b)) return s;
+  if (ctx->order != SC_ORDER_API_OUTPUT)
+    return fail(SC_ERR_UNSUPPORTED, "sc_decide_all_apps supports the API-output order");
+  if (!b->gt_off || !b->gt_lab) return fail(SC_ERR_INVALID_ARG, "sc_decide_all_apps needs gt_off and gt_lab");
+  if (b->dtype != SC_F32 && b->dtype != SC_BF16) return fail(SC_ERR_INVALID_ARG, "unknown dtype");
+  if (b->rows == 0) return SC_OK;
+  if (!b->logits) return fail(SC_ERR_INVALID_ARG, "logits is NULL");
+  const int64_t elt = b->dtype == SC_F32 ? 4 : 2;
+  if (b->ld < ctx->C || (b->ld * elt) % 16 || reinterpret_cast<uintptr_t>(b->logits) % 16)
+    return fail(SC_ERR_INVALID_ARG, "bad logits layout (ld >= C, ld*elt %% 16 == 0, 16-B aligned)");
+  int dev = 0;
+  if (cudaError_t e = cudaGetDevice(&dev)) return cuda_fail(e, "cudaGetDevice");
+  if (dev != ctx->device) return fail(SC_ERR_INVALID_ARG, "context belongs to another device");
+  DeviceInfo& di = device_info(dev);
+  sc::AllAppsParams p{};
+  p.ctx = dev_ctx(ctx);
+  p.catT = ctx->d_catT;
+  p.logits = static_cast<const uint8_t*>(b->logits);
+  p.rows = b->rows;
+  p.ld_bytes = b->ld * elt;
+  p.bf16 = b->dtype == SC_BF16;
+  p.copy_bytes = static_cast<uint32_t>(round_up(static_cast<int64_t>(ctx->C) * elt, 16));
+  p.row_bytes_pad = static_cast<int32_t>(round_up(p.copy_bytes, 128));
+  p.n_ent_total = ctx->n_ent_total;
+  p.gt_off = b->gt_off;
+  p.gt_lab = b->gt_lab;
+  p.n_incorrect = reinterpret_cast<unsigned long long*>(n_incorrect);
+  p.hist_pred = reinterpret_cast<unsigned long long*>(hist_pred);
+  p.decision = decision;
+  const int64_t A = ctx->n_apps;
+  int64_t off = 2 * static_cast<int64_t>(p.row_bytes_pad) + 4 * p.n_ent_total + 4 * (A + 1) + 4 * A + 64 * A + 2 * A;
+  p.bar_off = static_cast<int32_t>(round_up(off, 8));
+  const size_t smem = static_cast<size_t>(p.bar_off + 16);
+  if (smem > kSmemMax) return fail(SC_ERR_UNSUPPORTED, "contexts too large for the all-apps pass (shared memory)");
+  const int grid = static_cast<int>(std::min<int64_t>(b->rows, di.sms));
+  if (cudaError_t e = sc::launch_all_apps(p, grid, smem, static_cast<cudaStream_t>(stream)))
+    return cuda_fail(e, "all-apps kernel launch");
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return SC_OK;
 }
 
 sc_status sc_weights_from_hist(sc_context ctx, const uint64_t* hist_gt, float* w, sc_stream stream) {

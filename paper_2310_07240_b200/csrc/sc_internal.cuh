@@ -97,6 +97,25 @@ struct HistParams {
   unsigned int* done_counter;  // zero between calls (reset by the last CTA)
 };
 
+// "One read, many contexts" (sc_allapps.cu).
+struct AllAppsParams {
+  DevContext ctx;
+  const uint8_t* catT;      // [C][n_apps] label-major copy of the category table
+  const uint8_t* logits;
+  int64_t rows, ld_bytes;
+  int32_t bf16;
+  uint32_t copy_bytes;      // bytes of a row holding labels 0..C-1, rounded up to 16
+  int32_t row_bytes_pad;    // row buffer stride in shared memory
+  int32_t n_ent_total;      // entries of all applications
+  int32_t bar_off;
+  const int64_t* gt_off;
+  const int32_t* gt_lab;
+  unsigned long long* n_incorrect;
+  unsigned long long* hist_pred;
+  uint8_t* decision;        // [rows][n_apps] or NULL
+};
+cudaError_t launch_all_apps(const AllAppsParams& p, int grid, size_t smem, cudaStream_t st);
+
 // Launchers (sc_kernels.cu).  Return cudaError_t of the launch.
 // epl > 0: lane-resident entries (|W| <= 32*epl, whole rows per stage); 0: generic list path.
 cudaError_t launch_eval(const EvalParams& p, int epl, int grid, size_t smem, cudaStream_t st);

@@ -1,0 +1,41 @@
+"""GPU parity of "one read, many contexts" (sc_decide_all_apps, NEXT f3): the decisions
+of every row under every application equal the oracle's evaluation of each application
+separately; counters exact."""
+import numpy as np
+import pytest
+
+from conftest import gpu_available
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device")]
+
+
+@pytest.mark.parametrize("dtype,rows", [("f32", 600), ("bf16", 301)])
+def test_all_apps_parity(dtype, rows):
+    import torch
+    import paper_2310_07240_b200 as sc
+    import synth
+    from oracle import Oracle
+    from test_parity_gpu import to_dev
+    spec = synth.config_context(4)
+    wl = synth.Workload(spec, seed=4, dtype=dtype, layout=1)
+    b = wl.host_batch(1234, rows)
+    d = to_dev(b, dtype)
+    ctx = sc.Context(spec.C, spec.lists, multi_app=True)
+    A = spec.n_apps
+    ni = torch.zeros(A, dtype=torch.int64, device="cuda")
+    hp = torch.zeros(A * 256, dtype=torch.int64, device="cuda")
+    dec = torch.empty(rows * A, dtype=torch.uint8, device="cuda")
+    sc.sc_decide_all_apps(ctx, sc.Batch(logits=d["logits"], gt_off=d["gt_off"], gt_lab=d["gt_lab"]),
+                          n_incorrect=ni, hist_pred=hp, decision=dec)
+    torch.cuda.synchronize()
+    dec = dec.cpu().numpy().reshape(rows, A)
+    orc = Oracle.from_spec(spec)
+    ni_ref = np.zeros(A, np.uint64)
+    hp_ref = np.zeros(A * 256, np.uint64)
+    for a in range(0, A, 1):
+        r = orc.eval(b["logits"], b["gt_off"], b["gt_lab"], app=np.full(rows, a, np.uint16), want_loss=False)
+        np.testing.assert_array_equal(dec[:, a], r["decision"], err_msg=f"app {a}")
+        ni_ref += r["n_incorrect"]
+        hp_ref += r["hist_pred"]
+    np.testing.assert_array_equal(ni.cpu().numpy().astype(np.uint64), ni_ref)
+    np.testing.assert_array_equal(hp.cpu().numpy().astype(np.uint64), hp_ref)
