@@ -9,7 +9,7 @@
 // A persistent CTA per SM holds every application's mapped labels (sorted per app,
 // key = c << 8 | cat) in shared memory, double-buffers rows with TMA bulk copies, builds
 // G for all applications from the row's ground-truth labels and a label-major copy of
-// the category table (one coalesced 256-B read per label for 256 apps), then its 8 warps
+// the category table (one coalesced 256-B read per label for 256 apps), then its 32 warps
 // take the applications round-robin: split maxima over the app's labels, two REDUX pairs,
 // decision, correctness, shared-memory counters; counters flushed once per CTA.
 #include "sc_internal.cuh"
@@ -21,7 +21,7 @@ namespace sc {
 namespace {
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
-constexpr int kAAWarps = 8;
+constexpr int kAAWarps = 32;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
