@@ -254,6 +254,49 @@ sc_status sc_rebalance_sample(const uint8_t* gt_mask, int64_t rows, const float*
                               int64_t* out, void* workspace, size_t workspace_bytes, sc_stream stream);
 const char* sc_sample_last_error(void);
 
+/* ---- Classifier head fused with the evaluation (NEXT f4) ------------------------------
+ * The step upstream of the path: the API's logits are a linear head over features,
+ * z_i = x_i Wᵀ + b (x_i ∈ R^d, W ∈ R^{C×d}).  Labels outside 𝕎 are in no list, so they
+ * never pick a decision (the if-chain) and Eq. api_output
+ * only reads maxima over 𝕎: the head is compiled down to the |𝕎|
+ * mapped rows of W, computed on the tensor cores (tcgen05, bf16 operands, fp32
+ * accumulation in TMEM), and the decision, counters, loss and gradient are produced in the
+ * GEMM's epilogue.  The logits never reach HBM.  API-output order, one application.
+ *
+ * sc_head_load — compile the head for ctx: copies the mapped rows of W (in label order),
+ * their bias and keys into a device buffer the head owns (W and bias are not referenced
+ * afterwards).
+ *   weight  device bf16 (uint16 bit patterns) [C][ldw], ldw >= d;  d >= 1.
+ *   bias    device float [C] or NULL (0).
+ * SC_ERR_UNSUPPORTED: order != API_OUTPUT, n_apps != 1, or |𝕎| > 512.
+ * The copy is enqueued on `stream`; the head is usable on that stream when this returns. */
+typedef struct sc_head_s* sc_head;
+sc_status sc_head_load(sc_context ctx, const uint16_t* weight, int64_t ldw, int64_t d, const float* bias,
+                       sc_stream stream, sc_head* out);
+sc_status sc_head_free(sc_head head);
+/* d, and the number of head columns computed per row (|𝕎| padded to a multiple of 16). */
+sc_status sc_head_info(sc_head head, int64_t* d, int32_t* n_cols);
+
+typedef struct {
+  const uint16_t* x;       /* device bf16 [rows][ldx] features, ldx >= d, ldx % 8 == 0, 16-B aligned */
+  int64_t rows;
+  int64_t ldx;             /* elements */
+  const int64_t* gt_off;   /* ground truth as in sc_batch (CSR, rows+1) or NULL */
+  const int32_t* gt_lab;
+  const uint8_t* gt_mask;  /* or precomputed G_i (sc_decision_hist's gt_mask_out); wins over CSR */
+} sc_head_batch;
+
+/* sc_head_loss_fwd_bwd — z_i = x_i W_𝕎ᵀ + b_𝕎 (fp32 accumulation of bf16 products, then
+ * + bias in fp32), then exactly sc_loss_fwd_bwd's outputs for those logits (S = 2 slots;
+ * grad_idx holds label ids in [0, C), grad_val = dL_i/dz_c).  Every output may be NULL;
+ * the loss is computed when loss_sum, loss_row, grad_idx or grad_val is given, which needs
+ * the ground truth, as do n_incorrect and hist_gt.  The gradient w.r.t. x and W follows
+ * from grad_idx/grad_val (at most two rows of W per sample) and is the caller's. */
+sc_status sc_head_loss_fwd_bwd(sc_context ctx, sc_head head, const sc_head_batch* batch, const float* w,
+                               float grad_scale, double* loss_sum, float* loss_row, int32_t* grad_idx,
+                               float* grad_val, uint8_t* decision, uint64_t* n_incorrect, uint64_t* hist_pred,
+                               uint64_t* hist_gt, sc_stream stream);
+
 /* Thread-local text for the last non-OK status of this thread ("" if none). */
 const char* sc_last_error(void);
 

@@ -339,3 +339,26 @@ def sample(gt_mask, w, u1, u2):
     if rc != 0:
         raise ValueError("every weight is zero")
     return out[: len(u1)]
+
+
+# ------------------------------------------------------------------ classifier head (NEXT f4)
+
+def bf16_to_f64(bits) -> np.ndarray:
+    """bf16 bit patterns (uint16) -> float64: a bf16 is the upper half of an IEEE binary32."""
+    b = np.ascontiguousarray(bits, dtype=np.uint16)
+    return (b.astype(np.uint32) << np.uint32(16)).view(np.float32).astype(np.float64)
+
+
+def head_logits(x_bits, w_bits, bias=None) -> np.ndarray:
+    """z = x Wᵀ + b over ALL C labels — the linear classifier head whose outputs are the
+    API's confidences (the API output the application reads,
+    PAPER.md:862).  x [rows, d] and W [C, d] are bf16 bit patterns, bias [C] float or None.
+    Plain fp64: the products of two bf16 are exact in fp64 and the sum is a library matmul
+    (for the integer-valued workloads of synth.head_operands(kind="int") it is exact).
+    The fused GPU path computes only the mapped columns; the oracle keeps the definition."""
+    x = bf16_to_f64(x_bits)
+    W = bf16_to_f64(w_bits)
+    z = x @ W.T
+    if bias is not None:
+        z = z + np.asarray(bias, dtype=np.float64)[None, :]
+    return z

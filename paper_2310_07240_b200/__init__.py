@@ -20,7 +20,8 @@ from . import build as _build
 
 __all__ = [
     "ScError", "Context", "Batch", "sc_context_load", "sc_context_free", "sc_decide", "sc_decision_hist",
-    "sc_weights_from_hist", "sc_decision_hist_weights", "sc_loss_fwd_bwd", "sc_last_error", "sc_launch_count", "sc_last_kernel", "library_path",
+    "sc_weights_from_hist", "sc_decision_hist_weights", "sc_loss_fwd_bwd", "Head", "sc_head_load",
+    "sc_head_loss_fwd_bwd", "sc_last_error", "sc_launch_count", "sc_last_kernel", "library_path",
 ]
 
 SC_OK, SC_ERR_INVALID_ARG, SC_ERR_OOM, SC_ERR_CUDA, SC_ERR_UNSUPPORTED = range(5)
@@ -45,6 +46,17 @@ class _CBatch(ctypes.Structure):
         ("gt_lab", ctypes.c_void_p),
         ("gt_mask", ctypes.c_void_p),
         ("app", ctypes.c_void_p),
+    ]
+
+
+class _CHeadBatch(ctypes.Structure):
+    _fields_ = [
+        ("x", ctypes.c_void_p),
+        ("rows", ctypes.c_int64),
+        ("ldx", ctypes.c_int64),
+        ("gt_off", ctypes.c_void_p),
+        ("gt_lab", ctypes.c_void_p),
+        ("gt_mask", ctypes.c_void_p),
     ]
 
 
@@ -104,6 +116,14 @@ def _load():
     lib.sc_rebalance_sample.argtypes = [P, I64, P, P, I64, P, P, ctypes.c_size_t, P]
     lib.sc_sample_last_error.restype = ctypes.c_char_p
     lib.sc_sample_last_error.argtypes = []
+    lib.sc_head_load.restype = ctypes.c_int
+    lib.sc_head_load.argtypes = [P, P, I64, I64, P, P, ctypes.POINTER(P)]
+    lib.sc_head_free.restype = ctypes.c_int
+    lib.sc_head_free.argtypes = [P]
+    lib.sc_head_info.restype = ctypes.c_int
+    lib.sc_head_info.argtypes = [P, ctypes.POINTER(I64), ctypes.POINTER(I32)]
+    lib.sc_head_loss_fwd_bwd.restype = ctypes.c_int
+    lib.sc_head_loss_fwd_bwd.argtypes = [P, P, ctypes.POINTER(_CHeadBatch), P, F, P, P, P, P, P, P, P, P, P]
     return lib
 
 
@@ -367,6 +387,77 @@ def sc_loss_fwd_bwd(ctx: Context, batch: Batch, w=None, grad_scale: float = 1.0,
         _u64(n_incorrect, "n_incorrect", ctx.n_apps),
         _u64(hist_pred, "hist_pred", ctx.n_apps * 256),
         _u64(hist_gt, "hist_gt", ctx.n_apps * 256), _stream(stream)))
+
+
+# ------------------------------------------------------------------ classifier head (NEXT f4)
+
+class Head:
+    """Handle to a compiled classifier head (``sc_head``): the mapped rows of W (bf16,
+    [C, d]) and their bias, for the fused head GEMM + evaluation."""
+
+    def __init__(self, ctx: Context, weight, bias=None, stream=None):
+        torch = _torch()
+        if weight.dim() != 2 or weight.shape[0] != ctx.C:
+            raise ValueError("weight must be [C, d]")
+        if weight.stride(1) != 1:
+            raise ValueError("weight rows must be contiguous")
+        h = ctypes.c_void_p()
+        _check(_lib.sc_head_load(ctx.handle, _dev_ptr(weight, "weight", (torch.bfloat16,)), weight.stride(0),
+                                 weight.shape[1], _dev_ptr(bias, "bias", (torch.float32,), ctx.C),
+                                 _stream(stream), ctypes.byref(h)))
+        self._h = h
+        self.ctx = ctx
+
+    @property
+    def handle(self):
+        return self._h
+
+    def info(self):
+        """-> (d, n_cols): feature width and head columns computed per row."""
+        d, n = ctypes.c_int64(), ctypes.c_int32()
+        _check(_lib.sc_head_info(self._h, ctypes.byref(d), ctypes.byref(n)))
+        return d.value, n.value
+
+    def free(self):
+        if getattr(self, "_h", None):
+            _lib.sc_head_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def sc_head_load(ctx: Context, weight, bias=None, stream=None) -> Head:
+    return Head(ctx, weight, bias, stream)
+
+
+def sc_head_loss_fwd_bwd(ctx: Context, head: Head, x, gt_off=None, gt_lab=None, gt_mask=None, w=None,
+                         grad_scale: float = 1.0, loss_sum=None, loss_row=None, grad_idx=None, grad_val=None,
+                         decision=None, n_incorrect=None, hist_pred=None, hist_gt=None, stream=None):
+    """Head GEMM (tcgen05) with the evaluation in its epilogue: x bf16 [rows, d]."""
+    torch = _torch()
+    if x.dim() != 2 or x.stride(1) != 1:
+        raise ValueError("x must be a 2-D bf16 tensor with contiguous rows")
+    if not x.is_cuda or x.dtype != torch.bfloat16:
+        raise TypeError("x must be a CUDA bf16 tensor (no CPU fallback)")
+    rows = x.shape[0]
+    cb = _CHeadBatch(x.data_ptr(), rows, x.stride(0) if rows > 1 else max(x.stride(0), x.shape[1]),
+                     _dev_ptr(gt_off, "gt_off", (torch.int64,), rows + 1) if gt_off is not None else None,
+                     _dev_ptr(gt_lab, "gt_lab", (torch.int32,)) if gt_lab is not None else None,
+                     _dev_ptr(gt_mask, "gt_mask", (torch.uint8,), rows) if gt_mask is not None else None)
+    _check(_lib.sc_head_loss_fwd_bwd(
+        ctx.handle, head.handle, ctypes.byref(cb),
+        _dev_ptr(w, "w", (torch.float32,), 256), float(grad_scale),
+        _dev_ptr(loss_sum, "loss_sum", (torch.float64,), 1),
+        _dev_ptr(loss_row, "loss_row", (torch.float32,), rows),
+        _dev_ptr(grad_idx, "grad_idx", (torch.int32,), 2 * rows),
+        _dev_ptr(grad_val, "grad_val", (torch.float32,), 2 * rows),
+        _dev_ptr(decision, "decision", (torch.uint8,), rows),
+        _u64(n_incorrect, "n_incorrect", 1), _u64(hist_pred, "hist_pred", 256), _u64(hist_gt, "hist_gt", 256),
+        _stream(stream)))
 
 
 # ------------------------------------------------------------------ value ranges (PAPER.md:2058-2065)

@@ -1,6 +1,7 @@
 // sc_api.cu — host side of libsc: the C ABI declared in include/sc.h.
 // Validation, the context compile (a1), launch configuration and dispatch.
 #include "sc.h"
+#include "sc_host.h"
 #include "sc_internal.cuh"
 
 #include <atomic>
@@ -14,22 +15,6 @@
 
 #include <cuda_runtime.h>
 
-struct sc_context_s {
-  int32_t C = 0, n_apps = 0, max_ent = 0;
-  int32_t order = 0;
-  float tau = 0.f, theta = 0.5f, k = 1.f;
-  int device = 0;
-  std::vector<int32_t> nlists, n_mapped;
-  int64_t touched_sectors[2] = {0, 0};  // sum over apps of 32-B sectors holding mapped labels (f32, bf16)
-  int64_t touched_lines[2] = {0, 0};    // same for 128-B lines (the granularity HBM is read at, measured)
-  uint8_t* d_cat = nullptr;
-  uint32_t* d_ent = nullptr;
-  int32_t* d_ent_off = nullptr;
-  uint8_t* d_nlists = nullptr;
-  unsigned int* d_done = nullptr;  // completion counter of the fused hist+weights pre-pass
-  uint8_t* d_catT = nullptr;       // [C][n_apps] label-major category table (all-apps pass)
-  int32_t n_ent_total = 0;
-};
 
 namespace {
 
@@ -306,6 +291,27 @@ sc_status run_eval(const sc_context_s* ctx, const sc_batch* b, const float* w, f
 }
 
 }  // namespace
+
+namespace sc {
+sc_status set_error(sc_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+void note_launch(const char* kernel) {
+  g_last_kernel = kernel;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+int device_sms() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return device_info(dev).sms;
+}
+}  // namespace sc
 
 extern "C" {
 

@@ -1,0 +1,32 @@
+// sc_host.h — host-side state shared by the libsc translation units (not part of the ABI).
+#pragma once
+#include "sc.h"
+
+#include <cstdint>
+#include <vector>
+
+struct sc_context_s {
+  int32_t C = 0, n_apps = 0, max_ent = 0;
+  int32_t order = 0;
+  float tau = 0.f, theta = 0.5f, k = 1.f;
+  int device = 0;
+  std::vector<int32_t> nlists, n_mapped;
+  int64_t touched_sectors[2] = {0, 0};  // sum over apps of 32-B sectors holding mapped labels (f32, bf16)
+  int64_t touched_lines[2] = {0, 0};    // same for 128-B lines (the granularity HBM is read at, measured)
+  uint8_t* d_cat = nullptr;
+  uint32_t* d_ent = nullptr;
+  int32_t* d_ent_off = nullptr;
+  uint8_t* d_nlists = nullptr;
+  unsigned int* d_done = nullptr;  // completion counter of the fused hist+weights pre-pass
+  uint8_t* d_catT = nullptr;       // [C][n_apps] label-major category table (all-apps pass)
+  int32_t n_ent_total = 0;
+};
+
+namespace sc {
+// Record the message returned by sc_last_error(); returns st.
+sc_status set_error(sc_status st, const char* fmt, ...);
+// Count one kernel launch of libsc (sc_launch_count) and name it (sc_last_kernel).
+void note_launch(const char* kernel);
+// Streaming multiprocessors of the current device.
+int device_sms();
+}  // namespace sc

@@ -13,265 +13,13 @@
 //
 // hist_kernel: the ground-truth-only pre-pass (a2 + a6 for the mask histogram).
 // weights_kernel: a7, M/N from the mask histogram via a subset-sum (zeta) transform.
-#include "sc_internal.cuh"
+#include "sc_device.cuh"
 
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
 namespace sc {
 namespace {
-
-constexpr unsigned kFull = 0xFFFFFFFFu;
-
-// ------------------------------------------------------------------ PTX helpers
-
-__device__ __forceinline__ uint32_t smem_addr(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ void fence_mbar_init() {
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
-               : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "SC_WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra SC_WAIT_%=;\n"
-      "}\n" ::"r"(smem_addr(bar)),
-      "r"(parity)
-      : "memory");
-}
-
-__device__ __forceinline__ uint64_t evict_first_policy() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-
-// 1-D bulk copy global -> shared (TMA engine), completion counted on `bar`.
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
-                                         uint64_t pol) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
-          "r"(smem_addr(dst)),
-      "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(pol)
-      : "memory");
-}
-
-__device__ __forceinline__ void st_cs_f4(float* p, float4 v) {
-  asm volatile("st.global.cs.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
-               : "memory");
-}
-
-// ------------------------------------------------------------------ math (fp32, no fast-math)
-
-// σ(z) = 1/(1+e^{-z}) without overflow (reading A2).
-__device__ __forceinline__ float sigmoid_f(float z) {
-  if (z >= 0.f) return 1.f / (1.f + expf(-z));
-  const float e = expf(z);
-  return e / (1.f + e);
-}
-
-// σ'(z) = t/(1+t)^2, t = e^{-|z|}: no cancellation (σ(1-σ) in fp32 loses digits for |z| > 8).
-__device__ __forceinline__ float dsigmoid_f(float z) {
-  const float t = expf(-fabsf(z));
-  const float d = 1.f + t;
-  return t / (d * d);
-}
-
-// Lexicographic max over (z, -label): keys are c << 8 | cat, ordered like c.
-__device__ __forceinline__ bool beats(float zo, uint32_t ko, float z, uint32_t k) {
-  return zo > z || (zo == z && ko < k);
-}
-
-__device__ __forceinline__ float load_logit(const uint8_t* rowp, uint32_t col, int bf16) {
-  if (bf16) return __uint_as_float(static_cast<uint32_t>(*reinterpret_cast<const uint16_t*>(rowp + 2u * col)) << 16);
-  return *reinterpret_cast<const float*>(rowp + 4u * col);
-}
-
-// G_i from the CSR ground truth (a2): OR of 1 << cat[c] over ŷ_i.
-__device__ __forceinline__ uint32_t warp_gt_mask(const EvalParams& p, int64_t row, uint32_t a, int lane) {
-  const int64_t b = __ldg(p.gt_off + row), e = __ldg(p.gt_off + row + 1);
-  uint32_t G = 0;
-  const uint8_t* cat = p.ctx.cat + static_cast<int64_t>(a) * p.ctx.C;
-  for (int64_t t = b + lane; t < e; t += 32) G |= label_lists(__ldg(cat + __ldg(p.gt_lab + t)), p.ctx.order);
-  return __reduce_or_sync(kFull, G);
-}
-
-// ------------------------------------------------------------------ per-warp row batch
-
-// Results of up to 32 reduced rows, one row per lane, finished together.
-struct RowBatch {
-  float zp, zm;      // max logit over 𝒲_i (P⁺ side) and over 𝕎∖𝒲_i (P⁻ side)
-  uint32_t kp, km;   // their keys (label << 8 | cat), kNone if the set is empty
-  uint32_t G, app;
-  int64_t row;
-  int n;             // rows held (warp-uniform)
-};
-
-// a3-a9 epilogue for the rows in the batch: decision, correctness, loss and
-// gradient; per-row outputs and warp-aggregated counter atomics.
-__device__ __forceinline__ void finish_batch(const EvalParams& p, RowBatch& b, const float* wtab_smem, int lane) {
-  const bool active = lane < b.n;
-  const unsigned act = __ballot_sync(kFull, active);
-  const float tau = p.ctx.tau;
-  uint32_t dec = 0, correct = 1;
-  float L = 0.f, g0 = 0.f, g1 = 0.f;
-  int32_t i0 = -1, i1 = -1;
-  if (active) {
-    const uint32_t D = __ldg(p.ctx.nlists + b.app);
-    const bool has_p = b.kp != kNone, has_m = b.km != kNone;
-    const bool take_p = has_p && (!has_m || beats(b.zp, b.kp, b.zm, b.km));
-    const float zs = take_p ? b.zp : b.zm;
-    const uint32_t ks = take_p ? b.kp : b.km;
-    // a3: first mapped label in confidence order, if it is an API output (z > tau)
-    dec = ((has_p || has_m) && zs > tau) ? (ks & 0xFFu) : D;
-    const bool y = b.G != 0;
-    // a5: Decision(API(x)) ∈ Decision(ŷ) (reading A7)
-    correct = y ? (dec < D && ((b.G >> dec) & 1u)) : (dec == D);
-    if (p.decision) p.decision[b.row] = static_cast<uint8_t>(dec);
-    if (p.want_loss) {
-      // a8/a9: Eq. api_output and its gradient
-      const float wi = p.w ? (wtab_smem ? wtab_smem[b.G] : __ldg(p.w + b.app * 256u + b.G)) : 1.f;
-      const float k = p.ctx.k;
-      if (y && has_p) {  // y_i = 1 implies 𝒲_i ≠ ∅ for a G consistent with the context
-        const float pp = sigmoid_f(b.zp);
-        const bool m_over = has_m && b.zm > tau;
-        const float am = m_over ? sigmoid_f(b.zm) : p.ctx.theta;  // max(P⁻, θ)
-        const float x = am - pp;
-        const float ell = sigmoid_f(k * x);                          // S(x)
-        const float ds = k * dsigmoid_f(k * x);                      // S'(x)
-        L = wi * ell;
-        g0 = -wi * ds * dsigmoid_f(b.zp) * p.grad_scale;
-        i0 = static_cast<int32_t>(b.kp >> 8);
-        if (m_over) {
-          g1 = wi * ds * dsigmoid_f(b.zm) * p.grad_scale;
-          i1 = static_cast<int32_t>(b.km >> 8);
-        }
-      } else if (!y && has_m) {
-        const float x = sigmoid_f(b.zm) - p.ctx.theta;               // P⁻ − θ
-        const float ell = sigmoid_f(k * x);
-        const float ds = k * dsigmoid_f(k * x);
-        L = wi * ell;
-        g1 = wi * ds * dsigmoid_f(b.zm) * p.grad_scale;
-        i1 = static_cast<int32_t>(b.km >> 8);
-      }
-      if (p.loss_row) p.loss_row[b.row] = L;
-      if (p.grad_idx) {
-        p.grad_idx[2 * b.row] = i0;
-        p.grad_idx[2 * b.row + 1] = i1;
-      }
-      if (p.grad_val) {
-        p.grad_val[2 * b.row] = g0;
-        p.grad_val[2 * b.row + 1] = g1;
-      }
-    }
-  }
-  // a6 / a5 counters: one atomic per distinct (app, bin) in the warp.
-  if (p.hist_pred && active) {
-    const uint32_t key = b.app * 256u + dec;
-    const unsigned peers = __match_any_sync(act, key);
-    if (lane == __ffs(peers) - 1) atomicAdd(p.hist_pred + key, static_cast<unsigned long long>(__popc(peers)));
-  }
-  if (p.has_gt) {
-    if (p.hist_gt && active) {
-      const uint32_t key = b.app * 256u + b.G;
-      const unsigned peers = __match_any_sync(act, key);
-      if (lane == __ffs(peers) - 1) atomicAdd(p.hist_gt + key, static_cast<unsigned long long>(__popc(peers)));
-    }
-    const unsigned inc = __ballot_sync(kFull, active && !correct);
-    if (p.n_incorrect && (inc >> lane & 1u)) {
-      const unsigned peers = __match_any_sync(inc, b.app);
-      if (lane == __ffs(peers) - 1) atomicAdd(p.n_incorrect + b.app, static_cast<unsigned long long>(__popc(peers)));
-    }
-    if (p.loss_sum && p.want_loss) {
-      const uint32_t app0 = __shfl_sync(kFull, b.app, 0);
-      if (__all_sync(kFull, !active || b.app == app0)) {
-        double s = active ? static_cast<double>(L) : 0.0;
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(kFull, s, off);
-        if (lane == 0) atomicAdd(p.loss_sum + app0, s);
-      } else if (active) {
-        atomicAdd(p.loss_sum + b.app, static_cast<double>(L));
-      }
-    }
-  }
-  // dense gradient: the warp writes each row coalesced (zeros + <= 2 entries)
-  if (p.grad_dense) {
-    for (int t = 0; t < b.n; ++t) {
-      const int64_t row = __shfl_sync(kFull, b.row, t);
-      const int32_t c0 = __shfl_sync(kFull, i0, t), c1 = __shfl_sync(kFull, i1, t);
-      const float v0 = __shfl_sync(kFull, g0, t), v1 = __shfl_sync(kFull, g1, t);
-      float* out = p.grad_dense + row * p.ld;
-      const int64_t nv = p.ld >> 2;
-      for (int64_t v = lane; v < nv; v += 32) {
-        float e[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int64_t c = 4 * v + q;
-          if (c == c0) e[q] = v0;
-          if (c == c1) e[q] = v1;
-        }
-        st_cs_f4(out + 4 * v, make_float4(e[0], e[1], e[2], e[3]));
-      }
-    }
-  }
-  b.n = 0;
-}
-
-__device__ __forceinline__ void deposit(RowBatch& b, int lane, float zp, uint32_t kp, float zm, uint32_t km,
-                                        uint32_t G, uint32_t a, int64_t row) {
-  if (lane == b.n) {
-    b.zp = zp; b.kp = kp; b.zm = zm; b.km = km; b.G = G; b.app = a; b.row = row;
-  }
-  ++b.n;
-}
-
-// Shared-memory loads by 32-bit shared address (no generic-to-shared conversion per load).
-// volatile keeps them after the mbarrier wait that makes the TMA bytes visible.
-template <bool BF16>
-__device__ __forceinline__ float lds_z(uint32_t a) {
-  if constexpr (BF16) {
-    unsigned short v;
-    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
-    return __uint_as_float(static_cast<uint32_t>(v) << 16);
-  } else {
-    float v;
-    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
-    return v;
-  }
-}
-__device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
-  unsigned short v;
-  asm volatile("ld.shared.u8 %0, [%1];" : "=h"(v) : "r"(a));
-  return v;
-}
-__device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
-  unsigned short v;
-  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
-  return v;
-}
-__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
-  uint32_t v;
-  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
-  return v;
-}
 
 // ------------------------------------------------------------------ warp arg max (REDUX)
 

@@ -282,3 +282,46 @@ class Workload:
 def _ck(rc: int):
     if rc != 0:
         raise RuntimeError(f"synth CUDA launch failed: cudaError {rc}")
+
+
+# ------------------------------------------------------------------ classifier-head operands (NEXT f4)
+
+def f32_to_bf16_bits(a) -> np.ndarray:
+    """Round float32 to bf16 (round to nearest even) and return the bit patterns."""
+    u = np.ascontiguousarray(a, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    r = (u + 0x7FFF + ((u >> 16) & 1)) >> 16
+    return r.astype(np.uint16)
+
+
+def head_operands(C: int, d: int, rows: int, seed: int, kind: str = "int"):
+    """Seeded features x [rows, d] and head weights W [C, d] (bf16 bit patterns, uint16)
+    and bias [C] (float32).
+
+    kind "int":    x ∈ {-3..3}/8, W ∈ {-3..3}/16, bias ∈ {-64..64}/128.  Every product is a
+                   multiple of 2^-7 and every partial sum stays below 2^17·2^-7, so all fp32
+                   summation orders give the exact logits (and ties are frequent).
+    kind "normal": x ~ N(0, 1), W ~ N(0, 1/d), bias ~ N(0, 0.1²), rounded to bf16.
+    """
+    rng = np.random.default_rng(seed)
+    if kind == "int":
+        x = rng.integers(-3, 4, size=(rows, d)).astype(np.float32) / 8
+        W = rng.integers(-3, 4, size=(C, d)).astype(np.float32) / 16
+        b = rng.integers(-64, 65, size=C).astype(np.float32) / 128
+    elif kind == "normal":
+        x = rng.standard_normal((rows, d), dtype=np.float32)
+        W = rng.standard_normal((C, d), dtype=np.float32) / np.float32(np.sqrt(d))
+        b = (rng.standard_normal(C, dtype=np.float32) * np.float32(0.1)).astype(np.float32)
+    else:
+        raise ValueError(kind)
+    return f32_to_bf16_bits(x), f32_to_bf16_bits(W), b
+
+
+def head_operands_device(C: int, d: int, rows: int, seed: int, device="cuda"):
+    """Full-size "normal" operands generated on the GPU (torch generator; bench only)."""
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    x = torch.randn((rows, d), generator=g, device=device, dtype=torch.float32).to(torch.bfloat16)
+    W = (torch.randn((C, d), generator=g, device=device, dtype=torch.float32) / d ** 0.5).to(torch.bfloat16)
+    b = torch.randn((C,), generator=g, device=device, dtype=torch.float32) * 0.1
+    return x, W, b
