@@ -43,8 +43,10 @@ def parse():
     ap.add_argument("--config", type=int, default=CFG, choices=[1, 2, 3, 4, 5],
                     help="BASELINE.json config (default 2, the metric's config; others for characterisation)")
     ap.add_argument("--kernel", default=None, choices=["tma", "gather"], help="force an eval kernel (default: auto)")
-    ap.add_argument("--mode", default="step", choices=["step", "all_apps"],
-                    help="step: the hot path; all_apps: one read, every application (NEXT f3, config 4)")
+    ap.add_argument("--mode", default="step", choices=["step", "all_apps", "head"],
+                    help="step: the hot path; all_apps: one read, every application (NEXT f3, config 4); "
+                         "head: classifier-head GEMM fused with the evaluation (NEXT f4)")
+    ap.add_argument("--d", type=int, default=2048, help="--mode head: feature width (ResNet-50 penultimate = 2048)")
     ap.add_argument("--order", default="api_output", choices=["api_output", "app_choice", "multi_select"],
                     help="decision pattern (default: the north star's API-output order)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -304,6 +306,8 @@ def run_ours(args):
             dist.barrier()
 
     stream = torch.cuda.current_stream(dev)
+    if args.mode == "head":
+        return run_head(args, sc, ctx, spec, gt_off, gt_lab, B, dev, stream, rank, data)
     if args.mode == "all_apps":
         return run_all_apps(args, sc, ctx, logits, gt_off, gt_lab, B, dev, stream, rank)
     for _ in range(args.warmup):
@@ -432,6 +436,96 @@ def run_all_apps(args, sc, ctx, logits, gt_off, gt_lab, B, dev, stream, rank):
                           "value": B * A / (ms / 1e3), "unit": "evaluations/s", "ms_per_step": ms, "rows": B,
                           "apps": A, "dtype": args.dtype, "config": {"workload": workload_name(args.config, args.dtype)},
                           "reread_equivalent_ms": None}), flush=True)
+    return 0
+
+
+def run_head(args, sc, ctx, spec, gt_off, gt_lab, B, dev, stream, rank, data):
+    """Classifier head z = x W_𝕎ᵀ + b on tcgen05 with decide + loss fwd/bwd in the GEMM
+    epilogue (sc_head_loss_fwd_bwd), against the unfused pair it replaces: a cuBLAS GEMM
+    writing all C bf16 logits, then sc_loss_fwd_bwd reading them back."""
+    import torch
+    import synth
+    del data["logits"]
+    torch.cuda.empty_cache()
+    x, W, b = synth.head_operands_device(spec.C, args.d, B, seed=args.config)
+    head = sc.Head(ctx, W, b)
+    d, n_cols = head.info()
+    gm = torch.empty(B + 16, dtype=torch.uint8, device=dev)
+    hg = torch.zeros(256, dtype=torch.int64, device=dev)
+    w = torch.empty(256, dtype=torch.float32, device=dev)
+    out = dict(decision=torch.empty(B, dtype=torch.uint8, device=dev),
+               grad_idx=torch.empty(2 * B, dtype=torch.int32, device=dev),
+               grad_val=torch.empty(2 * B, dtype=torch.float32, device=dev),
+               loss_sum=torch.zeros(1, dtype=torch.float64, device=dev),
+               n_incorrect=torch.zeros(1, dtype=torch.int64, device=dev),
+               hist_pred=torch.zeros(256, dtype=torch.int64, device=dev))
+
+    def fused():
+        hg.zero_()
+        sc.sc_decision_hist_weights(ctx, sc.Batch(gt_off=gt_off, gt_lab=gt_lab, rows=B), hg, w, gt_mask_out=gm)
+        sc.sc_head_loss_fwd_bwd(ctx, head, x, gt_mask=gm, w=w, grad_scale=1.0 / B, **out)
+
+    logits = torch.empty((B, spec.C), dtype=torch.bfloat16, device=dev)
+
+    def unfused():
+        hg.zero_()
+        sc.sc_decision_hist_weights(ctx, sc.Batch(gt_off=gt_off, gt_lab=gt_lab, rows=B), hg, w, gt_mask_out=gm)
+        torch.addmm(b.to(torch.bfloat16), x, W.t(), out=logits)
+        sc.sc_loss_fwd_bwd(ctx, sc.Batch(logits=logits, gt_mask=gm), w=w, grad_scale=1.0 / B, **out)
+
+    def timed(fn, steps):
+        for _ in range(args.warmup):
+            fn()
+        torch.cuda.synchronize(dev)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        for _ in range(steps):
+            fn()
+        e.record(stream)
+        torch.cuda.synchronize(dev)
+        return s.elapsed_time(e) / steps
+
+    launches0 = sc.sc_launch_count()
+    with ClockSampler(dev.index or 0) as clk:
+        ms = timed(fused, args.steps)
+    launches = sc.sc_launch_count() - launches0
+    # the head kernel alone (events around the one launch, same stream)
+    ks, ke = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    k_total = 0.0
+    for _ in range(args.steps):
+        sc.sc_decision_hist_weights(ctx, sc.Batch(gt_off=gt_off, gt_lab=gt_lab, rows=B), hg.zero_(), w, gt_mask_out=gm)
+        ks.record(stream)
+        sc.sc_head_loss_fwd_bwd(ctx, head, x, gt_mask=gm, w=w, grad_scale=1.0 / B, **out)
+        ke.record(stream)
+        torch.cuda.synchronize(dev)
+        k_total += ks.elapsed_time(ke)
+    k_ms = k_total / args.steps
+    kname = sc.sc_last_kernel()
+    un_ms = timed(unfused, max(3, args.steps // 4))
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    tc = peaks.get("bf16_tflops", 1662.7)
+    per_row = d * 2 + 1 + 1 + 16  # features + G_i + decision + sparse gradient
+    achieved = B * per_row / (k_ms / 1e3) / 1e9
+    n_mapped = int(spec.mapped()[0].sum())
+    tflops = B * 2.0 * d * n_mapped / (k_ms / 1e3) / 1e12
+    line = {
+        "metric": "samples/s for the classifier head fused with decide+loss fwd/bwd (NEXT f4)",
+        "value": B / (ms / 1e3), "unit": "samples/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "dtype": "bf16 operands, f32 accumulate", "data": "synthetic",
+        "config": {"workload": f"{WORKLOADS[args.config]}, bf16 features d={d}, head over the {n_mapped} mapped "
+                               f"labels ({n_cols} columns)", "rows": B, "d": d},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                     "kernel": kname, "kernel_ms": k_ms, "algorithmic_bytes_per_row": per_row,
+                     "tensor": {"achieved_tflops": tflops, "peak_tflops": tc, "frac": tflops / tc,
+                                "flops_per_row": 2 * d * n_mapped}},
+        "unfused": {"ms_per_step": un_ms, "what": f"cuBLAS addmm -> bf16 logits [B, {spec.C}] + sc_loss_fwd_bwd",
+                    "speedup_fused": un_ms / ms},
+        "gpu_launches": int(launches), "clocks": clk.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
     return 0
 
 

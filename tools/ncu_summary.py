@@ -1,6 +1,6 @@
 """Summarise an ncu report (raw page) and a launch list into profiles/ (run here, no GPU).
 
-usage: python tools/ncu_summary.py REPORT.ncu-rep LAUNCHES.csv OUT.json OUT.txt ROWS
+usage: python tools/ncu_summary.py REPORT.ncu-rep LAUNCHES.csv OUT.json OUT.txt ROWS [KERNEL_SUBSTRING]
 """
 import csv
 import io
@@ -57,7 +57,8 @@ def launches(path):
 if __name__ == "__main__":
     rep, launch_csv, out_json, out_txt, rows = sys.argv[1:6]
     rows = int(rows)
-    r = raw(rep)[0]
+    want = sys.argv[6] if len(sys.argv) > 6 else ""
+    r = [k for k in raw(rep) if want in k["kernel"]][0]
     traffic = to_bytes(r["dram__bytes_read.sum"]) + to_bytes(r["dram__bytes_write.sum"])
     summ = {"report": rep, "metrics": r, "dram_bytes_per_launch": traffic, "dram_bytes_per_row": traffic / rows,
             "launch_list": launches(launch_csv)}
