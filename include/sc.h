@@ -268,13 +268,16 @@ const char* sc_sample_last_error(void);
  * afterwards).
  *   weight  device bf16 (uint16 bit patterns) [C][ldw], ldw >= d;  d >= 1.
  *   bias    device float [C] or NULL (0).
- * SC_ERR_UNSUPPORTED: order != API_OUTPUT, n_apps != 1, or |𝕎| > 512.
+ * SC_ERR_UNSUPPORTED: order != API_OUTPUT, n_apps != 1, or more than 512 head columns
+ * (see sc_head_info).
  * The copy is enqueued on `stream`; the head is usable on that stream when this returns. */
 typedef struct sc_head_s* sc_head;
 sc_status sc_head_load(sc_context ctx, const uint16_t* weight, int64_t ldw, int64_t d, const float* bias,
                        sc_stream stream, sc_head* out);
 sc_status sc_head_free(sc_head head);
-/* d, and the number of head columns computed per row (|𝕎| padded to a multiple of 16). */
+/* d, and the number of head columns computed per row: the mapped labels grouped by list
+ * (code order, ascending label id inside a list), each list padded to a multiple of 16,
+ * the total to a multiple of 32.  SC_ERR_UNSUPPORTED from sc_head_load when that exceeds 512. */
 sc_status sc_head_info(sc_head head, int64_t* d, int32_t* n_cols);
 
 typedef struct {

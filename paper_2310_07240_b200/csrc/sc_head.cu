@@ -4,18 +4,26 @@
 // PAPER.md:128-134, :862; Eq. api_output reads maxima over 𝕎 only),
 // then the API-output epilogue of sc_loss_fwd_bwd (rows a3-a9) on the accumulators.
 //
-// One persistent CTA per SM, 128-row tiles, warp-specialised:
-//   warp 0      TMA producer: per 64-wide k-block, the x tile [128 x 64] and the compiled
-//               head W_𝕎 [n_cols x 64] (both K-major, 128-B swizzle) into a stage of the
-//               shared-memory ring (full/empty mbarriers).
-//   warp 1      allocates 512 TMEM columns; one lane issues tcgen05.mma (M=128, N=chunk,
-//               K=16, bf16 x bf16 -> fp32 in TMEM), frees stages with tcgen05.commit and
-//               signals the epilogue per tile (double-buffered accumulators when n_cols <= 256).
-//   warps 2-5   epilogue: each thread owns one row (TMEM lane), tcgen05.ld its n_cols
-//               accumulators, adds the bias, keeps the split maxima (P⁺ over cat ∈ G_i, P⁻
-//               over the rest of 𝕎; ascending label order, so strict > keeps the smallest id
-//               on ties, reading A8) and runs finish_batch (decision, counters, loss, grad).
-// The features are the only HBM stream (d·2 bytes per row); W_𝕎 stays in L2.
+// Head columns are grouped by list (code order), ascending label id inside a list, each
+// list padded to a multiple of 16 columns (zero weights, bias -inf), so the epilogue takes
+// per-list arg maxima over whole 16-column TMEM loads with a branch-free tree and never
+// looks a column's list up; P⁺ / P⁻ are then arg maxima over the <= 8 list winners.
+//
+// Persistent CTAs, 128-row tiles, in clusters of Q CTAs (Q in {1,2,4,8}), warp-specialised:
+//   warp 0      TMA producer: per 64-wide k-block, the CTA's x tile [128 x 64] and 1/Q of
+//               the compiled head W_𝕎 [n_cols x 64] (both K-major, 128-B swizzle), the W
+//               slice multicast to every CTA of the cluster: W (L2-resident, the same for all
+//               tiles) leaves L2 once per cluster instead of once per CTA.
+//   warp 1      allocates 512 TMEM columns; one lane issues tcgen05.mma (M=128, N <= 256,
+//               K=16, bf16 x bf16 -> fp32 in TMEM) and frees each stage in every CTA of the
+//               cluster with a multicast tcgen05.commit (the W slices it holds came from all
+//               of them); double-buffered accumulators when n_cols <= 256.
+//   warps 2-5   epilogue: each thread owns one row (TMEM lane), tcgen05.ld its columns 16 at
+//               a time (the next load in flight while the current one is reduced), adds the
+//               bias, per-list arg max, split maxima by G_i, then finish_batch (decision,
+//               counters, loss, gradient).
+// The CTAs of a cluster step through the same number of tiles (a CTA past the last tile
+// computes a zero-filled one and discards it), so every multicast has all its receivers.
 #include "sc_device.cuh"
 #include "sc_host.h"
 
@@ -23,47 +31,118 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstdlib>
 #include <mutex>
+#include <string>
+#include <vector>
 
 namespace sc {
 namespace {
 
 constexpr int kBM = 128;           // rows per tile (UMMA M)
 constexpr int kBK = 64;            // bf16 elements per k-block = one 128-B swizzle row
-constexpr int kHeadThreads = 192;  // 6 warps
+constexpr int kHeadThreads = 224;  // 7 warps
 constexpr int kMaxCols = 512;      // TMEM columns
+constexpr int kMaxLists = 8;
 
 struct HeadParams {
   EvalParams ep;            // context, ground truth, loss and output pointers (finish_batch)
   const uint32_t* keys;     // [n_cols] c << 8 | cat, kNone for padding columns
-  const float* bias;        // [n_cols]
-  int64_t rows, n_tiles;
+  const float* bias;        // [n_cols], -inf for padding columns
+  int64_t rows;
+  int64_t n_units;          // row units: 128 rows (one CTA) or 256 rows (a CTA pair)
   int32_t n_kb;             // k-blocks
-  int32_t n_cols;           // head columns (multiple of 16)
+  int32_t n_cols;           // head columns (multiple of 32)
   int32_t chunk;            // columns per MMA (n_cols or n_cols / 2)
   int32_t n_chunks;
   int32_t acc_bufs;         // 2: double-buffered accumulators
-  int32_t stages;
-  int32_t stage_bytes;      // A + B
+  int32_t kbs;              // k-blocks per x stage (one 3-D TMA box of kbs x [128 x 64])
+  int32_t n_xb;             // x stages per unit = ceil(n_kb / kbs)
+  int32_t x_stages, w_stages;
+  int32_t x_stage_bytes;    // kbs * 16 KB
+  int32_t w_stage_bytes;    // W rows this CTA holds * 128 B (one k-block)
+  int32_t w_ring_off;       // byte offset of the W ring (after the x ring)
+  int32_t x3d;              // x tensor map is 3-D {64, rows, n_kb} (d % 64 == 0), else 2-D
   int32_t tab_off;          // keys / bias in shared memory
   int32_t bar_off;
+  int32_t n_lists;          // D'
+  int32_t list_col0[kMaxLists];  // first column of list j (multiple of 16)
+  int32_t list_nch[kMaxLists];   // 16-column groups of list j
+  int32_t probe;            // experiment (SC_HEAD_PROBE): bit 0 skips the epilogue's reduction, bit 1 the MMAs
 };
 
-// ------------------------------------------------------------------ tcgen05 / TMA PTX
+// ------------------------------------------------------------------ tcgen05 / TMA / cluster PTX
 
-__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int32_t c0, int32_t c1, uint64_t* bar,
+// TMA tile loads.  CG2: the CTA-pair form, whose mbarrier may live in the peer CTA (the
+// pair's leader counts the bytes both CTAs load).
+template <bool CG2>
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int32_t c0, int32_t c1, uint32_t bar,
                                        uint64_t pol) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_addr(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_addr(bar)), "l"(pol)
-      : "memory");
+  if constexpr (CG2)
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_addr(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar), "l"(pol)
+        : "memory");
+  else
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_addr(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar), "l"(pol)
+        : "memory");
+}
+
+// 3-D box {64, 128 rows, kbs k-blocks} of x viewed as [n_kb][rows][64]: kbs swizzled
+// [128 x 64] tiles back to back, each row's kbs*128 B contiguous in global memory.
+template <bool CG2>
+__device__ __forceinline__ void tma_3d(void* dst, const CUtensorMap* map, int32_t c0, int32_t c1, int32_t c2,
+                                       uint32_t bar, uint64_t pol) {
+  if constexpr (CG2)
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_addr(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar), "l"(pol)
+        : "memory");
+  else
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_addr(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar), "l"(pol)
+        : "memory");
 }
 
 __device__ __forceinline__ uint64_t evict_last_policy() {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
   return pol;
+}
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// shared::cluster address of the same shared variable in CTA `rank` of the cluster.
+__device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx_cl(uint32_t bar_cl, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(bar_cl), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_cl(uint32_t bar_cl) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cl) : "memory");
 }
 
 // Shared-memory matrix descriptor, K-major, 128-B swizzle: rows of 128 B, 8-row groups
@@ -73,26 +152,45 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
          (2ull << 61);
 }
 
-// Instruction descriptor, kind::f16: fp32 accumulator, bf16 A and B, both K-major, M=128, N.
-__host__ __device__ constexpr uint32_t idesc_bf16(int n) {
+// Instruction descriptor, kind::f16: fp32 accumulator, bf16 A and B, both K-major, M x N.
+__host__ __device__ constexpr uint32_t idesc_bf16(int m, int n) {
   return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
-         (static_cast<uint32_t>(kBM >> 4) << 24);
+         (static_cast<uint32_t>(m >> 4) << 24);
 }
 
+// D (TMEM) (+)= A (smem) · Bᵀ (smem).  CG2: M = 256 over the CTA pair — each CTA holds its
+// 128 rows of A and half of B's columns at the same shared-memory offsets, and receives its
+// 128 rows x N of D in its own TMEM; issued by the pair's leader only.
+template <bool CG2>
 __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                           uint32_t accumulate) {
-  asm volatile(
-      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
+  if constexpr (CG2)
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+  else
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
 }
 
-// Arrive once on `bar` when every tcgen05.mma issued so far by this thread has completed.
+// Arrive once on `bar` (CG2: at `bar`'s offset in both CTAs of the pair) when every
+// tcgen05.mma issued so far by this thread has completed.
+template <bool CG2>
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                   smem_addr(bar))
-               : "memory");
+  if constexpr (CG2)
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_addr(bar)),
+        "h"(static_cast<uint16_t>(3))
+        : "memory");
+  else
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_addr(bar))
+                 : "memory");
 }
 
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -106,69 +204,155 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
         "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
       : "r"(taddr));
 }
-__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// Wait for the outstanding tcgen05.ld; `v` passes through so no use of it is hoisted above.
+__device__ __forceinline__ void tmem_wait_ld(uint32_t (&v)[16]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7]),
+                 "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]), "+r"(v[14]), "+r"(v[15])
+               :
+               : "memory");
+}
+
+// Arg max of 16 columns (z, index); strict > keeps the lower index on ties (reading A4:
+// the lower column of a list is the smaller label id).
+__device__ __forceinline__ void argmax16(const float (&z)[16], float& zo, int& io) {
+  float a[8];
+  int ia[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const bool r = z[2 * i + 1] > z[2 * i];
+    a[i] = r ? z[2 * i + 1] : z[2 * i];
+    ia[i] = r ? 2 * i + 1 : 2 * i;
+  }
+#pragma unroll
+  for (int w = 4; w >= 1; w >>= 1)
+#pragma unroll
+    for (int i = 0; i < w; ++i) {
+      const bool r = a[2 * i + 1] > a[2 * i];
+      a[i] = r ? a[2 * i + 1] : a[2 * i];
+      ia[i] = r ? ia[2 * i + 1] : ia[2 * i];
+    }
+  zo = a[0];
+  io = ia[0];
+}
 
 // ------------------------------------------------------------------ kernel
 
+// PAIR: clusters of two CTAs on one TPC run M = 256 MMAs (cta_group::2): each CTA streams
+// its own 128 rows of x and half of W_𝕎, so a CTA moves half the W bytes per row that a lone
+// CTA would (W, re-read for every row tile, outweighs x at d = 2048, |𝕎| = 180).
+template <bool PAIR>
 __global__ void __launch_bounds__(kHeadThreads, 1)
     head_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w,
-                const HeadParams p) {
+                const __grid_constant__ HeadParams p) {
   extern __shared__ uint8_t sm_raw[];
-  // 1024-B alignment for the 128-B swizzle atoms
+  // 1024-B alignment for the 128-B swizzle atoms (the same offsets in both CTAs of a pair)
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   uint32_t* s_keys = reinterpret_cast<uint32_t*>(sm + p.tab_off);
   float* s_bias = reinterpret_cast<float*>(s_keys + p.n_cols);
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + p.bar_off);
-  uint64_t* full = bar;                       // [stages]
-  uint64_t* empty = bar + p.stages;           // [stages]
-  uint64_t* tfull = bar + 2 * p.stages;       // [2]
-  uint64_t* tempty = tfull + 2;               // [2]
+  uint64_t* xfull = bar;                      // [x_stages]  (PAIR: the leader's counts both CTAs)
+  uint64_t* xempty = xfull + p.x_stages;      // [x_stages]
+  uint64_t* wfull = xempty + p.x_stages;      // [w_stages]  (PAIR: the leader's counts both CTAs)
+  uint64_t* wempty = wfull + p.w_stages;      // [w_stages]
+  uint64_t* tfull = wempty + p.w_stages;      // [2]
+  uint64_t* tempty = tfull + 2;               // [2]         (PAIR: the leader's counts both CTAs)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
+  constexpr int kUnit = PAIR ? 2 * kBM : kBM;
 
   for (int i = tid; i < p.n_cols; i += blockDim.x) {
     s_keys[i] = __ldg(p.keys + i);
     s_bias[i] = __ldg(p.bias + i);
   }
   if (tid == 0) {
-    for (int s = 0; s < p.stages; ++s) {
-      mbar_init(full + s, 1);
-      mbar_init(empty + s, 1);
+    for (int s = 0; s < p.x_stages; ++s) {
+      mbar_init(xfull + s, PAIR ? 2 : 1);
+      mbar_init(xempty + s, 1);
+    }
+    for (int s = 0; s < p.w_stages; ++s) {
+      mbar_init(wfull + s, PAIR ? 2 : 1);
+      mbar_init(wempty + s, 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(tfull + b, 1);
-      mbar_init(tempty + b, 4);  // one arrive per epilogue warp
+      mbar_init(tempty + b, PAIR ? 8 : 4);  // one arrive per epilogue warp (of both CTAs)
     }
     fence_mbar_init();
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(tmem_slot)),
-                 "n"(kMaxCols)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if constexpr (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(tmem_slot)),
+                   "n"(kMaxCols)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(tmem_slot)),
+                   "n"(kMaxCols)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (PAIR) cluster_sync();  // both CTAs' barriers exist before either signals the other
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const uint32_t a_bytes = kBM * kBK * 2;
+  // units u = unit0 + step * n_grid_units (a pair shares its unit sequence)
+  const int64_t unit0 = PAIR ? blockIdx.x / 2 : blockIdx.x;
+  const int64_t n_grid_units = PAIR ? gridDim.x / 2 : gridDim.x;
+  const int64_t n_steps = unit0 < p.n_units ? (p.n_units - unit0 + n_grid_units - 1) / n_grid_units : 0;
+  // the leader's full barriers, in shared::cluster space (its own for a lone CTA)
+  const uint32_t xfull_l = PAIR ? mapa(smem_addr(xfull), 0) : smem_addr(xfull);
+  const uint32_t wfull_l = PAIR ? mapa(smem_addr(wfull), 0) : smem_addr(wfull);
+  const uint32_t tempty_l = PAIR ? mapa(smem_addr(tempty), 0) : smem_addr(tempty);
 
   if (warp == 0) {
     if (lane == 0) {
-      // ---------------- TMA producer
-      const uint64_t pol_x = evict_first_policy(), pol_w = evict_last_policy();
+      // ---------------- x producer: kbs k-blocks of this CTA's 128 rows per stage (from HBM)
+      const uint64_t pol_x = evict_first_policy();
+      const uint32_t tx = static_cast<uint32_t>(p.x_stage_bytes);
       int s = 0;
       uint32_t ph = 0;
-      for (int64_t t = blockIdx.x; t < p.n_tiles; t += gridDim.x) {
-        const int32_t row0 = static_cast<int32_t>(t * kBM);
+      for (int64_t st = 0; st < n_steps; ++st) {
+        // may be past the last row: TMA fills zeros, the epilogue skips those rows
+        const int32_t row0 = static_cast<int32_t>((unit0 + st * n_grid_units) * kUnit + rank * kBM);
+        for (int xb = 0; xb < p.n_xb; ++xb) {
+          mbar_wait(xempty + s, ph ^ 1u);
+          uint8_t* stg = sm + static_cast<size_t>(s) * p.x_stage_bytes;
+          const uint32_t fb = xfull_l + 8u * s;
+          if (rank == 0) mbar_arrive_expect_tx(xfull + s, tx);
+          else mbar_arrive_expect_tx_cl(fb, tx);
+          if (p.x3d) tma_3d<PAIR>(stg, &map_x, 0, row0, xb * p.kbs, fb, pol_x);
+          else tma_2d<PAIR>(stg, &map_x, xb * kBK, row0, fb, pol_x);
+          if (++s == p.x_stages) {
+            s = 0;
+            ph ^= 1u;
+          }
+        }
+      }
+    }
+  } else if (warp == 6) {
+    if (lane == 0) {
+      // ---------------- W producer: one k-block of this CTA's W_𝕎 rows per stage (L2-resident)
+      const uint64_t pol_w = evict_last_policy();
+      const uint32_t tx = static_cast<uint32_t>(p.w_stage_bytes);
+      const int rows_c = PAIR ? p.chunk / 2 : p.chunk;  // W rows per MMA chunk held here
+      int s = 0;
+      uint32_t ph = 0;
+      for (int64_t st = 0; st < n_steps; ++st) {
         for (int kb = 0; kb < p.n_kb; ++kb) {
-          mbar_wait(empty + s, ph ^ 1u);
-          uint8_t* st = sm + static_cast<size_t>(s) * p.stage_bytes;
-          mbar_arrive_expect_tx(full + s, static_cast<uint32_t>(p.stage_bytes));
-          tma_2d(st, &map_x, kb * kBK, row0, full + s, pol_x);
+          mbar_wait(wempty + s, ph ^ 1u);
+          uint8_t* stg = sm + p.w_ring_off + static_cast<size_t>(s) * p.w_stage_bytes;
+          const uint32_t fb = wfull_l + 8u * s;
+          if (rank == 0) mbar_arrive_expect_tx(wfull + s, tx);
+          else mbar_arrive_expect_tx_cl(fb, tx);
           for (int c = 0; c < p.n_chunks; ++c)
-            tma_2d(st + a_bytes + c * p.chunk * (kBK * 2), &map_w, kb * kBK, c * p.chunk, full + s, pol_w);
-          if (++s == p.stages) {
+            tma_2d<PAIR>(stg + c * rows_c * (kBK * 2), &map_w, 0,
+                         kb * p.n_cols + c * p.chunk + static_cast<int>(rank) * rows_c, fb, pol_w);
+          if (++s == p.w_stages) {
             s = 0;
             ph ^= 1u;
           }
@@ -176,50 +360,74 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------- MMA issuer
-      const uint32_t idesc = idesc_bf16(p.chunk);
-      int s = 0, b = 0;
-      uint32_t ph = 0, tph[2] = {0, 0};
-      for (int64_t t = blockIdx.x; t < p.n_tiles; t += gridDim.x) {
-        mbar_wait(tempty + b, tph[b] ^ 1u);  // the epilogue drained this accumulator
+    if (lane == 0 && rank == 0) {
+      // ---------------- MMA issuer (the pair's leader)
+      const uint32_t idesc = idesc_bf16(PAIR ? 2 * kBM : kBM, p.chunk);
+      // descriptors advance by address >> 4 in their low bits: x stage, k-block in the
+      // stage (16 KB), 32 B per K=16 step; W stage; second MMA's columns
+      const uint64_t a_desc0 = sw128_desc(smem_addr(sm));
+      const uint64_t b_desc0 = sw128_desc(smem_addr(sm + p.w_ring_off));
+      const uint64_t x_step = static_cast<uint32_t>(p.x_stage_bytes) >> 4;
+      const uint64_t w_step = static_cast<uint32_t>(p.w_stage_bytes) >> 4;
+      const uint64_t c_step = static_cast<uint32_t>((PAIR ? p.chunk / 2 : p.chunk) * kBK * 2) >> 4;
+      const bool two = p.n_chunks == 2;
+      const bool no_mma = (p.probe & 2) != 0;
+      int xs = 0, ws = 0, b = 0;
+      uint32_t xph = 0, wph = 0, tph[2] = {0, 0};
+      for (int64_t st = 0; st < n_steps; ++st) {
+        mbar_wait(tempty + b, tph[b] ^ 1u);  // the epilogue(s) drained this accumulator
         tph[b] ^= 1u;
         tc_fence_after();
         const uint32_t acc = tmem_base + static_cast<uint32_t>(b * p.n_cols);
-        for (int kb = 0; kb < p.n_kb; ++kb) {
-          mbar_wait(full + s, ph);
+        for (int xb = 0; xb < p.n_xb; ++xb) {
+          mbar_wait(xfull + xs, xph);
           tc_fence_after();
-          const uint32_t sa = smem_addr(sm + static_cast<size_t>(s) * p.stage_bytes);
+          const uint64_t ax = a_desc0 + static_cast<uint64_t>(xs) * x_step;
+          const int nk = min(p.kbs, p.n_kb - xb * p.kbs);
+          for (int kx = 0; kx < nk; ++kx) {
+            mbar_wait(wfull + ws, wph);
+            tc_fence_after();
+            const uint64_t ad = ax + static_cast<uint64_t>(kx) * (a_bytes >> 4);
+            const uint64_t bd = b_desc0 + static_cast<uint64_t>(ws) * w_step;
+            if (!no_mma) {
+              const bool first = (xb | kx) == 0;
 #pragma unroll
-          for (int k = 0; k < kBK / 16; ++k) {
-            const uint64_t ad = sw128_desc(sa + 32u * k);
-            for (int c = 0; c < p.n_chunks; ++c) {
-              const uint64_t bd = sw128_desc(sa + a_bytes + c * p.chunk * (kBK * 2) + 32u * k);
-              umma_bf16(acc + c * p.chunk, ad, bd, idesc, (kb | k) != 0);
+              for (int k = 0; k < kBK / 16; ++k) {
+                const uint32_t accum = (first && k == 0) ? 0u : 1u;
+                umma_bf16<PAIR>(acc, ad + 2 * k, bd + 2 * k, idesc, accum);
+                if (two) umma_bf16<PAIR>(acc + p.chunk, ad + 2 * k, bd + c_step + 2 * k, idesc, accum);
+              }
+            }
+            umma_commit<PAIR>(wempty + ws);  // W stage free (in both CTAs) once read
+            if (++ws == p.w_stages) {
+              ws = 0;
+              wph ^= 1u;
             }
           }
-          umma_commit(empty + s);  // stage reusable once these MMAs have read it
-          if (++s == p.stages) {
-            s = 0;
-            ph ^= 1u;
+          umma_commit<PAIR>(xempty + xs);
+          if (++xs == p.x_stages) {
+            xs = 0;
+            xph ^= 1u;
           }
         }
-        umma_commit(tfull + b);  // accumulator complete
+        umma_commit<PAIR>(tfull + b);  // accumulator complete (in both CTAs)
         if (p.acc_bufs == 2) b ^= 1;
       }
     }
-  } else {
+  } else if (warp <= 5) {
     // ---------------- epilogue: one row per thread
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const uint32_t lane_base = static_cast<uint32_t>(32 * q) << 16;
     const EvalParams& ep = p.ep;
     const uint8_t* cat = ep.ctx.cat;
+    const int D = p.n_lists;
     int b = 0;
     uint32_t tph[2] = {0, 0};
     RowBatch rb;
     rb.n = 0;
-    for (int64_t t = blockIdx.x; t < p.n_tiles; t += gridDim.x) {
-      const int64_t row = t * kBM + 32 * q + lane;
+    for (int64_t st = 0; st < n_steps; ++st) {
+      const int64_t first = (unit0 + st * n_grid_units) * kUnit + rank * kBM + 32 * q;
+      const int64_t row = first + lane;
       const bool active = row < p.rows;
       // G_i before waiting on the accumulator (overlaps the MMA)
       uint32_t G = 0;
@@ -234,30 +442,92 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
       mbar_wait(tfull + b, tph[b]);
       tph[b] ^= 1u;
       tc_fence_after();
-      float zp = -CUDART_INF_F, zm = -CUDART_INF_F;
-      uint32_t kp = kNone, km = kNone;
       const uint32_t acc = tmem_base + lane_base + static_cast<uint32_t>(b * p.n_cols);
-      for (int c0 = 0; c0 < p.n_cols; c0 += 16) {
-        uint32_t v[16];
-        tmem_ld16(acc + c0, v);
-        tmem_wait_ld();
+      // per-list arg max over the list's 16-column groups; the next group's load is in
+      // flight while the current one is reduced
+      float lz[kMaxLists];
+      int lc[kMaxLists];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const uint32_t key = s_keys[c0 + j];
-          if (key == kNone) continue;
-          const float z = __uint_as_float(v[j]) + s_bias[c0 + j];
-          if ((G >> (key & 0xFFu)) & 1u) {
-            if (z > zp) { zp = z; kp = key; }
-          } else {
-            if (z > zm) { zm = z; km = key; }
-          }
+      for (int j = 0; j < kMaxLists; ++j) {
+        lz[j] = -CUDART_INF_F;
+        lc[j] = -1;
+      }
+      uint32_t v[16], vn[16];
+      int j = 0, g = 0;  // list, group within the list
+      while (j < D && p.list_nch[j] == 0) ++j;
+      if (p.probe & 1) j = D;
+      if (j < D) {
+        tmem_ld16(acc + p.list_col0[j], v);
+        tmem_wait_ld(v);
+      }
+      float run_z = -CUDART_INF_F;
+      int run_c = -1;
+      while (j < D) {
+        const int col = p.list_col0[j] + 16 * g;
+        // next group (warp-uniform)
+        int jn = j, gn = g + 1;
+        if (gn == p.list_nch[jn]) {
+          gn = 0;
+          ++jn;
+          while (jn < D && p.list_nch[jn] == 0) ++jn;
+        }
+        if (jn < D) tmem_ld16(acc + p.list_col0[jn] + 16 * gn, vn);
+        float z[16];
+        const float4* b4 = reinterpret_cast<const float4*>(s_bias + col);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float4 bb = b4[i];
+          z[4 * i + 0] = __uint_as_float(v[4 * i + 0]) + bb.x;
+          z[4 * i + 1] = __uint_as_float(v[4 * i + 1]) + bb.y;
+          z[4 * i + 2] = __uint_as_float(v[4 * i + 2]) + bb.z;
+          z[4 * i + 3] = __uint_as_float(v[4 * i + 3]) + bb.w;
+        }
+        float zc;
+        int ic;
+        argmax16(z, zc, ic);
+        if (zc > run_z) {  // strict: an earlier group (smaller labels) keeps ties
+          run_z = zc;
+          run_c = col + ic;
+        }
+        if (jn != j) {  // list j done
+#pragma unroll
+          for (int jj = 0; jj < kMaxLists; ++jj)
+            if (jj == j) {
+              lz[jj] = run_z;
+              lc[jj] = run_c;
+            }
+          run_z = -CUDART_INF_F;
+          run_c = -1;
+        }
+        j = jn;
+        g = gn;
+        if (j < D) {
+          tmem_wait_ld(vn);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = vn[i];
         }
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(tempty + b);  // the MMA may overwrite this accumulator
+      if (lane == 0) {  // the MMA may overwrite this accumulator
+        if (rank == 0) mbar_arrive(tempty + b);
+        else mbar_arrive_cl(tempty_l + 8u * b);
+      }
       if (p.acc_bufs == 2) b ^= 1;
-      const int64_t first = t * kBM + 32 * q;
+      // split maxima over the list winners: P⁺ over lists in G_i, P⁻ over the rest (A8)
+      float zp = -CUDART_INF_F, zm = -CUDART_INF_F;
+      uint32_t kp = kNone, km = kNone;
+#pragma unroll
+      for (int jj = 0; jj < kMaxLists; ++jj) {
+        if (lc[jj] >= 0) {
+          const uint32_t key = s_keys[lc[jj]];
+          if ((G >> jj) & 1u) {
+            if (beats(lz[jj], key, zp, kp)) { zp = lz[jj]; kp = key; }
+          } else {
+            if (beats(lz[jj], key, zm, km)) { zm = lz[jj]; km = key; }
+          }
+        }
+      }
       const int64_t nrow = p.rows - first;
       if (nrow > 0) {
         rb.zp = zp; rb.kp = kp; rb.zm = zm; rb.km = km; rb.G = G; rb.app = 0; rb.row = row;
@@ -268,28 +538,31 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (PAIR) cluster_sync();  // neither CTA leaves while the other may still signal it
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(kMaxCols)
-                 : "memory");
+    if constexpr (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(kMaxCols)
+                   : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(kMaxCols)
+                   : "memory");
   }
 }
 
-// Compiled head rows: Wm[j] = W[c_j] (zero padding to d_pad, zero rows past |𝕎|).
-__global__ void head_gather_kernel(const uint16_t* W, int64_t ldw, int64_t d, int64_t d_pad, const float* bias,
-                                   const uint32_t* ent, int32_t n_mapped, int32_t n_cols, uint16_t* Wm,
-                                   float* bias_m, uint32_t* keys) {
+// Compiled head, k-block major: Wm[kb][j][0..63] = W[label_j][64 kb .. 64 kb + 63] (zeros past
+// d and for padding columns), so the W_𝕎 slice of one k-block is one contiguous n_cols x 128 B
+// run: every CTA reads the same k-block at about the same time, and a contiguous block spreads
+// over all L2 slices where a strided one (4 KB apart) piles onto a few.
+__global__ void head_gather_kernel(const uint16_t* W, int64_t ldw, int64_t d, int32_t n_kb, int32_t n,
+                                   const float* bias, const int32_t* col_label, uint16_t* Wm, float* bias_m) {
   const int j = blockIdx.x;
-  const bool mapped = j < n_mapped;
-  const uint32_t key = mapped ? ent[j] : kNone;
-  const int64_t c = key >> 8;
-  for (int64_t i = threadIdx.x; i < d_pad; i += blockDim.x)
-    Wm[static_cast<int64_t>(j) * d_pad + i] = (mapped && i < d) ? W[c * ldw + i] : uint16_t(0);
-  if (threadIdx.x == 0) {
-    keys[j] = key;
-    bias_m[j] = (mapped && bias) ? bias[c] : 0.f;
+  const int32_t c = col_label[j];
+  for (int64_t i = threadIdx.x; i < static_cast<int64_t>(n_kb) * 64; i += blockDim.x) {
+    const int64_t kb = i >> 6, k = i & 63;
+    Wm[(kb * n + j) * 64 + k] = (c >= 0 && i < d) ? W[c * ldw + i] : uint16_t(0);
   }
-  (void)n_cols;
+  if (threadIdx.x == 0) bias_m[j] = c < 0 ? -CUDART_INF_F : (bias ? bias[c] : 0.f);
 }
 
 }  // namespace
@@ -301,10 +574,14 @@ struct sc_head_s {
   int device = 0;
   int64_t d = 0, d_pad = 0;
   int32_t n_mapped = 0, n_cols = 0, chunk = 0, n_chunks = 0;
-  uint16_t* Wm = nullptr;  // [n_cols][d_pad]
+  int32_t n_lists = 0;
+  int32_t list_col0[sc::kMaxLists] = {}, list_nch[sc::kMaxLists] = {};
+  uint16_t* Wm = nullptr;  // [n_kb][n_cols][64]
   float* bias = nullptr;   // [n_cols]
   uint32_t* keys = nullptr;
-  CUtensorMap map_w;
+  int32_t* col_label = nullptr;
+  CUtensorMap map_w[2];    // [0]: box rows = chunk (one CTA), [1]: chunk / 2 (CTA pair)
+  bool map_ok[2] = {false, false};
 };
 
 namespace {
@@ -339,7 +616,76 @@ bool make_map(CUtensorMap* m, const void* base, int64_t cols, int64_t rows, int6
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// 3-D bf16 tensor map over row-major x [rows][ld] (d % 64 == 0) viewed as {64, rows, d/64}:
+// box {64, 128, kbs}, 128-B swizzle -> kbs [128 x 64] K-major tiles back to back.
+bool make_map3(CUtensorMap* m, const void* base, int64_t d, int64_t rows, int64_t ld, int kbs) {
+  EncodeTiled enc = encode_fn();
+  if (!enc) return false;
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(sc::kBK), static_cast<cuuint64_t>(rows),
+                              static_cast<cuuint64_t>(d / sc::kBK)};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(ld) * 2, static_cast<cuuint64_t>(sc::kBK) * 2};
+  const cuuint32_t box[3] = {static_cast<cuuint32_t>(sc::kBK), static_cast<cuuint32_t>(sc::kBM),
+                             static_cast<cuuint32_t>(kbs)};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 constexpr size_t kHeadSmemMax = 227 * 1024;
+
+// One CTA per SM; CTA pairs (cta_group::2) with SC_HEAD_CLUSTER=2 when the pairs cover
+// >= 90 % of the SMs.  Memoised: the occupancy query costs more
+// than a small launch.
+struct HeadLaunch {
+  bool pair = false;
+  int units = 0;  // co-resident CTAs (single) or pairs
+};
+
+HeadLaunch pick_launch(size_t smem, int sms, int64_t n_tiles) {
+  int forced = 0;
+  if (const char* e = std::getenv("SC_HEAD_CLUSTER")) forced = std::atoi(e);
+  static std::mutex mu;
+  static std::vector<std::pair<std::array<int64_t, 3>, int>> memo;  // (smem, sms, 0) -> pairs
+  int pairs = -1;
+  {
+    const std::array<int64_t, 3> key = {static_cast<int64_t>(smem), sms, 0};
+    std::lock_guard<std::mutex> lock(mu);
+    for (auto& kv : memo)
+      if (kv.first == key) pairs = kv.second;
+    if (pairs < 0) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(static_cast<unsigned>(2 * (sms / 2)));
+      cfg.blockDim = dim3(sc::kHeadThreads);
+      cfg.dynamicSmemBytes = smem;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = 2;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, sc::head_kernel<true>, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        n = 0;
+      }
+      pairs = n;
+      memo.emplace_back(key, pairs);
+    }
+  }
+  HeadLaunch hl;
+  // Pairs are correct (tests) but measured slower than lone CTAs on cfg2 (1.45 vs 1.01 ms at
+  // d = 2048): opt-in until the cross-CTA handshake is understood.
+  const bool pair_ok = pairs >= 1 && (forced == 2 || 2 * pairs * 10 >= sms * 9);
+  if (forced == 2 && pair_ok && n_tiles >= 2) {
+    hl.pair = true;
+    hl.units = pairs;
+  } else {
+    hl.units = sms;
+  }
+  return hl;
+}
 
 }  // namespace
 
@@ -352,32 +698,63 @@ sc_status sc_head_load(sc_context ctx, const uint16_t* weight, int64_t ldw, int6
   if (d < 1 || ldw < d) return sc::set_error(SC_ERR_INVALID_ARG, "sc_head_load: need d >= 1 and ldw >= d");
   if (ctx->order != SC_ORDER_API_OUTPUT || ctx->n_apps != 1)
     return sc::set_error(SC_ERR_UNSUPPORTED, "sc_head_load: API-output order and one application only");
-  const int32_t nm = ctx->n_mapped[0];
-  if (nm > sc::kMaxCols)
-    return sc::set_error(SC_ERR_UNSUPPORTED, "sc_head_load: |W| = %d mapped labels > %d", nm, sc::kMaxCols);
   if (d > (int64_t(1) << 31) - sc::kBK) return sc::set_error(SC_ERR_INVALID_ARG, "sc_head_load: d too large");
+  const int32_t nm = ctx->n_mapped[0];
+  const int32_t D = ctx->nlists[0];
+  // mapped labels of the app (sorted by id), grouped by list, each list padded to 16 columns
+  std::vector<uint32_t> ent(std::max(nm, 1));
+  cudaError_t e = cudaMemcpy(ent.data(), ctx->d_ent, static_cast<size_t>(nm) * 4, cudaMemcpyDeviceToHost);
+  if (e) return sc::set_error(SC_ERR_CUDA, "sc_head_load: %s", cudaGetErrorString(e));
+  std::vector<int32_t> col_label;
+  std::vector<uint32_t> keys;
   sc_head h = new sc_head_s;
+  h->n_lists = D;
+  for (int32_t j = 0; j < D; ++j) {
+    h->list_col0[j] = static_cast<int32_t>(col_label.size());
+    for (int32_t t = 0; t < nm; ++t)
+      if ((ent[t] & 0xFFu) == static_cast<uint32_t>(j)) {
+        col_label.push_back(static_cast<int32_t>(ent[t] >> 8));
+        keys.push_back(ent[t]);
+      }
+    while (col_label.size() % 16) {
+      col_label.push_back(-1);
+      keys.push_back(sc::kNone);
+    }
+    h->list_nch[j] = (static_cast<int32_t>(col_label.size()) - h->list_col0[j]) / 16;
+  }
+  while (col_label.size() < 32 || col_label.size() % 32) {  // W slices of 8-row multiples for q <= 4
+    col_label.push_back(-1);
+    keys.push_back(sc::kNone);
+  }
+  const int32_t n = static_cast<int32_t>(col_label.size());
+  if (n > sc::kMaxCols) {
+    sc_head_free(h);
+    return sc::set_error(SC_ERR_UNSUPPORTED,
+                         "sc_head_load: |W| = %d mapped labels need %d head columns (lists padded to 16) > %d", nm, n,
+                         sc::kMaxCols);
+  }
   h->d = d;
   h->d_pad = (d + 7) / 8 * 8;
   h->n_mapped = nm;
-  int32_t n = std::max<int32_t>(16, (nm + 15) / 16 * 16);
+  h->n_cols = n;
   if (n <= 256) {
     h->chunk = n;
     h->n_chunks = 1;
-  } else {  // two equal MMAs of <= 256 columns (one TMA box size)
-    h->chunk = ((n + 1) / 2 + 15) / 16 * 16;
+  } else {  // two MMAs of n/2 <= 256 columns
+    h->chunk = n / 2;
     h->n_chunks = 2;
-    n = 2 * h->chunk;
   }
-  h->n_cols = n;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  cudaError_t e = cudaGetDevice(&h->device);
-  if (!e) e = cudaMalloc(&h->Wm, static_cast<size_t>(n) * h->d_pad * 2);
+  e = cudaGetDevice(&h->device);
+  const int32_t n_kb = static_cast<int32_t>((d + sc::kBK - 1) / sc::kBK);
+  if (!e) e = cudaMalloc(&h->Wm, static_cast<size_t>(n) * n_kb * sc::kBK * 2);
   if (!e) e = cudaMalloc(&h->bias, static_cast<size_t>(n) * 4);
   if (!e) e = cudaMalloc(&h->keys, static_cast<size_t>(n) * 4);
+  if (!e) e = cudaMalloc(&h->col_label, static_cast<size_t>(n) * 4);
+  if (!e) e = cudaMemcpyAsync(h->keys, keys.data(), static_cast<size_t>(n) * 4, cudaMemcpyHostToDevice, st);
+  if (!e) e = cudaMemcpyAsync(h->col_label, col_label.data(), static_cast<size_t>(n) * 4, cudaMemcpyHostToDevice, st);
   if (!e) {
-    sc::head_gather_kernel<<<n, 256, 0, st>>>(weight, ldw, d, h->d_pad, bias, ctx->d_ent, nm, n, h->Wm, h->bias,
-                                             h->keys);
+    sc::head_gather_kernel<<<n, 256, 0, st>>>(weight, ldw, d, n_kb, n, bias, h->col_label, h->Wm, h->bias);
     sc::note_launch("head_gather");
     e = cudaGetLastError();
   }
@@ -387,7 +764,9 @@ sc_status sc_head_load(sc_context ctx, const uint16_t* weight, int64_t ldw, int6
     return sc::set_error(e == cudaErrorMemoryAllocation ? SC_ERR_OOM : SC_ERR_CUDA, "sc_head_load: %s",
                          cudaGetErrorString(e));
   }
-  if (!make_map(&h->map_w, h->Wm, d, n, h->d_pad, h->chunk)) {
+  h->map_ok[0] = make_map(&h->map_w[0], h->Wm, sc::kBK, static_cast<int64_t>(n_kb) * n, sc::kBK, h->chunk);
+  h->map_ok[1] = make_map(&h->map_w[1], h->Wm, sc::kBK, static_cast<int64_t>(n_kb) * n, sc::kBK, h->chunk / 2);
+  if (!h->map_ok[0]) {
     sc_head_free(h);
     return sc::set_error(SC_ERR_CUDA, "sc_head_load: cuTensorMapEncodeTiled failed");
   }
@@ -400,6 +779,7 @@ sc_status sc_head_free(sc_head h) {
   cudaFree(h->Wm);
   cudaFree(h->bias);
   cudaFree(h->keys);
+  cudaFree(h->col_label);
   delete h;
   return SC_OK;
 }
@@ -420,7 +800,7 @@ sc_status sc_head_loss_fwd_bwd(sc_context ctx, sc_head head, const sc_head_batch
     return sc::set_error(SC_ERR_UNSUPPORTED, "sc_head_loss_fwd_bwd: API-output order and one application only");
   const sc_head_batch& b = *batch;
   if (b.rows < 0) return sc::set_error(SC_ERR_INVALID_ARG, "sc_head_loss_fwd_bwd: rows < 0");
-  if (b.rows > (int64_t(1) << 31) - sc::kBM)
+  if (b.rows > (int64_t(1) << 31) - (int64_t(1) << 20))
     return sc::set_error(SC_ERR_INVALID_ARG, "sc_head_loss_fwd_bwd: rows >= 2^31");
   if (b.rows > 0 && !b.x) return sc::set_error(SC_ERR_INVALID_ARG, "sc_head_loss_fwd_bwd: x is NULL");
   if (b.ldx < head->d || b.ldx % 8 != 0 || (reinterpret_cast<uintptr_t>(b.x) & 15u))
@@ -467,40 +847,117 @@ sc_status sc_head_loss_fwd_bwd(sc_context ctx, sc_head head, const sc_head_batch
   p.keys = head->keys;
   p.bias = head->bias;
   p.rows = b.rows;
-  p.n_tiles = (b.rows + sc::kBM - 1) / sc::kBM;
   p.n_kb = static_cast<int32_t>((head->d + sc::kBK - 1) / sc::kBK);
   p.n_cols = head->n_cols;
   p.chunk = head->chunk;
   p.n_chunks = head->n_chunks;
   p.acc_bufs = 2 * head->n_cols <= sc::kMaxCols ? 2 : 1;
-  p.stage_bytes = sc::kBM * sc::kBK * 2 + head->n_cols * sc::kBK * 2;
+  p.n_lists = head->n_lists;
+  for (int j = 0; j < sc::kMaxLists; ++j) {
+    p.list_col0[j] = head->list_col0[j];
+    p.list_nch[j] = head->list_nch[j];
+  }
+  p.probe = std::getenv("SC_HEAD_PROBE") ? std::atoi(std::getenv("SC_HEAD_PROBE")) : 0;
+  const int a_bytes = sc::kBM * sc::kBK * 2;
   const int tab_bytes = head->n_cols * 8;
-  const int bar_bytes = 8 * (2 * 8 + 4) + 16;
-  int stages = static_cast<int>((kHeadSmemMax - 1024 - tab_bytes - bar_bytes) / p.stage_bytes);
-  stages = std::min(stages, 8);
-  if (const char* s = getenv("SC_HEAD_STAGES")) stages = std::max(1, std::min(stages, atoi(s)));
-  if (stages < 2) return sc::set_error(SC_ERR_UNSUPPORTED, "sc_head_loss_fwd_bwd: head too wide for the ring");
-  p.stages = stages;
-  p.tab_off = stages * p.stage_bytes;
-  p.bar_off = (p.tab_off + tab_bytes + 7) / 8 * 8;
-  const size_t smem = 1024 + p.bar_off + 8 * (2 * stages + 4) + 16;
-
-  CUtensorMap map_x;
-  if (!make_map(&map_x, b.x, head->d, b.rows, b.ldx, sc::kBM))
-    return sc::set_error(SC_ERR_CUDA, "sc_head_loss_fwd_bwd: cuTensorMapEncodeTiled failed");
-  static std::once_flag attr_once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(attr_once, [] {
-    attr_err = cudaFuncSetAttribute(sc::head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(kHeadSmemMax));
-  });
-  if (attr_err) return sc::set_error(SC_ERR_CUDA, "sc_head_loss_fwd_bwd: %s", cudaGetErrorString(attr_err));
+  const int bar_bytes = 8 * (2 * 32 + 4) + 16;
+  const int64_t budget = static_cast<int64_t>(kHeadSmemMax) - 1024 - tab_bytes - bar_bytes;
   const int sms = sc::device_sms();
-  const int grid = static_cast<int>(std::min<int64_t>(p.n_tiles, sms));
-  sc::head_kernel<<<grid, sc::kHeadThreads, smem, static_cast<cudaStream_t>(stream)>>>(map_x, head->map_w, p);
-  sc::note_launch("head_tcgen05");
-  if (cudaError_t e = cudaGetLastError())
-    return sc::set_error(SC_ERR_CUDA, "sc_head_loss_fwd_bwd: %s", cudaGetErrorString(e));
+  const int64_t n_tiles = (b.rows + sc::kBM - 1) / sc::kBM;
+  // the launch shape needs the ring's smem size; the ring needs to know whether W is halved:
+  // plan for the pair first (the smem size only shrinks for single CTAs' larger W stages)
+  bool pair = false;
+  HeadLaunch hl;
+  bool x3d = false;
+  size_t smem = 0;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    const bool want_pair = attempt == 0;
+    p.w_stage_bytes = (want_pair ? head->n_cols / 2 : head->n_cols) * sc::kBK * 2;
+    // x: 3-D boxes of kbs k-blocks (rows read kbs*128 B at a time) when d % 64 == 0; as many
+    // x bytes in flight as fit next to >= 3 W stages (>= 2 for wide heads)
+    x3d = head->d % sc::kBK == 0 && !(std::getenv("SC_HEAD_X2D"));
+    int kbs_max = x3d ? 4 : 1, kbs_min = 1;
+    if (const char* e = std::getenv("SC_HEAD_KBS")) kbs_min = kbs_max = std::max(1, std::atoi(e));
+    int64_t best_score = -1;
+    int best_kbs = 1, best_xs = 0, best_ws = 0;
+    for (int kbs = kbs_min; kbs <= kbs_max; kbs *= 2) {
+      if (kbs > p.n_kb && kbs > 1) break;
+      for (int xs = 2; xs <= 16; ++xs) {
+        const int64_t xbytes = static_cast<int64_t>(xs) * kbs * a_bytes;
+        const int64_t rest = budget - xbytes;
+        if (rest < 0) break;
+        const int ws = static_cast<int>(std::min<int64_t>(16, rest / p.w_stage_bytes));
+        // measured (cfg2, d = 2048): 5-6 W stages next to ~96 KB of x beat deeper x rings
+        int ws_min = p.w_stage_bytes > 32 * 1024 ? 2 : 5;
+        if (const char* e = std::getenv("SC_HEAD_WSTAGES")) ws_min = std::max(ws_min, std::atoi(e));
+        if (ws < ws_min) break;
+        // prefer more x bytes in flight, then longer contiguous runs, then more W stages
+        const int64_t score = xbytes * 64 + kbs * 16 + ws;
+        if (score > best_score) {
+          best_score = score;
+          best_kbs = kbs;
+          best_xs = xs;
+          best_ws = ws;
+        }
+      }
+    }
+    if (best_xs < 2) return sc::set_error(SC_ERR_UNSUPPORTED, "sc_head_loss_fwd_bwd: head too wide for the ring");
+    if (best_kbs == 1) x3d = false;
+    p.kbs = best_kbs;
+    p.n_xb = (p.n_kb + p.kbs - 1) / p.kbs;
+    p.x_stages = best_xs;
+    p.w_stages = best_ws;
+    p.x_stage_bytes = p.kbs * a_bytes;
+    p.w_ring_off = p.x_stages * p.x_stage_bytes;
+    p.tab_off = p.w_ring_off + p.w_stages * p.w_stage_bytes;
+    p.bar_off = (p.tab_off + tab_bytes + 7) / 8 * 8;
+    smem = 1024 + p.bar_off + 8 * (2 * p.x_stages + 2 * p.w_stages + 4) + 16;
+    static std::once_flag attr_once;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(attr_once, [] {
+      attr_err = cudaFuncSetAttribute(sc::head_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(kHeadSmemMax));
+      if (!attr_err)
+        attr_err = cudaFuncSetAttribute(sc::head_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(kHeadSmemMax));
+    });
+    if (attr_err) return sc::set_error(SC_ERR_CUDA, "sc_head_loss_fwd_bwd: %s", cudaGetErrorString(attr_err));
+    hl = pick_launch(smem, sms, n_tiles);
+    if (want_pair && !(hl.pair && head->map_ok[1])) continue;  // re-plan the ring for a lone CTA
+    pair = want_pair;
+    break;
+  }
+  p.n_units = pair ? (b.rows + 2 * sc::kBM - 1) / (2 * sc::kBM) : n_tiles;
+  CUtensorMap map_x;
+  p.x3d = x3d ? 1 : 0;
+  if (x3d ? !make_map3(&map_x, b.x, head->d, b.rows, b.ldx, p.kbs)
+          : !make_map(&map_x, b.x, head->d, b.rows, b.ldx, sc::kBM))
+    return sc::set_error(SC_ERR_CUDA, "sc_head_loss_fwd_bwd: cuTensorMapEncodeTiled failed");
+  const int64_t units = std::max<int64_t>(1, std::min<int64_t>(pair ? hl.units : sms, p.n_units));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t le = cudaSuccess;
+  if (pair) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(2 * units));
+    cfg.blockDim = dim3(sc::kHeadThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    le = cudaLaunchKernelEx(&cfg, sc::head_kernel<true>, map_x, head->map_w[1], p);
+    sc::note_launch("head_tcgen05_pair");
+  } else {
+    sc::head_kernel<false><<<static_cast<unsigned>(units), sc::kHeadThreads, smem, st>>>(map_x, head->map_w[0], p);
+    sc::note_launch("head_tcgen05");
+  }
+  if (le) return sc::set_error(SC_ERR_CUDA, "sc_head_loss_fwd_bwd: %s", cudaGetErrorString(le));
+  if (cudaError_t e2 = cudaGetLastError())
+    return sc::set_error(SC_ERR_CUDA, "sc_head_loss_fwd_bwd: %s", cudaGetErrorString(e2));
   return SC_OK;
 }
 

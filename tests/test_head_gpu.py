@@ -113,12 +113,22 @@ def gt_for(spec, rows, seed):
     return hb["gt_off"], hb["gt_lab"]
 
 
+def explicit_spec(C, lists):
+    _, _, synth, _ = _mods()
+    return synth.ContextSpec(C, [[np.asarray(l, dtype=np.int32) for l in lists]], 0.0, 10.0)
+
+
+# head columns: each list padded to 16, the total to 32 (sc_head_info)
 SPECS = {
-    "cfg1": lambda s: s.config_context(1),                      # 18 mapped -> 32 columns
-    "cfg2": lambda s: s.config_context(2),                      # 180 mapped -> 192 columns
-    "w256": lambda s: custom_spec(1000, (100, 100, 56), 9),     # 256 columns, one MMA, 2 accumulators
-    "w300": lambda s: custom_spec(1000, (120, 100, 80), 10),    # two MMAs of 160, one accumulator
-    "w512": lambda s: custom_spec(1000, (200, 150, 100, 62), 11),  # two MMAs of 256
+    "cfg1": lambda s: s.config_context(1),                      # (9,3,6) -> 16+16+16 -> 64 columns
+    "cfg2": lambda s: s.config_context(2),                      # (90,30,60) -> 96+32+64 = 192
+    "w256": lambda s: custom_spec(1000, (96, 96, 64), 9),       # 256 columns, one MMA, 2 accumulators
+    "w300": lambda s: custom_spec(1000, (120, 100, 80), 10),    # 128+112+80 = 320: two MMAs of 160, one accumulator
+    "w512": lambda s: custom_spec(1000, (192, 144, 96, 62), 11),  # 496 -> 512: two MMAs of 256
+    "d8": lambda s: custom_spec(1000, (10, 20, 30, 5, 7, 3, 50, 1), 12),  # D' = 8 lists
+    # overlapping lists (reading A5): list 1 keeps only 41..60, list 2 is empty, list 3 after it
+    "ovl": lambda s: explicit_spec(300, [list(range(0, 41)), list(range(20, 61)), list(range(5, 30)),
+                                         list(range(100, 117)) + [3]]),
 }
 
 
@@ -133,6 +143,8 @@ SPECS = {
     ("w300", 1024, 700, "csr"),
     ("w512", 512, 513, "mask"),
     ("cfg2", 2048, 1, "csr"),
+    ("d8", 256, 1500, "csr"),
+    ("ovl", 192, 900, "mask"),
 ])
 def test_head_exact(name, d, rows, mode):
     torch, sc, synth, _ = _mods()
@@ -193,6 +205,7 @@ def test_head_errors():
     _, W, b = synth.head_operands(spec.C, 64, 1, seed=1, kind="int")
     head = sc.Head(ctx, bits_to_dev(W), torch.from_numpy(b).cuda())
     assert head.info() == (64, 192)
+    assert sc.Head(ctx, bits_to_dev(synth.head_operands(spec.C, 8, 1, seed=1)[1]), None).info() == (8, 192)
     x = torch.zeros((10, 64), dtype=torch.bfloat16, device="cuda")
     with pytest.raises(sc.ScError):  # loss without ground truth
         sc.sc_head_loss_fwd_bwd(ctx, head, x, loss_row=torch.zeros(10, device="cuda"))
@@ -213,6 +226,25 @@ def test_head_errors():
     ctxb = sc.Context(big.C, big.lists, big.tau, big.k, multi_app=True)
     with pytest.raises(sc.ScError, match="UNSUPPORTED"):
         sc.Head(ctxb, bits_to_dev(W), None)
+
+
+@pytest.mark.parametrize("q", [1, 2])
+@pytest.mark.parametrize("name,rows", [("cfg2", 148 * 128 * 2 + 1000), ("w300", 5000), ("cfg1", 300), ("w512", 700)])
+def test_head_single_and_pair(q, name, rows, monkeypatch):
+    """Lone CTAs (cta_group::1, M = 128) and CTA pairs (cta_group::2, M = 256, W halves in the
+    two CTAs), SC_HEAD_CLUSTER; unit counts that leave some CTAs without rows in the last step,
+    odd tile counts (a pair's second CTA past the end)."""
+    torch, sc, synth, _ = _mods()
+    spec = SPECS[name](synth)
+    d = 320
+    x, W, b = synth.head_operands(spec.C, d, rows, seed=q + rows, kind="int")
+    gt_off, gt_lab = gt_for(spec, rows, seed=q)
+    w = weights(spec, gt_off, gt_lab)
+    monkeypatch.setenv("SC_HEAD_CLUSTER", str(q))
+    g = run_head(spec, x, W, b, gt_off, gt_lab, w=w, mode="mask", grad_scale=1.0 / rows)
+    assert sc.sc_last_kernel() == ("head_tcgen05_pair" if q == 2 else "head_tcgen05")
+    o, _, _ = oracle_eval(spec, x, W, b, gt_off, gt_lab, w=w, grad_scale=1.0 / rows)
+    compare_exact(g, o)
 
 
 def margins_fragile(z, spec, G, tau, eps):
