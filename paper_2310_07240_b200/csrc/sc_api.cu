@@ -193,12 +193,12 @@ sc_status run_eval(const sc_context_s* ctx, const sc_batch* b, const float* w, f
   const bool whole_rows = W * p.ld_bytes <= stage_cap && force_chunk == 0;
   // mapped labels in registers when whole rows fit a stage and |W| <= 1024
   int epl = 0;
-  // Lane-resident entries cut the per-row instruction count; they pay when the row is
-  // short per mapped label (measured: bf16 cfg2, 11 B/label, 1.6x faster), while the
-  // shared-list path streams f32 cfg2 (22 B/label) 1-3 % faster.
-  const bool compute_bound = p.ld_bytes < 16 * static_cast<int64_t>(std::max(ctx->max_ent, 1));
+  // Lane-resident entries cut the per-row instruction count (bf16 cfg2: 1.6x faster than the
+  // shared list); with the batch epilogue moved after the stage release they also stream
+  // f32 cfg2 fastest (0.592 vs 0.625 ms, 7.09 TB/s), so they are the default wherever whole
+  // rows fit a stage.  SC_EPL=0 forces the shared-list path.
   const char* epl_env = std::getenv("SC_EPL");
-  const bool want_epl = epl_env ? std::atoi(epl_env) != 0 : compute_bound;
+  const bool want_epl = epl_env ? std::atoi(epl_env) != 0 : true;
   if (whole_rows && ctx->max_ent <= 1024 && want_epl) epl = std::max(0, sc::eval_epl_for(ctx->max_ent));
   int64_t logits_region;
   p.ng = 1;

@@ -325,6 +325,7 @@ __global__ void __launch_bounds__(kThreads, 1) eval_kernel(const EvalParams p) {
     int st_idx = grp;
     uint32_t ph = 0;
     const UnitSched us(p);
+    int lim = 32 - 2 * (cw % 16);  // first batch size of this warp (staggered), then 32
     for (int64_t i = grp; i < us.count; i += ng) {
       const int64_t u = us.unit(i);
       const int64_t r0 = u * p.R;
@@ -352,11 +353,20 @@ __global__ void __launch_bounds__(kThreads, 1) eval_kernel(const EvalParams p) {
         float zp, zm;
         uint32_t kp, km;
         scan_vals<EPL>(le, pm, zs, zp, kp, zm, km);
+        if (b.n == lim) {  // several rows per warp in this stage
+          finish_batch(p, b, wtab, lane);
+          lim = 32;
+        }
         deposit(b, lane, zp, kp, zm, km, G, a, row);
-        if (b.n == 32) finish_batch(p, b, wtab, lane);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(empty + st_idx);
+      // the batch epilogue runs after the stage is released, and the warps' batch boundaries
+      // are staggered (lim) so they do not all hold the pipeline in the same stage
+      if (b.n == lim) {
+        finish_batch(p, b, wtab, lane);
+        lim = 32;
+      }
       st_idx += ng;
       if (st_idx >= p.stages) { st_idx -= p.stages; ph ^= 1u; }
     }
@@ -381,6 +391,7 @@ __global__ void __launch_bounds__(kThreads, 1) eval_kernel(const EvalParams p) {
       cur_app = static_cast<int32_t>(a);
     };
     const UnitSched us(p);
+    int lim = 32 - 2 * (cw % 16);  // first batch size of this warp (staggered), then 32
     for (int64_t i = 0; i < us.count; ++i) {
       const int64_t u = us.unit(i);
       const int64_t r0 = u * p.R;
@@ -410,12 +421,19 @@ __global__ void __launch_bounds__(kThreads, 1) eval_kernel(const EvalParams p) {
           }
           warp_argmax(zp, kp);
           warp_argmax(zm, km);
+          if (b.n == lim) {  // several rows per warp in this stage
+            finish_batch(p, b, wtab, lane);
+            lim = 32;
+          }
           deposit(b, lane, zp, kp, zm, km, G, a, row);
-          if (b.n == 32) finish_batch(p, b, wtab, lane);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(empty + s);
         if (++s == p.stages) { s = 0; phase ^= 1u; }
+        if (b.n == lim) {  // after the release; staggered over the warps (see the EPL path)
+          finish_batch(p, b, wtab, lane);
+          lim = 32;
+        }
       } else {
         const bool mine = rows_here > 0;
         const int64_t row = r0 + cw;
@@ -456,7 +474,10 @@ __global__ void __launch_bounds__(kThreads, 1) eval_kernel(const EvalParams p) {
           warp_argmax(zp, kp);
           warp_argmax(zm, km);
           deposit(b, lane, zp, kp, zm, km, G, a, row);
-          if (b.n == 32) finish_batch(p, b, wtab, lane);
+          if (b.n == lim) {
+            finish_batch(p, b, wtab, lane);
+            lim = 32;
+          }
         }
       }
     }
