@@ -85,6 +85,8 @@ def lib():
         L.orc_ranges_weights.argtypes = [I32, P, P]
         L.orc_sample.restype = ctypes.c_int
         L.orc_sample.argtypes = [P, I64, P, I64, P, P, P]
+        L.orc_gt_hist.restype = ctypes.c_int
+        L.orc_gt_hist.argtypes = [P, I64, P, P, P, P, P]
         L.orc_eval.restype = ctypes.c_int
         L.orc_eval.argtypes = [P, I64, I64, I32, P, P, P, P, P, D] + [P] * 10
         _lib = L
@@ -239,6 +241,19 @@ class Oracle:
         return w
 
     # ---- whole batch ----
+    def gt_hist(self, gt_off, gt_lab, app=None):
+        """Ground truth only: (gt_mask [rows], hist_gt [n_apps*256]) — orc_gt_hist."""
+        gt_off = np.ascontiguousarray(gt_off, dtype=np.int64)
+        rows = len(gt_off) - 1
+        gt_lab = np.ascontiguousarray(gt_lab if len(gt_lab) else [0], dtype=np.int32)
+        if app is not None:
+            app = np.ascontiguousarray(app, dtype=np.uint16)
+        gm = np.zeros(max(rows, 1), np.uint8)
+        H = np.zeros(self.n_apps * 256, np.uint64)
+        if lib().orc_gt_hist(ctypes.byref(self._ctx), rows, _p(gt_off), _p(gt_lab), _p(app), _p(gm), _p(H)) != 0:
+            raise ValueError("oracle rejected the ground truth (out-of-range id)")
+        return gm[:rows], H
+
     def eval(self, logits, gt_off=None, gt_lab=None, app=None, w=None, grad_scale: float = 1.0,
              want_loss: bool = True):
         """All outputs for a batch.  logits: float32 [rows, ld] or uint16 (bf16 bits).

@@ -435,6 +435,34 @@ int orc_eval(const orc_ctx* x, int64_t rows, int64_t ld, int32_t dtype, const vo
   return rc;
 }
 
+/* The ground-truth-only pass (rows a2 + a6 of SURVEY.md §8(a)): G_i = the lists the
+ * ground-truth labels of input i hit (Multi-Select: the raw list set,
+ * PAPER.md:2031) and the mask histogram hist_gt[a][G_i] += 1 whose entries give the N_i
+ * counts.  The same per-row definitions orc_eval uses, without logits,
+ * so full-size tests can build the weights before the full pass.  Any output may be NULL;
+ * hist_gt ACCUMULATES.  Returns 0, or -1 on an out-of-range id. */
+int orc_gt_hist(const orc_ctx* x, int64_t rows, const int64_t* gt_off, const int32_t* gt_lab,
+                const uint16_t* app, uint8_t* gt_mask, uint64_t* hist_gt) {
+  const int32_t C = x->C;
+  int8_t* cat = (int8_t*)malloc((size_t)x->n_apps * (size_t)(C > 0 ? C : 1));
+  int rc = 0;
+  for (int32_t a = 0; a < x->n_apps; ++a) orc_compile(x, a, cat + (int64_t)a * C);
+  for (int64_t i = 0; i < rows && rc == 0; ++i) {
+    const int32_t a = app ? (int32_t)app[i] : 0;
+    if (a >= x->n_apps) { rc = -1; break; }
+    for (int64_t t = gt_off[i]; t < gt_off[i + 1]; ++t)
+      if (gt_lab[t] < 0 || gt_lab[t] >= C) rc = -1;
+    if (rc) break;
+    const int32_t* gl = gt_lab + gt_off[i];
+    const int64_t gn = gt_off[i + 1] - gt_off[i];
+    const uint32_t G = x->order == 2 ? orc_gt_set_raw(x, a, gl, gn) : orc_gt_set(cat + (int64_t)a * C, gl, gn);
+    if (gt_mask) gt_mask[i] = (uint8_t)G;
+    if (hist_gt) hist_gt[(int64_t)a * 256 + G] += 1;
+  }
+  free(cat);
+  return rc;
+}
+
 /* ---------------------------------------------------------------- value ranges */
 
 /* Value-ranges applications: the API returns a score O_i (e.g. a

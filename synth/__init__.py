@@ -246,6 +246,20 @@ class Workload:
                               off.ctypes.data, lab.ctypes.data, logits.ctypes.data)
         return dict(logits=logits[:n], gt_off=off, gt_lab=lab[: int(off[-1])], app=app[:n])
 
+    def host_gt(self, row0: int, n: int):
+        """Ground truth (and app ids) of rows [row0, row0+n) only — no logits."""
+        lib = _host_lib()
+        sp = self._spec(self._mapped.ctypes.data, self._woff.ctypes.data, self._wlab.ctypes.data)
+        cnt = np.empty(max(n, 1), dtype=np.int64)
+        lib.synth_host_gt_count(ctypes.byref(sp), row0, n, cnt.ctypes.data)
+        off = np.zeros(n + 1, dtype=np.int64)
+        off[1:] = np.cumsum(cnt[:n])
+        lab = np.empty(max(int(off[-1]), 1), dtype=np.int32)
+        lib.synth_host_gt_fill(ctypes.byref(sp), row0, n, off.ctypes.data, lab.ctypes.data)
+        app = np.empty(max(n, 1), dtype=np.uint16)
+        lib.synth_host_apps(ctypes.byref(sp), row0, n, app.ctypes.data)
+        return dict(gt_off=off, gt_lab=lab[: int(off[-1])], app=app[:n])
+
     # ---- device (torch) ----
     def device_batch(self, row0: int, n: int, device="cuda", with_app: bool | None = None):
         """Rows [row0, row0+n) generated on the GPU by synth_cuda.cu (torch tensors)."""

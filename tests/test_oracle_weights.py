@@ -85,3 +85,23 @@ def test_absent_mask_weight_zero():
     assert w[0] == pytest.approx(15 / 10) and w[1] == pytest.approx(15 / 5)
     assert w[2] == 0.0          # no input touches class 1 alone -> N = 0 -> w = 0 (reading A13)
     assert w[3] == pytest.approx(15 / 5)  # {0,1} intersects the five {0} inputs
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4])
+def test_gt_hist_pass_agrees_with_full_pass(cfg):
+    """orc_gt_hist (ground truth only, used to build the full-size tests' weights) gives the
+    same G_i and mask histogram as the full pass, for every decision pattern."""
+    import synth
+    spec = synth.config_context(cfg)
+    wl = synth.Workload(spec, seed=cfg)
+    b = wl.host_batch(1234, 600)
+    g = wl.host_gt(1234, 600)
+    for k in ("gt_off", "gt_lab", "app"):
+        np.testing.assert_array_equal(b[k], g[k])
+    app = b["app"] if spec.n_apps > 1 else None
+    for order in (0, 1, 2):
+        orc = Oracle.from_spec(spec, order=order)
+        r = orc.eval(b["logits"], b["gt_off"], b["gt_lab"], app=app, want_loss=False)
+        gm, H = orc.gt_hist(g["gt_off"], g["gt_lab"], app=app)
+        np.testing.assert_array_equal(gm, r["gt_mask"])
+        np.testing.assert_array_equal(H, r["hist_gt"])

@@ -7,7 +7,10 @@ for args in "--config 2 --dtype f32 --kernel tma" "--config 2 --dtype f32 --kern
             "--config 3 --dtype f32 --kernel tma" "--config 3 --dtype f32 --kernel gather" \
             "--config 3 --dtype bf16 --kernel tma" "--config 3 --dtype bf16 --kernel gather" \
             "--config 4 --dtype f32 --kernel tma" "--config 4 --dtype f32 --kernel gather" \
-            "--config 1 --dtype f32 --kernel tma" "--config 1 --dtype f32 --kernel gather"; do
+            "--config 4 --dtype bf16 --kernel tma" "--config 4 --dtype bf16 --kernel gather" \
+            "--config 5 --dtype f32" "--config 5 --dtype bf16" \
+            "--config 1 --dtype f32 --kernel tma" "--config 1 --dtype f32 --kernel gather" \
+            "--config 2 --dtype f32 --order app_choice" "--config 2 --dtype f32 --order multi_select"; do
   tag=$(echo $args | tr -d ' -' )
   timeout 300 python bench.py $args --steps ${STEPS:-100} --warmup 5 --no-cpu-baseline --no-e2e > $OUT/m_$tag.json 2> $OUT/m_$tag.err
   python - "$OUT/m_$tag.json" "$args" <<'PY'
