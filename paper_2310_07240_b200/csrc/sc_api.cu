@@ -66,6 +66,9 @@ sc::DevContext dev_ctx(const sc_context_s* c) {
   d.ent = c->d_ent;
   d.ent_off = c->d_ent_off;
   d.nlists = c->d_nlists;
+  d.lent = c->d_lent;
+  d.lent_off = c->d_lent_off;
+  d.lslot = c->d_lslot;
   d.C = c->C;
   d.n_apps = c->n_apps;
   d.max_ent = c->max_ent;
@@ -84,9 +87,12 @@ sc_status check_batch_common(const sc_context_s* ctx, const sc_batch* b) {
   return SC_OK;
 }
 
-double gather_threshold() {
+// Largest fraction of touched 128-B lines at which the sector-sparse gather is chosen.
+// Measured crossovers on B200: cfg3 f32 (0.81 touched) gather 5.41 ms vs TMA 5.80 ms; cfg4
+// f32 (256 apps, 0.875 touched on average) gather 3.02 ms vs blocked TMA 2.38 ms.
+double gather_threshold(int n_apps) {
   const char* s = std::getenv("SC_GATHER_MAX_FRAC");
-  return s ? std::atof(s) : 0.9;
+  return s ? std::atof(s) : (n_apps > 1 ? 0.7 : 0.85);
 }
 
 int stage_kb_override() {
@@ -147,23 +153,39 @@ sc_status run_eval(const sc_context_s* ctx, const sc_batch* b, const float* w, f
   p.hist_pred = reinterpret_cast<unsigned long long*>(hist_pred);
   p.hist_gt = reinterpret_cast<unsigned long long*>(hist_gt);
 
+  // per-list patterns (application-choice order, Multi-Select) need every list's arg max
+  const int pat = ctx->order == SC_ORDER_API_OUTPUT ? 0 : 1;
+  const char* epl_env = std::getenv("SC_EPL");
+  const bool want_epl = epl_env ? std::atoi(epl_env) != 0 : true;
+  const int64_t force_chunk = std::getenv("SC_FORCE_CHUNK") ? std::atoll(std::getenv("SC_FORCE_CHUNK")) : 0;
+  const bool whole_rows = sc::kConsumerWarps * p.ld_bytes <= 64 * 1024 && force_chunk == 0;
+  // lane-resident entries on the TMA ring: whole rows per stage and |W| <= 1024
+  // (per-list patterns: <= 8 list-major slots per app, one per register slot)
+  const bool lane_ok = whole_rows && ctx->max_ent <= 1024 && want_epl &&
+                       (pat ? ctx->max_slots <= 8 : sc::eval_epl_for(ctx->max_ent) > 0);
   // ---- kernel choice: sector-sparse gather when the mapped labels leave enough row sectors untouched
   {
     const char* kenv = std::getenv("SC_KERNEL");
     const int dt = b->dtype == SC_BF16 ? 1 : 0;
     // HBM is read in 128-B lines here (measured: sector-sparse loads still move whole lines),
-    // so the sparse gather only pays when whole lines of the row stay untouched; it also
-    // wins for multi-app batches (no per-stage side-band / per-row context switch cost).
+    // so the sparse gather only pays when whole lines of the row stay untouched.  Multi-app
+    // batches stream on the TMA ring with a blocked schedule (cfg4, B200: f32 2.38 ms vs
+    // 2.96 ms gather, bf16 1.42 ms vs 5.17 ms).
     const int64_t lines_row = (static_cast<int64_t>(ctx->C) * elt + 127) / 128;
     const double frac = static_cast<double>(ctx->touched_lines[dt]) / (static_cast<double>(lines_row) * ctx->n_apps);
-    bool gather = ctx->max_ent <= 1024 && (frac <= gather_threshold() || ctx->n_apps > 1);
+    bool gather = ctx->max_ent <= 1024 && frac <= gather_threshold(ctx->n_apps);
     if (kenv && std::string(kenv) == "tma") gather = false;
     if (kenv && std::string(kenv) == "gather" && ctx->max_ent <= 1024) gather = true;
-    if (ctx->order != SC_ORDER_API_OUTPUT) {
-      // per-list maxima (application-choice order, Multi-Select) run on the gather kernel
+    if (pat) {
+      // per-list maxima: on the TMA ring with lane-resident entries, or on the gather kernel
+      // (always when rows are wider than a stage allows)
       if (ctx->max_ent > 1024)
         return fail(SC_ERR_UNSUPPORTED, "this decision pattern supports at most 1024 mapped labels per app");
-      gather = true;
+      // B200 cfg2: application-choice f32 0.77 ms (TMA slots) vs 0.83 ms (gather), bf16 0.55 ms;
+      // Multi-Select f32 0.89 vs 0.86 ms; cfg4 f32 application-choice 2.98 vs 3.34 ms
+      gather = !lane_ok;
+      if (kenv && std::string(kenv) == "tma" && lane_ok) gather = false;
+      if (kenv && std::string(kenv) == "gather") gather = true;
     }
     if (gather) {
       p.ld_flavor = std::getenv("SC_LD_FLAVOR") ? std::atoi(std::getenv("SC_LD_FLAVOR")) : 0;
@@ -189,17 +211,13 @@ sc_status run_eval(const sc_context_s* ctx, const sc_batch* b, const float* w, f
   const int W = sc::kConsumerWarps;
   const int64_t stage_cap = 64 * 1024;
   p.copy_row_bytes = static_cast<int32_t>(round_up(static_cast<int64_t>(ctx->C) * elt, 16));
-  const int64_t force_chunk = std::getenv("SC_FORCE_CHUNK") ? std::atoll(std::getenv("SC_FORCE_CHUNK")) : 0;
-  const bool whole_rows = W * p.ld_bytes <= stage_cap && force_chunk == 0;
   // mapped labels in registers when whole rows fit a stage and |W| <= 1024
   int epl = 0;
   // Lane-resident entries cut the per-row instruction count (bf16 cfg2: 1.6x faster than the
   // shared list); with the batch epilogue moved after the stage release they also stream
   // f32 cfg2 fastest (0.592 vs 0.625 ms, 7.09 TB/s), so they are the default wherever whole
   // rows fit a stage.  SC_EPL=0 forces the shared-list path.
-  const char* epl_env = std::getenv("SC_EPL");
-  const bool want_epl = epl_env ? std::atoi(epl_env) != 0 : true;
-  if (whole_rows && ctx->max_ent <= 1024 && want_epl) epl = std::max(0, sc::eval_epl_for(ctx->max_ent));
+  if (lane_ok) epl = pat ? std::max(1, ctx->max_slots) : sc::eval_epl_for(ctx->max_ent);
   int64_t logits_region;
   p.ng = 1;
   if (epl > 0) {
@@ -245,7 +263,7 @@ sc_status run_eval(const sc_context_s* ctx, const sc_batch* b, const float* w, f
   int64_t pmtab_bytes = 0;
   if (epl > 0) {
     p.ent_mode = 3;  // lane registers
-    if (ctx->n_apps == 1) {
+    if (ctx->n_apps == 1 && !pat) {
       p.pmtab_bits = ctx->nlists[0];
       pmtab_bytes = (int64_t(1) << p.pmtab_bits) * 32 * 4;
     }
@@ -282,10 +300,14 @@ sc_status run_eval(const sc_context_s* ctx, const sc_batch* b, const float* w, f
 
   p.split_copy = std::getenv("SC_SPLIT_COPY") ? 1 : 0;
   p.no_evict_first = std::getenv("SC_NO_EVICT_FIRST") ? 1 : 0;
-  p.blocked = std::getenv("SC_BLOCKED") ? std::atoi(std::getenv("SC_BLOCKED")) : 0;
+  // Unit schedule: round-robin for one application; one contiguous block of units per CTA
+  // when rows carry application ids.  With round-robin every CTA works inside the same
+  // application at once and cfg4 (contiguous 2^18-row blocks per app) ran at half the
+  // bandwidth (bf16 2.90 ms vs 1.42 ms blocked, f32 3.56 vs 2.38 ms, B200).
+  p.blocked = std::getenv("SC_BLOCKED") ? std::atoi(std::getenv("SC_BLOCKED")) : (b->app ? 1 : 0);
   const int grid = static_cast<int>(std::min<int64_t>(p.nunits, di.sms));
-  if (cudaError_t e = sc::launch_eval(p, epl, grid, smem, st)) return cuda_fail(e, "eval kernel launch");
-  g_last_kernel = epl ? "tma_ring_epl" + std::to_string(epl) : "tma_ring_list";
+  if (cudaError_t e = sc::launch_eval(p, epl, pat, grid, smem, st)) return cuda_fail(e, "eval kernel launch");
+  g_last_kernel = epl ? (pat ? "tma_ring_lists_epl" : "tma_ring_epl") + std::to_string(epl) : "tma_ring_list";
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return SC_OK;
 }
@@ -391,6 +413,27 @@ sc_status sc_context_load(int32_t C, int32_t n_apps, const int32_t* n_lists, con
     ctx->max_ent = std::max(ctx->max_ent, ent_off[a + 1] - ent_off[a]);
   }
   if (ent.empty()) ent.push_back(0);
+  // per-list patterns: list-major slots (DevContext::lent) — list j's members in ascending
+  // label order, padded to 32 entries per slot, so a warp reduces one list per slot
+  std::vector<uint32_t> lent;
+  std::vector<int32_t> lent_off(n_apps + 1, 0);
+  std::vector<uint32_t> lslot(n_apps, 0);
+  if (order != SC_ORDER_API_OUTPUT) {
+    for (int32_t a = 0; a < n_apps; ++a) {
+      int slots = 0;
+      for (int32_t j = 0; j < n_lists[a]; ++j) {
+        const size_t before = lent.size();
+        for (int32_t e = ent_off[a]; e < ent_off[a + 1]; ++e)
+          if (sc::label_lists(static_cast<uint8_t>(ent[e] & 0xFFu), order) >> j & 1u) lent.push_back(ent[e]);
+        while ((lent.size() - before) % 32) lent.push_back(sc::kNone);
+        for (size_t q = before; q < lent.size(); q += 32, ++slots)
+          if (slots < 8) lslot[a] |= static_cast<uint32_t>(j) << (4 * slots);
+      }
+      lent_off[a + 1] = static_cast<int32_t>(lent.size());
+      ctx->max_slots = std::max(ctx->max_slots, slots);
+    }
+  }
+  if (lent.empty()) lent.push_back(sc::kNone);
   std::vector<uint8_t> nl(n_apps);
   for (int32_t a = 0; a < n_apps; ++a) nl[a] = static_cast<uint8_t>(n_lists[a]);
 
@@ -399,6 +442,12 @@ sc_status sc_context_load(int32_t C, int32_t n_apps, const int32_t* n_lists, con
   if (!e) e = cudaMalloc(&ctx->d_ent, ent.size() * 4);
   if (!e) e = cudaMalloc(&ctx->d_ent_off, ent_off.size() * 4);
   if (!e) e = cudaMalloc(&ctx->d_nlists, nl.size());
+  if (!e) e = cudaMalloc(&ctx->d_lent, lent.size() * 4);
+  if (!e) e = cudaMalloc(&ctx->d_lent_off, lent_off.size() * 4);
+  if (!e) e = cudaMalloc(&ctx->d_lslot, lslot.size() * 4);
+  if (!e) e = cudaMemcpy(ctx->d_lent, lent.data(), lent.size() * 4, cudaMemcpyHostToDevice);
+  if (!e) e = cudaMemcpy(ctx->d_lent_off, lent_off.data(), lent_off.size() * 4, cudaMemcpyHostToDevice);
+  if (!e) e = cudaMemcpy(ctx->d_lslot, lslot.data(), lslot.size() * 4, cudaMemcpyHostToDevice);
   if (!e) e = cudaMalloc(&ctx->d_done, sizeof(unsigned int));
   std::vector<uint8_t> catT(static_cast<size_t>(n_apps) * C);
   for (int32_t a = 0; a < n_apps; ++a)
@@ -424,6 +473,9 @@ sc_status sc_context_free(sc_context ctx) {
   cudaFree(ctx->d_cat);
   cudaFree(ctx->d_ent);
   cudaFree(ctx->d_ent_off);
+  cudaFree(ctx->d_lent);
+  cudaFree(ctx->d_lent_off);
+  cudaFree(ctx->d_lslot);
   cudaFree(ctx->d_nlists);
   cudaFree(ctx->d_done);
   cudaFree(ctx->d_catT);

@@ -9,21 +9,21 @@
 // per-list arg maxima over whole 16-column TMEM loads with a branch-free tree and never
 // looks a column's list up; P⁺ / P⁻ are then arg maxima over the <= 8 list winners.
 //
-// Persistent CTAs, 128-row tiles, in clusters of Q CTAs (Q in {1,2,4,8}), warp-specialised:
-//   warp 0      TMA producer: per 64-wide k-block, the CTA's x tile [128 x 64] and 1/Q of
-//               the compiled head W_𝕎 [n_cols x 64] (both K-major, 128-B swizzle), the W
-//               slice multicast to every CTA of the cluster: W (L2-resident, the same for all
-//               tiles) leaves L2 once per cluster instead of once per CTA.
+// Persistent CTAs (one per SM), 128-row tiles, warp-specialised:
+//   warp 0      x producer: per stage, kbs 64-wide k-blocks of the CTA's x tile [128 x 64]
+//               (one 3-D TMA box, K-major, 128-B swizzle, L2 evict-first).
+//   warp 6      W producer: one k-block of the compiled head W_𝕎 [n_cols x 64] per stage
+//               (k-block-major layout, L2 evict-last: W is re-read for every row tile).
 //   warp 1      allocates 512 TMEM columns; one lane issues tcgen05.mma (M=128, N <= 256,
-//               K=16, bf16 x bf16 -> fp32 in TMEM) and frees each stage in every CTA of the
-//               cluster with a multicast tcgen05.commit (the W slices it holds came from all
-//               of them); double-buffered accumulators when n_cols <= 256.
+//               K=16, bf16 x bf16 -> fp32 in TMEM) and frees the x / W stages with
+//               tcgen05.commit; double-buffered accumulators when n_cols <= 256.
 //   warps 2-5   epilogue: each thread owns one row (TMEM lane), tcgen05.ld its columns 16 at
 //               a time (the next load in flight while the current one is reduced), adds the
 //               bias, per-list arg max, split maxima by G_i, then finish_batch (decision,
 //               counters, loss, gradient).
-// The CTAs of a cluster step through the same number of tiles (a CTA past the last tile
-// computes a zero-filled one and discards it), so every multicast has all its receivers.
+// PAIR (opt-in, SC_HEAD_CLUSTER=2): CTA pairs run M = 256 MMAs with cta_group::2, each CTA
+// streaming its own 128 rows of x and half of W_𝕎; the leader's barriers count both CTAs'
+// bytes and a multicast tcgen05.commit frees the stages of both.
 #include "sc_device.cuh"
 #include "sc_host.h"
 

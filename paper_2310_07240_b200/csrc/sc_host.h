@@ -20,6 +20,10 @@ struct sc_context_s {
   unsigned int* d_done = nullptr;  // completion counter of the fused hist+weights pre-pass
   uint8_t* d_catT = nullptr;       // [C][n_apps] label-major category table (all-apps pass)
   int32_t n_ent_total = 0;
+  int32_t max_slots = 0;           // per-list patterns: most list-major 32-entry slots of an app
+  uint32_t* d_lent = nullptr;
+  int32_t* d_lent_off = nullptr;
+  uint32_t* d_lslot = nullptr;
 };
 
 namespace sc {

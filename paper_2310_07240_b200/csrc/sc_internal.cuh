@@ -21,6 +21,12 @@ struct DevContext {
   const uint32_t* ent;      // per app, mapped labels sorted by id: key = c << 8 | cat[c]
   const int32_t* ent_off;   // [n_apps+1]
   const uint8_t* nlists;    // [n_apps]  D'
+  // per-list patterns (application-choice order, Multi-Select), list-major slots: per app,
+  // list j's member labels (ascending keys) padded with kNone to a multiple of 32 — one
+  // 32-entry slot per lane position, every slot inside one list
+  const uint32_t* lent = nullptr;     // slot entries
+  const int32_t* lent_off = nullptr;  // [n_apps+1]  (multiples of 32)
+  const uint32_t* lslot = nullptr;    // [n_apps]  list of slot s in bits 4s..4s+3 (<= 8 slots)
   int32_t C, n_apps, max_ent;
   float tau, theta, k;
   int32_t order;            // kApiOutput / kAppChoice / kMultiSelect
@@ -118,7 +124,7 @@ cudaError_t launch_all_apps(const AllAppsParams& p, int grid, size_t smem, cudaS
 
 // Launchers (sc_kernels.cu).  Return cudaError_t of the launch.
 // epl > 0: lane-resident entries (|W| <= 32*epl, whole rows per stage); 0: generic list path.
-cudaError_t launch_eval(const EvalParams& p, int epl, int grid, size_t smem, cudaStream_t st);
+cudaError_t launch_eval(const EvalParams& p, int epl, int pat, int grid, size_t smem, cudaStream_t st);
 // Sector-sparse variant: epl = entries per lane capacity (1,2,4,8,16,32 -> |W| <= 32*epl).
 // pat 0: split maxima (API-output order); pat 1: per-list maxima (application-choice, Multi-Select).
 cudaError_t launch_gather(const EvalParams& p, int epl, int pat, int sms, cudaStream_t st);
@@ -126,6 +132,6 @@ cudaError_t launch_hist(const HistParams& p, int grid, size_t smem, cudaStream_t
 cudaError_t launch_weights(const unsigned long long* hist, float* w, int n_apps, cudaStream_t st);
 cudaError_t set_eval_smem_limit(size_t smem);
 // Smallest compiled lane-resident entry capacity for max_ent mapped labels (-1: none fits).
-int eval_epl_for(int max_ent);
+int eval_epl_for(int max_ent, int pat = 0);
 
 }  // namespace sc

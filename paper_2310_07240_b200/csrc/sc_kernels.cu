@@ -171,320 +171,6 @@ __device__ __forceinline__ void scan_vals(const LaneEnt<EPL>& le, uint32_t pm, c
   warp_argmax(zm, km);
 }
 
-// ------------------------------------------------------------------ fused evaluation kernel
-
-// The CTA's units: round-robin (u = blockIdx + i*grid) or one contiguous block per CTA.
-struct UnitSched {
-  int64_t base, stride, count;
-  __device__ __forceinline__ UnitSched(const EvalParams& p) {
-    if (p.blocked) {
-      const int64_t per = (p.nunits + gridDim.x - 1) / gridDim.x;
-      base = static_cast<int64_t>(blockIdx.x) * per;
-      stride = 1;
-      count = p.nunits - base < per ? p.nunits - base : per;
-      if (count < 0) count = 0;
-    } else {
-      base = blockIdx.x;
-      stride = gridDim.x;
-      count = (p.nunits - blockIdx.x + gridDim.x - 1) / gridDim.x;
-    }
-  }
-  __device__ __forceinline__ int64_t unit(int64_t i) const { return base + i * stride; }
-};
-
-// EPL > 0: whole rows per stage, mapped labels held in registers (|𝕎| <= 32*EPL).
-// EPL == 0: generic path — entries read from a shared/global list, rows may be split
-// into column chunks across stages (large C).
-template <int EPL, bool BF16>
-__global__ void __launch_bounds__(kThreads, 1) eval_kernel(const EvalParams p) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.bar_off);
-  uint64_t* empty = full + p.stages;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-  // ---- prologue: barriers, context entries and weights into shared memory
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < p.stages; ++s) {
-      mbar_init(full + s, 1);
-      mbar_init(empty + s, kConsumerWarps / p.ng);
-    }
-    fence_mbar_init();
-  }
-  uint32_t* ent_smem = reinterpret_cast<uint32_t*>(smem + p.ent_smem_off);
-  if (EPL == 0 && p.ent_mode == 0) {
-    const int n = p.ctx.ent_off[1];
-    for (int e = threadIdx.x; e < n; e += blockDim.x) ent_smem[e] = __ldg(p.ctx.ent + e);
-  }
-  float* wtab = p.wtab_off >= 0 ? reinterpret_cast<float*>(smem + p.wtab_off) : nullptr;
-  if (wtab)
-    for (int m = threadIdx.x; m < 256; m += blockDim.x) wtab[m] = __ldg(p.w + m);
-  __syncthreads();
-
-  if (warp == 0) {
-    // ================= TMA producer (one lane) =================
-    if (lane == 0) {
-      uint64_t pol = evict_first_policy();
-      if (p.no_evict_first) asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
-      int s = 0;
-      uint32_t phase = 0;
-      const UnitSched us(p);
-      for (int64_t i = 0; i < us.count; ++i) {
-        const int64_t u = us.unit(i);
-        const int64_t r0 = u * p.R;
-        const int nr = static_cast<int>((p.rows - r0 < p.R ? p.rows - r0 : (int64_t)p.R));
-        for (int kc = 0; kc < p.nchunks; ++kc) {
-          mbar_wait(empty + s, phase ^ 1u);
-          uint8_t* st = smem + static_cast<size_t>(s) * p.stage_bytes;
-          uint32_t bytes = 0;
-          const uint8_t* src_m = nullptr;
-          const uint8_t* src_a = nullptr;
-          uint32_t nb_m = 0, nb_a = 0;
-          if (kc == 0) {
-            if (p.gt_mask) {
-              const uintptr_t lo = reinterpret_cast<uintptr_t>(p.gt_mask + r0) & ~uintptr_t(15);
-              const uintptr_t hi = (reinterpret_cast<uintptr_t>(p.gt_mask + r0 + nr) + 15) & ~uintptr_t(15);
-              src_m = reinterpret_cast<const uint8_t*>(lo);
-              nb_m = static_cast<uint32_t>(hi - lo);
-            }
-            if (p.app) {
-              const uintptr_t lo = reinterpret_cast<uintptr_t>(p.app + r0) & ~uintptr_t(15);
-              const uintptr_t hi = (reinterpret_cast<uintptr_t>(p.app + r0 + nr) + 15) & ~uintptr_t(15);
-              src_a = reinterpret_cast<const uint8_t*>(lo);
-              nb_a = static_cast<uint32_t>(hi - lo);
-            }
-          }
-          if (p.nchunks == 1) {
-            bytes = static_cast<uint32_t>(nr * p.ld_bytes);
-          } else {
-            const int rem = p.copy_row_bytes - kc * p.chunk_bytes;
-            const uint32_t cb = static_cast<uint32_t>(rem < p.chunk_bytes ? rem : p.chunk_bytes);
-            bytes = cb * nr;
-          }
-          mbar_arrive_expect_tx(full + s, bytes + nb_m + nb_a);
-          if (p.nchunks == 1 && !p.split_copy) {
-            bulk_g2s(st, p.logits + r0 * p.ld_bytes, bytes, full + s, pol);
-          } else if (p.nchunks == 1) {
-            const uint32_t rb = static_cast<uint32_t>(p.ld_bytes);
-            for (int j = 0; j < nr; ++j) bulk_g2s(st + static_cast<size_t>(j) * rb, p.logits + (r0 + j) * p.ld_bytes, rb, full + s, pol);
-          } else {
-            const uint32_t cb = bytes / nr;
-            for (int j = 0; j < nr; ++j)
-              bulk_g2s(st + static_cast<size_t>(j) * p.chunk_bytes,
-                       p.logits + (r0 + j) * p.ld_bytes + static_cast<int64_t>(kc) * p.chunk_bytes, cb, full + s,
-                       pol);
-          }
-          if (nb_m) bulk_g2s(st + p.mask_off, src_m, nb_m, full + s, pol);
-          if (nb_a) bulk_g2s(st + p.app_off, src_a, nb_a, full + s, pol);
-          if (++s == p.stages) { s = 0; phase ^= 1u; }
-        }
-      }
-    }
-    return;
-  }
-
-  // ================= consumer warps =================
-  const int cw = warp - 1;
-  RowBatch b;
-  b.n = 0; b.zp = b.zm = 0.f; b.kp = b.km = kNone; b.G = 0; b.app = 0; b.row = 0;
-
-  auto row_app_mask = [&](const uint8_t* st, int64_t r0, int64_t row, uint32_t& a, uint32_t& G) {
-    a = 0;
-    if (p.app) {
-      const uintptr_t lo = reinterpret_cast<uintptr_t>(p.app + r0) & ~uintptr_t(15);
-      a = *reinterpret_cast<const uint16_t*>(st + p.app_off + (reinterpret_cast<uintptr_t>(p.app + row) - lo));
-    }
-    G = 0;
-    if (p.gt_mask) {
-      const uintptr_t lo = reinterpret_cast<uintptr_t>(p.gt_mask + r0) & ~uintptr_t(15);
-      G = st[p.mask_off + (reinterpret_cast<uintptr_t>(p.gt_mask + row) - lo)];
-    } else if (p.has_gt) {
-      G = warp_gt_mask(p, row, a, lane);
-    }
-  };
-
-  int s = 0;
-  uint32_t phase = 0;
-  if constexpr (EPL > 0) {
-    // ---- whole rows, lane-resident entries.  Consumer warps form NG groups of WG warps;
-    // CTA-local unit i lives in stage i % S and is consumed by group i % NG only, so a
-    // stage is released as soon as its WG warps are done (no CTA-wide stage barrier).
-    LaneEnt<EPL> le;
-    constexpr uint32_t kElt = BF16 ? 2u : 4u;
-    lane_ent_load(le, p.ctx.ent + __ldg(p.ctx.ent_off), __ldg(p.ctx.ent_off + 1) - __ldg(p.ctx.ent_off), 0, lane,
-                  kElt);
-    // single app: table of plus-masks per G value (one LDS per row instead of 8 selects)
-    uint32_t* pmtab = p.pmtab_off >= 0 ? reinterpret_cast<uint32_t*>(smem + p.pmtab_off) : nullptr;
-    if (pmtab) {
-      for (int g = cw; g < (1 << p.pmtab_bits); g += kConsumerWarps) pmtab[g * 32 + lane] = plus_mask(le, g);
-      asm volatile("bar.sync 1, %0;" ::"r"(kConsumerWarps * 32) : "memory");
-    }
-    const int ng = p.ng, wg = kConsumerWarps / p.ng;
-    const int grp = cw / wg, wi = cw % wg;
-    const uint32_t sbase = smem_addr(smem);
-    // this group's units are the CTA-local indices grp, grp+ng, ...: stage and phase advance by ng
-    int st_idx = grp;
-    uint32_t ph = 0;
-    const UnitSched us(p);
-    int lim = 32 - 2 * (cw % 16);  // first batch size of this warp (staggered), then 32
-    for (int64_t i = grp; i < us.count; i += ng) {
-      const int64_t u = us.unit(i);
-      const int64_t r0 = u * p.R;
-      const int nr = static_cast<int>((p.rows - r0 < p.R ? p.rows - r0 : (int64_t)p.R));
-      mbar_wait(full + st_idx, ph);
-      const uint32_t st_off = static_cast<uint32_t>(st_idx) * p.stage_bytes;
-      // side-band windows start at the 16-B boundary below row r0
-      const uint32_t m_base = st_off + p.mask_off + (p.gt_mask ? (reinterpret_cast<uintptr_t>(p.gt_mask + r0) & 15u) : 0u);
-      const uint32_t a_base = st_off + p.app_off + (p.app ? (reinterpret_cast<uintptr_t>(p.app + r0) & 15u) : 0u);
-      for (int j = wi; j < nr; j += wg) {
-        const int64_t row = r0 + j;
-        const uint32_t a = p.app ? lds_u16(sbase + a_base + 2u * j) : 0u;
-        uint32_t G = 0;
-        if (p.gt_mask) G = lds_u8(sbase + m_base + j);
-        else if (p.has_gt) G = warp_gt_mask(p, row, a, lane);
-        if (static_cast<int32_t>(a) != le.app) {
-          const int32_t e0 = __ldg(p.ctx.ent_off + a);
-          lane_ent_load(le, p.ctx.ent + e0, __ldg(p.ctx.ent_off + a + 1) - e0, static_cast<int32_t>(a), lane, kElt);
-        }
-        const uint32_t srow = sbase + st_off + static_cast<uint32_t>(j) * static_cast<uint32_t>(p.ld_bytes);
-        float zs[EPL];
-#pragma unroll
-        for (int t = 0; t < EPL; ++t) zs[t] = lds_z<BF16>(srow + le.off(t, kElt));
-        const uint32_t pm = pmtab ? lds_u32(sbase + p.pmtab_off + (G * 32 + lane) * 4) : plus_mask(le, G);
-        float zp, zm;
-        uint32_t kp, km;
-        scan_vals<EPL>(le, pm, zs, zp, kp, zm, km);
-        if (b.n == lim) {  // several rows per warp in this stage
-          finish_batch(p, b, wtab, lane);
-          lim = 32;
-        }
-        deposit(b, lane, zp, kp, zm, km, G, a, row);
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(empty + st_idx);
-      // the batch epilogue runs after the stage is released, and the warps' batch boundaries
-      // are staggered (lim) so they do not all hold the pipeline in the same stage
-      if (b.n == lim) {
-        finish_batch(p, b, wtab, lane);
-        lim = 32;
-      }
-      st_idx += ng;
-      if (st_idx >= p.stages) { st_idx -= p.stages; ph ^= 1u; }
-    }
-  } else {
-    // ---- generic: entries from a list, rows possibly split into column chunks
-    uint32_t* slot = p.ent_mode == 1 ? ent_smem + static_cast<size_t>(cw) * p.ent_slot : nullptr;
-    int32_t cur_app = -1;
-    const uint32_t* ents = p.ent_mode == 0 ? ent_smem : nullptr;
-    int32_t n_ent = p.ent_mode == 0 ? p.ctx.ent_off[1] : 0;
-    auto select_app = [&](uint32_t a) {
-      if (p.ent_mode == 0 || static_cast<int32_t>(a) == cur_app) return;
-      const int32_t e0 = __ldg(p.ctx.ent_off + a), e1 = __ldg(p.ctx.ent_off + a + 1);
-      n_ent = e1 - e0;
-      if (p.ent_mode == 1) {
-        __syncwarp();
-        for (int e = lane; e < n_ent; e += 32) slot[e] = __ldg(p.ctx.ent + e0 + e);
-        __syncwarp();
-        ents = slot;
-      } else {
-        ents = p.ctx.ent + e0;
-      }
-      cur_app = static_cast<int32_t>(a);
-    };
-    const UnitSched us(p);
-    int lim = 32 - 2 * (cw % 16);  // first batch size of this warp (staggered), then 32
-    for (int64_t i = 0; i < us.count; ++i) {
-      const int64_t u = us.unit(i);
-      const int64_t r0 = u * p.R;
-      const int nr = static_cast<int>((p.rows - r0 < p.R ? p.rows - r0 : (int64_t)p.R));
-      // rows of this warp: one per stage pass when chunked (R == W), else j = cw + W*t
-      const int rows_here = p.nchunks == 1 ? (nr > cw ? (nr - cw + kConsumerWarps - 1) / kConsumerWarps : 0)
-                                           : (cw < nr ? 1 : 0);
-      if (p.nchunks == 1) {
-        mbar_wait(full + s, phase);
-        const uint8_t* st = smem + static_cast<size_t>(s) * p.stage_bytes;
-        for (int j = cw; j < nr; j += kConsumerWarps) {
-          const int64_t row = r0 + j;
-          uint32_t a, G;
-          row_app_mask(st, r0, row, a, G);
-          select_app(a);
-          const uint8_t* rowp = st + static_cast<int64_t>(j) * p.ld_bytes;
-          float zp = -CUDART_INF_F, zm = -CUDART_INF_F;
-          uint32_t kp = kNone, km = kNone;
-          for (int e = lane; e < n_ent; e += 32) {
-            const uint32_t key = ents[e];
-            const float z = load_logit(rowp, key >> 8, BF16);
-            if ((G >> (key & 0xFFu)) & 1u) {
-              if (z > zp) { zp = z; kp = key; }
-            } else {
-              if (z > zm) { zm = z; km = key; }
-            }
-          }
-          warp_argmax(zp, kp);
-          warp_argmax(zm, km);
-          if (b.n == lim) {  // several rows per warp in this stage
-            finish_batch(p, b, wtab, lane);
-            lim = 32;
-          }
-          deposit(b, lane, zp, kp, zm, km, G, a, row);
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(empty + s);
-        if (++s == p.stages) { s = 0; phase ^= 1u; }
-        if (b.n == lim) {  // after the release; staggered over the warps (see the EPL path)
-          finish_batch(p, b, wtab, lane);
-          lim = 32;
-        }
-      } else {
-        const bool mine = rows_here > 0;
-        const int64_t row = r0 + cw;
-        uint32_t a = 0, G = 0;
-        float zp = -CUDART_INF_F, zm = -CUDART_INF_F;
-        uint32_t kp = kNone, km = kNone;
-        int pos = 0;
-        for (int kc = 0; kc < p.nchunks; ++kc) {
-          mbar_wait(full + s, phase);
-          const uint8_t* st = smem + static_cast<size_t>(s) * p.stage_bytes;
-          if (mine) {
-            if (kc == 0) {
-              row_app_mask(st, r0, row, a, G);
-              select_app(a);
-            }
-            const uint8_t* rowp = st + static_cast<int64_t>(cw) * p.chunk_bytes;
-            const uint32_t c_lo = static_cast<uint32_t>(kc) * p.chunk_elems;
-            const uint32_t c_hi = c_lo + p.chunk_elems;
-            int stop = n_ent;
-            for (int e = pos + lane; e < n_ent; e += 32) {
-              const uint32_t key = ents[e];
-              const uint32_t col = key >> 8;
-              if (col >= c_hi) { stop = e; break; }
-              const float z = load_logit(rowp, col - c_lo, BF16);
-              if ((G >> (key & 0xFFu)) & 1u) {
-                if (z > zp) { zp = z; kp = key; }
-              } else {
-                if (z > zm) { zm = z; km = key; }
-              }
-            }
-            pos = static_cast<int>(__reduce_min_sync(kFull, static_cast<uint32_t>(stop)));
-          }
-          __syncwarp();
-          if (lane == 0) mbar_arrive(empty + s);
-          if (++s == p.stages) { s = 0; phase ^= 1u; }
-        }
-        if (mine) {
-          warp_argmax(zp, kp);
-          warp_argmax(zm, km);
-          deposit(b, lane, zp, kp, zm, km, G, a, row);
-          if (b.n == lim) {
-            finish_batch(p, b, wtab, lane);
-            lim = 32;
-          }
-        }
-      }
-    }
-  }
-  if (b.n > 0) finish_batch(p, b, wtab, lane);
-}
-
 // ------------------------------------------------------------------ per-list maxima (NEXT f1)
 
 // The application-choice order and Multi-Select need the arg max of every list (P_j,
@@ -539,11 +225,102 @@ __device__ __forceinline__ void scan_lists(const LaneEnt<EPL>& le, int D, const 
   }
 }
 
+__device__ __forceinline__ void finish_lists_core(const EvalParams& p, RowBatch& b, const float (&zj)[8],
+                                                  const uint32_t (&kj)[8], const float* wtab_smem, int lane);
+
 // Epilogue of the application-choice order (Eq. app_choice) and Multi-Select (Eq.
 // multi-select) for the batch's rows, one row per lane; counters as in finish_batch.
 __device__ __forceinline__ void finish_lists(const EvalParams& p, RowBatch& b, ListBatch lb, const float* wtab_smem,
                                              int lane) {
   __syncwarp();
+  float zj[8];
+  uint32_t kj[8];
+  const int D = lane < b.n ? __ldg(p.ctx.nlists + b.app) : 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    zj[j] = j < D ? lb.z[lane * kListPad + j] : -CUDART_INF_F;
+    kj[j] = j < D ? lb.k[lane * kListPad + j] : kNone;
+  }
+  finish_lists_core(p, b, zj, kj, wtab_smem, lane);
+}
+
+// The per-list patterns on the TMA ring use list-major slots (DevContext::lent): slot t of
+// an application holds 32 labels of ONE list (lane l: entry t*32 + l), so a row needs one
+// warp arg max per slot — not one masked scan of every entry per list — and the list
+// maxima are assembled per lane (one row each) in the batch epilogue.
+template <int EPL>
+struct SlotEnt {
+  uint32_t key[EPL];  // c << 8 | cat[c], kNone for padding
+  uint32_t off[EPL];  // byte offset of the label in a row (0 for padding)
+  int ns;             // slots of the application (warp-uniform)
+  int32_t app;
+};
+
+template <int EPL>
+__device__ __forceinline__ void slot_ent_load(SlotEnt<EPL>& se, const DevContext& c, int32_t app, int lane,
+                                              uint32_t elt) {
+  const int32_t e0 = __ldg(c.lent_off + app), e1 = __ldg(c.lent_off + app + 1);
+  se.ns = (e1 - e0) >> 5;
+  se.app = app;
+#pragma unroll
+  for (int t = 0; t < EPL; ++t) {
+    const uint32_t k = t < se.ns ? __ldg(c.lent + e0 + t * 32 + lane) : kNone;
+    se.key[t] = k;
+    se.off[t] = k == kNone ? 0u : (k >> 8) * elt;
+  }
+}
+
+// a3 for one row: the arg max of every slot; lane `slot` keeps them (sz, sk).
+template <int EPL>
+__device__ __forceinline__ void scan_slots(const SlotEnt<EPL>& se, const float (&zs)[EPL], float (&sz)[EPL],
+                                           uint32_t (&sk)[EPL], int slot, int lane) {
+#pragma unroll
+  for (int t = 0; t < EPL; ++t) {
+    if (t < se.ns) {  // warp-uniform
+      float z = zs[t];
+      uint32_t k = se.key[t];
+      warp_argmax(z, k);
+      if (lane == slot) {
+        sz[t] = z;
+        sk[t] = k;
+      }
+    }
+  }
+}
+
+// Batch epilogue: each lane folds its row's slot maxima into list maxima (P_j, PAPER.md:2026,
+// :2050), then the shared per-list epilogue.
+template <int EPL>
+__device__ __forceinline__ void finish_slots(const EvalParams& p, RowBatch& b, const float (&sz)[EPL],
+                                             const uint32_t (&sk)[EPL], const float* wtab_smem, int lane) {
+  float zj[8];
+  uint32_t kj[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    zj[j] = -CUDART_INF_F;
+    kj[j] = kNone;
+  }
+  if (lane < b.n) {
+    const uint32_t lists = __ldg(p.ctx.lslot + b.app);
+    const int ns = (__ldg(p.ctx.lent_off + b.app + 1) - __ldg(p.ctx.lent_off + b.app)) >> 5;
+#pragma unroll
+    for (int t = 0; t < EPL; ++t) {
+      if (t < ns && sk[t] != kNone) {
+        const uint32_t j = (lists >> (4 * t)) & 15u;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (q == static_cast<int>(j) && beats(sz[t], sk[t], zj[q], kj[q])) {
+            zj[q] = sz[t];
+            kj[q] = sk[t];
+          }
+      }
+    }
+  }
+  finish_lists_core(p, b, zj, kj, wtab_smem, lane);
+}
+
+__device__ __forceinline__ void finish_lists_core(const EvalParams& p, RowBatch& b, const float (&zj)[8],
+                                                  const uint32_t (&kj)[8], const float* wtab_smem, int lane) {
   const bool active = lane < b.n;
   const unsigned act = __ballot_sync(kFull, active);
   const float tau = p.ctx.tau, theta = p.ctx.theta, k = p.ctx.k;
@@ -557,13 +334,6 @@ __device__ __forceinline__ void finish_lists(const EvalParams& p, RowBatch& b, L
   for (int q = 0; q < 8; ++q) { gi[q] = -1; gv[q] = 0.f; }
   if (active) {
     const int D = __ldg(p.ctx.nlists + b.app);
-    float zj[8];
-    uint32_t kj[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      zj[j] = j < D ? lb.z[lane * kListPad + j] : -CUDART_INF_F;
-      kj[j] = j < D ? lb.k[lane * kListPad + j] : kNone;
-    }
     const uint32_t G = b.G;
     const bool y = G != 0;
     const float wi = p.w ? (wtab_smem ? wtab_smem[G] : __ldg(p.w + b.app * 256u + G)) : 1.f;
@@ -696,6 +466,347 @@ __device__ __forceinline__ void finish_lists(const EvalParams& p, RowBatch& b, L
   }
   __syncwarp();
   b.n = 0;
+}
+
+// ------------------------------------------------------------------ fused evaluation kernel
+
+// The CTA's units: round-robin (u = blockIdx + i*grid) or one contiguous block per CTA.
+struct UnitSched {
+  int64_t base, stride, count;
+  __device__ __forceinline__ UnitSched(const EvalParams& p) {
+    if (p.blocked) {
+      const int64_t per = (p.nunits + gridDim.x - 1) / gridDim.x;
+      base = static_cast<int64_t>(blockIdx.x) * per;
+      stride = 1;
+      count = p.nunits - base < per ? p.nunits - base : per;
+      if (count < 0) count = 0;
+    } else {
+      base = blockIdx.x;
+      stride = gridDim.x;
+      count = (p.nunits - blockIdx.x + gridDim.x - 1) / gridDim.x;
+    }
+  }
+  __device__ __forceinline__ int64_t unit(int64_t i) const { return base + i * stride; }
+};
+
+// EPL > 0: whole rows per stage, mapped labels held in registers (|𝕎| <= 32*EPL).
+// EPL == 0: generic path — entries read from a shared/global list, rows may be split
+// into column chunks across stages (large C).
+// PAT = 1: the per-list patterns (application-choice order, Multi-Select) on the same
+// ring — EPL = list-major slots per app, one warp arg max per slot (scan_slots), list
+// maxima assembled in the batch epilogue (finish_slots).
+template <int EPL, bool BF16, int PAT>
+__global__ void __launch_bounds__(kThreads, 1) eval_kernel(const EvalParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.bar_off);
+  uint64_t* empty = full + p.stages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  // ---- prologue: barriers, context entries and weights into shared memory
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < p.stages; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, kConsumerWarps / p.ng);
+    }
+    fence_mbar_init();
+  }
+  uint32_t* ent_smem = reinterpret_cast<uint32_t*>(smem + p.ent_smem_off);
+  if (EPL == 0 && p.ent_mode == 0) {
+    const int n = p.ctx.ent_off[1];
+    for (int e = threadIdx.x; e < n; e += blockDim.x) ent_smem[e] = __ldg(p.ctx.ent + e);
+  }
+  float* wtab = p.wtab_off >= 0 ? reinterpret_cast<float*>(smem + p.wtab_off) : nullptr;
+  if (wtab)
+    for (int m = threadIdx.x; m < 256; m += blockDim.x) wtab[m] = __ldg(p.w + m);
+  __syncthreads();
+
+  if (warp == 0) {
+    // ================= TMA producer (one lane) =================
+    if (lane == 0) {
+      uint64_t pol = evict_first_policy();
+      if (p.no_evict_first) asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+      int s = 0;
+      uint32_t phase = 0;
+      const UnitSched us(p);
+      for (int64_t i = 0; i < us.count; ++i) {
+        const int64_t u = us.unit(i);
+        const int64_t r0 = u * p.R;
+        const int nr = static_cast<int>((p.rows - r0 < p.R ? p.rows - r0 : (int64_t)p.R));
+        for (int kc = 0; kc < p.nchunks; ++kc) {
+          mbar_wait(empty + s, phase ^ 1u);
+          uint8_t* st = smem + static_cast<size_t>(s) * p.stage_bytes;
+          uint32_t bytes = 0;
+          const uint8_t* src_m = nullptr;
+          const uint8_t* src_a = nullptr;
+          uint32_t nb_m = 0, nb_a = 0;
+          if (kc == 0) {
+            if (p.gt_mask) {
+              const uintptr_t lo = reinterpret_cast<uintptr_t>(p.gt_mask + r0) & ~uintptr_t(15);
+              const uintptr_t hi = (reinterpret_cast<uintptr_t>(p.gt_mask + r0 + nr) + 15) & ~uintptr_t(15);
+              src_m = reinterpret_cast<const uint8_t*>(lo);
+              nb_m = static_cast<uint32_t>(hi - lo);
+            }
+            if (p.app) {
+              const uintptr_t lo = reinterpret_cast<uintptr_t>(p.app + r0) & ~uintptr_t(15);
+              const uintptr_t hi = (reinterpret_cast<uintptr_t>(p.app + r0 + nr) + 15) & ~uintptr_t(15);
+              src_a = reinterpret_cast<const uint8_t*>(lo);
+              nb_a = static_cast<uint32_t>(hi - lo);
+            }
+          }
+          if (p.nchunks == 1) {
+            bytes = static_cast<uint32_t>(nr * p.ld_bytes);
+          } else {
+            const int rem = p.copy_row_bytes - kc * p.chunk_bytes;
+            const uint32_t cb = static_cast<uint32_t>(rem < p.chunk_bytes ? rem : p.chunk_bytes);
+            bytes = cb * nr;
+          }
+          mbar_arrive_expect_tx(full + s, bytes + nb_m + nb_a);
+          if (p.nchunks == 1 && !p.split_copy) {
+            bulk_g2s(st, p.logits + r0 * p.ld_bytes, bytes, full + s, pol);
+          } else if (p.nchunks == 1) {
+            const uint32_t rb = static_cast<uint32_t>(p.ld_bytes);
+            for (int j = 0; j < nr; ++j) bulk_g2s(st + static_cast<size_t>(j) * rb, p.logits + (r0 + j) * p.ld_bytes, rb, full + s, pol);
+          } else {
+            const uint32_t cb = bytes / nr;
+            for (int j = 0; j < nr; ++j)
+              bulk_g2s(st + static_cast<size_t>(j) * p.chunk_bytes,
+                       p.logits + (r0 + j) * p.ld_bytes + static_cast<int64_t>(kc) * p.chunk_bytes, cb, full + s,
+                       pol);
+          }
+          if (nb_m) bulk_g2s(st + p.mask_off, src_m, nb_m, full + s, pol);
+          if (nb_a) bulk_g2s(st + p.app_off, src_a, nb_a, full + s, pol);
+          if (++s == p.stages) { s = 0; phase ^= 1u; }
+        }
+      }
+    }
+    return;
+  }
+
+  // ================= consumer warps =================
+  const int cw = warp - 1;
+  RowBatch b;
+  b.n = 0; b.zp = b.zm = 0.f; b.kp = b.km = kNone; b.G = 0; b.app = 0; b.row = 0;
+
+  auto row_app_mask = [&](const uint8_t* st, int64_t r0, int64_t row, uint32_t& a, uint32_t& G) {
+    a = 0;
+    if (p.app) {
+      const uintptr_t lo = reinterpret_cast<uintptr_t>(p.app + r0) & ~uintptr_t(15);
+      a = *reinterpret_cast<const uint16_t*>(st + p.app_off + (reinterpret_cast<uintptr_t>(p.app + row) - lo));
+    }
+    G = 0;
+    if (p.gt_mask) {
+      const uintptr_t lo = reinterpret_cast<uintptr_t>(p.gt_mask + r0) & ~uintptr_t(15);
+      G = st[p.mask_off + (reinterpret_cast<uintptr_t>(p.gt_mask + row) - lo)];
+    } else if (p.has_gt) {
+      G = warp_gt_mask(p, row, a, lane);
+    }
+  };
+
+  int s = 0;
+  uint32_t phase = 0;
+  if constexpr (EPL > 0) {
+    // ---- whole rows, lane-resident entries.  Consumer warps form NG groups of WG warps;
+    // CTA-local unit i lives in stage i % S and is consumed by group i % NG only, so a
+    // stage is released as soon as its WG warps are done (no CTA-wide stage barrier).
+    constexpr uint32_t kElt = BF16 ? 2u : 4u;
+    LaneEnt<PAT ? 1 : EPL> le;  // split maxima (PAT 0)
+    SlotEnt<PAT ? EPL : 1> se;  // list-major slots (PAT 1)
+    float sz[PAT ? EPL : 1];    // this lane's batch row: arg max of every slot (PAT 1)
+    uint32_t sk[PAT ? EPL : 1];
+    if constexpr (PAT == 0)
+      lane_ent_load(le, p.ctx.ent + __ldg(p.ctx.ent_off), __ldg(p.ctx.ent_off + 1) - __ldg(p.ctx.ent_off), 0, lane,
+                    kElt);
+    else
+      slot_ent_load(se, p.ctx, 0, lane, kElt);
+    // single app: table of plus-masks per G value (one LDS per row instead of 8 selects)
+    uint32_t* pmtab = p.pmtab_off >= 0 ? reinterpret_cast<uint32_t*>(smem + p.pmtab_off) : nullptr;
+    if (PAT == 0 && pmtab) {
+      for (int g = cw; g < (1 << p.pmtab_bits); g += kConsumerWarps) pmtab[g * 32 + lane] = plus_mask(le, g);
+      asm volatile("bar.sync 1, %0;" ::"r"(kConsumerWarps * 32) : "memory");
+    }
+    const int ng = p.ng, wg = kConsumerWarps / p.ng;
+    const int grp = cw / wg, wi = cw % wg;
+    const uint32_t sbase = smem_addr(smem);
+    // this group's units are the CTA-local indices grp, grp+ng, ...: stage and phase advance by ng
+    int st_idx = grp;
+    uint32_t ph = 0;
+    const UnitSched us(p);
+    int lim = 32 - 2 * (cw % 16);  // first batch size of this warp (staggered), then 32
+    for (int64_t i = grp; i < us.count; i += ng) {
+      const int64_t u = us.unit(i);
+      const int64_t r0 = u * p.R;
+      const int nr = static_cast<int>((p.rows - r0 < p.R ? p.rows - r0 : (int64_t)p.R));
+      mbar_wait(full + st_idx, ph);
+      const uint32_t st_off = static_cast<uint32_t>(st_idx) * p.stage_bytes;
+      // side-band windows start at the 16-B boundary below row r0
+      const uint32_t m_base = st_off + p.mask_off + (p.gt_mask ? (reinterpret_cast<uintptr_t>(p.gt_mask + r0) & 15u) : 0u);
+      const uint32_t a_base = st_off + p.app_off + (p.app ? (reinterpret_cast<uintptr_t>(p.app + r0) & 15u) : 0u);
+      for (int j = wi; j < nr; j += wg) {
+        const int64_t row = r0 + j;
+        const uint32_t a = p.app ? lds_u16(sbase + a_base + 2u * j) : 0u;
+        uint32_t G = 0;
+        if (p.gt_mask) G = lds_u8(sbase + m_base + j);
+        else if (p.has_gt) G = warp_gt_mask(p, row, a, lane);
+        const uint32_t srow = sbase + st_off + static_cast<uint32_t>(j) * static_cast<uint32_t>(p.ld_bytes);
+        float zs[EPL];
+        if constexpr (PAT == 0) {
+          if (static_cast<int32_t>(a) != le.app) {
+            const int32_t e0 = __ldg(p.ctx.ent_off + a);
+            lane_ent_load(le, p.ctx.ent + e0, __ldg(p.ctx.ent_off + a + 1) - e0, static_cast<int32_t>(a), lane, kElt);
+          }
+#pragma unroll
+          for (int t = 0; t < EPL; ++t) zs[t] = lds_z<BF16>(srow + le.off(t, kElt));
+          const uint32_t pm = pmtab ? lds_u32(sbase + p.pmtab_off + (G * 32 + lane) * 4) : plus_mask(le, G);
+          float zp, zm;
+          uint32_t kp, km;
+          scan_vals<EPL>(le, pm, zs, zp, kp, zm, km);
+          if (b.n == lim) {  // several rows per warp in this stage
+            finish_batch(p, b, wtab, lane);
+            lim = 32;
+          }
+          deposit(b, lane, zp, kp, zm, km, G, a, row);
+        } else {
+          if (static_cast<int32_t>(a) != se.app) slot_ent_load(se, p.ctx, static_cast<int32_t>(a), lane, kElt);
+#pragma unroll
+          for (int t = 0; t < EPL; ++t) zs[t] = t < se.ns ? lds_z<BF16>(srow + se.off[t]) : 0.f;
+          if (b.n == lim) {  // the batch's slot maxima live in sz/sk: finish before the next scan
+            finish_slots<EPL>(p, b, sz, sk, wtab, lane);
+            lim = 32;
+          }
+          scan_slots<EPL>(se, zs, sz, sk, b.n, lane);
+          deposit(b, lane, 0.f, kNone, 0.f, kNone, G, a, row);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + st_idx);
+      // the batch epilogue runs after the stage is released, and the warps' batch boundaries
+      // are staggered (lim) so they do not all hold the pipeline in the same stage
+      if (b.n == lim) {
+        if constexpr (PAT == 0) finish_batch(p, b, wtab, lane);
+        else finish_slots<EPL>(p, b, sz, sk, wtab, lane);
+        lim = 32;
+      }
+      st_idx += ng;
+      if (st_idx >= p.stages) { st_idx -= p.stages; ph ^= 1u; }
+    }
+    if (b.n > 0) {
+      if constexpr (PAT == 0) finish_batch(p, b, wtab, lane);
+      else finish_slots<EPL>(p, b, sz, sk, wtab, lane);
+    }
+    return;
+  } else {
+    // ---- generic: entries from a list, rows possibly split into column chunks
+    uint32_t* slot = p.ent_mode == 1 ? ent_smem + static_cast<size_t>(cw) * p.ent_slot : nullptr;
+    int32_t cur_app = -1;
+    const uint32_t* ents = p.ent_mode == 0 ? ent_smem : nullptr;
+    int32_t n_ent = p.ent_mode == 0 ? p.ctx.ent_off[1] : 0;
+    auto select_app = [&](uint32_t a) {
+      if (p.ent_mode == 0 || static_cast<int32_t>(a) == cur_app) return;
+      const int32_t e0 = __ldg(p.ctx.ent_off + a), e1 = __ldg(p.ctx.ent_off + a + 1);
+      n_ent = e1 - e0;
+      if (p.ent_mode == 1) {
+        __syncwarp();
+        for (int e = lane; e < n_ent; e += 32) slot[e] = __ldg(p.ctx.ent + e0 + e);
+        __syncwarp();
+        ents = slot;
+      } else {
+        ents = p.ctx.ent + e0;
+      }
+      cur_app = static_cast<int32_t>(a);
+    };
+    const UnitSched us(p);
+    int lim = 32 - 2 * (cw % 16);  // first batch size of this warp (staggered), then 32
+    for (int64_t i = 0; i < us.count; ++i) {
+      const int64_t u = us.unit(i);
+      const int64_t r0 = u * p.R;
+      const int nr = static_cast<int>((p.rows - r0 < p.R ? p.rows - r0 : (int64_t)p.R));
+      // rows of this warp: one per stage pass when chunked (R == W), else j = cw + W*t
+      const int rows_here = p.nchunks == 1 ? (nr > cw ? (nr - cw + kConsumerWarps - 1) / kConsumerWarps : 0)
+                                           : (cw < nr ? 1 : 0);
+      if (p.nchunks == 1) {
+        mbar_wait(full + s, phase);
+        const uint8_t* st = smem + static_cast<size_t>(s) * p.stage_bytes;
+        for (int j = cw; j < nr; j += kConsumerWarps) {
+          const int64_t row = r0 + j;
+          uint32_t a, G;
+          row_app_mask(st, r0, row, a, G);
+          select_app(a);
+          const uint8_t* rowp = st + static_cast<int64_t>(j) * p.ld_bytes;
+          float zp = -CUDART_INF_F, zm = -CUDART_INF_F;
+          uint32_t kp = kNone, km = kNone;
+          for (int e = lane; e < n_ent; e += 32) {
+            const uint32_t key = ents[e];
+            const float z = load_logit(rowp, key >> 8, BF16);
+            if ((G >> (key & 0xFFu)) & 1u) {
+              if (z > zp) { zp = z; kp = key; }
+            } else {
+              if (z > zm) { zm = z; km = key; }
+            }
+          }
+          warp_argmax(zp, kp);
+          warp_argmax(zm, km);
+          if (b.n == lim) {  // several rows per warp in this stage
+            finish_batch(p, b, wtab, lane);
+            lim = 32;
+          }
+          deposit(b, lane, zp, kp, zm, km, G, a, row);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + s);
+        if (++s == p.stages) { s = 0; phase ^= 1u; }
+        if (b.n == lim) {  // after the release; staggered over the warps (see the EPL path)
+          finish_batch(p, b, wtab, lane);
+          lim = 32;
+        }
+      } else {
+        const bool mine = rows_here > 0;
+        const int64_t row = r0 + cw;
+        uint32_t a = 0, G = 0;
+        float zp = -CUDART_INF_F, zm = -CUDART_INF_F;
+        uint32_t kp = kNone, km = kNone;
+        int pos = 0;
+        for (int kc = 0; kc < p.nchunks; ++kc) {
+          mbar_wait(full + s, phase);
+          const uint8_t* st = smem + static_cast<size_t>(s) * p.stage_bytes;
+          if (mine) {
+            if (kc == 0) {
+              row_app_mask(st, r0, row, a, G);
+              select_app(a);
+            }
+            const uint8_t* rowp = st + static_cast<int64_t>(cw) * p.chunk_bytes;
+            const uint32_t c_lo = static_cast<uint32_t>(kc) * p.chunk_elems;
+            const uint32_t c_hi = c_lo + p.chunk_elems;
+            int stop = n_ent;
+            for (int e = pos + lane; e < n_ent; e += 32) {
+              const uint32_t key = ents[e];
+              const uint32_t col = key >> 8;
+              if (col >= c_hi) { stop = e; break; }
+              const float z = load_logit(rowp, col - c_lo, BF16);
+              if ((G >> (key & 0xFFu)) & 1u) {
+                if (z > zp) { zp = z; kp = key; }
+              } else {
+                if (z > zm) { zm = z; km = key; }
+              }
+            }
+            pos = static_cast<int>(__reduce_min_sync(kFull, static_cast<uint32_t>(stop)));
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(empty + s);
+          if (++s == p.stages) { s = 0; phase ^= 1u; }
+        }
+        if (mine) {
+          warp_argmax(zp, kp);
+          warp_argmax(zm, km);
+          deposit(b, lane, zp, kp, zm, km, G, a, row);
+          if (b.n == lim) {
+            finish_batch(p, b, wtab, lane);
+            lim = 32;
+          }
+        }
+      }
+    }
+  }
+  if (b.n > 0) finish_batch(p, b, wtab, lane);
 }
 
 // ------------------------------------------------------------------ sector-sparse gather kernel
@@ -975,47 +1086,65 @@ __device__ void weights_one_app(const unsigned long long* H, float* w_app) {
 
 }  // namespace
 
-template <int EPL>
+template <int EPL, int PAT = 0>
 static cudaError_t set_limit_t(size_t smem) {
-  cudaError_t e = cudaFuncSetAttribute(eval_kernel<EPL, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e = cudaFuncSetAttribute(eval_kernel<EPL, false, PAT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e) return e;
-  return cudaFuncSetAttribute(eval_kernel<EPL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  return cudaFuncSetAttribute(eval_kernel<EPL, true, PAT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               static_cast<int>(smem));
 }
 
 #define SC_EVAL_EPLS(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(12) X(16) X(24) X(32)
+#define SC_EVAL_EPLS_PAT(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8)  // per-list patterns: slots (PAT = 1)
 
 cudaError_t set_eval_smem_limit(size_t smem) {
   cudaError_t e = set_limit_t<0>(smem);
 #define SC_SET(N) if (!e) e = set_limit_t<N>(smem);
   SC_EVAL_EPLS(SC_SET)
 #undef SC_SET
+#define SC_SET(N) if (!e) e = set_limit_t<N, 1>(smem);
+  SC_EVAL_EPLS_PAT(SC_SET)
+#undef SC_SET
   return e;
 }
 
-int eval_epl_for(int max_ent) {
+int eval_epl_for(int max_ent, int pat) {
   const int need = (max_ent + 31) / 32;
 #define SC_PICK(N) if (need <= N) return N;
-  SC_EVAL_EPLS(SC_PICK)
+  if (pat) {
+    SC_EVAL_EPLS_PAT(SC_PICK)
+  } else {
+    SC_EVAL_EPLS(SC_PICK)
+  }
 #undef SC_PICK
   return -1;
 }
 
 template <bool BF16>
-static void launch_eval_dt(const EvalParams& p, int epl, int grid, size_t smem, cudaStream_t st) {
+static void launch_eval_dt(const EvalParams& p, int epl, int pat, int grid, size_t smem, cudaStream_t st) {
+  if (pat) {
+    switch (epl) {
+#define SC_CASE(N) case N: eval_kernel<N, BF16, 1><<<grid, kThreads, smem, st>>>(p); break;
+      SC_EVAL_EPLS_PAT(SC_CASE)
+#undef SC_CASE
+      default: break;
+    }
+    return;
+  }
   switch (epl) {
-    case 0: eval_kernel<0, BF16><<<grid, kThreads, smem, st>>>(p); break;
-#define SC_CASE(N) case N: eval_kernel<N, BF16><<<grid, kThreads, smem, st>>>(p); break;
+    case 0: eval_kernel<0, BF16, 0><<<grid, kThreads, smem, st>>>(p); break;
+#define SC_CASE(N) case N: eval_kernel<N, BF16, 0><<<grid, kThreads, smem, st>>>(p); break;
     SC_EVAL_EPLS(SC_CASE)
 #undef SC_CASE
     default: break;
   }
 }
 
-cudaError_t launch_eval(const EvalParams& p, int epl, int grid, size_t smem, cudaStream_t st) {
-  if (p.bf16) launch_eval_dt<true>(p, epl, grid, smem, st);
-  else launch_eval_dt<false>(p, epl, grid, smem, st);
+cudaError_t launch_eval(const EvalParams& p, int epl, int pat, int grid, size_t smem, cudaStream_t st) {
+  if (pat && epl <= 0) return cudaErrorInvalidValue;  // the per-list patterns need lane-resident entries
+  if (p.bf16) launch_eval_dt<true>(p, epl, pat, grid, smem, st);
+  else launch_eval_dt<false>(p, epl, pat, grid, smem, st);
   return cudaGetLastError();
 }
 

@@ -1,13 +1,14 @@
 """GPU parity of the other decision patterns against the oracle:
 Multi-Choice application-choice order (Eq. app_choice) and Multi-Select (Eq. multi-select).
-Same bar as the hot path: decisions, G, counters and gradient indices bit-exact; loss and
+Both kernels (the TMA ring with lane-resident entries, the sector-sparse gather) meet the
+same bar as the hot path: decisions, G, counters and gradient indices bit-exact; loss and
 gradient values within 1e-5 relative; overlapping lists exercise the two membership rules
 (first list for the choice orders, every list for Multi-Select)."""
 import numpy as np
 import pytest
 
 from conftest import gpu_available
-from test_parity_gpu import compare, run_gpu, run_oracle, tie_heavy_batch, to_dev
+from test_parity_gpu import compare, kernel, run_gpu, run_oracle, tie_heavy_batch, to_dev  # noqa: F401 (fixture)
 
 pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device")]
 
@@ -24,7 +25,7 @@ APP_CHOICE, MULTI_SELECT = 1, 2
     (4, "f32", (1 << 18) - 700, 1500, "mask", 0),
     (4, "bf16", 10, 999, "mask", 1),
 ])
-def test_patterns_configs(order, cfg, dtype, row0, rows, mode, layout):
+def test_patterns_configs(order, cfg, dtype, row0, rows, mode, layout, kernel):
     import synth
     spec = synth.config_context(cfg)
     wl = synth.Workload(spec, seed=cfg, dtype=dtype, layout=layout)
@@ -37,7 +38,7 @@ def test_patterns_configs(order, cfg, dtype, row0, rows, mode, layout):
 
 @pytest.mark.parametrize("order", [APP_CHOICE, MULTI_SELECT])
 @pytest.mark.parametrize("C,ld,rows", [(1, 4, 100), (4, 4, 333), (37, 40, 1000), (300, 300, 777), (4097, 4100, 97)])
-def test_patterns_tie_heavy_overlapping(order, C, ld, rows):
+def test_patterns_tie_heavy_overlapping(order, C, ld, rows, kernel):
     import synth
     rng = np.random.default_rng(C * 11 + rows + order)
     for tau in (0.0, -1.0):
@@ -51,7 +52,7 @@ def test_patterns_tie_heavy_overlapping(order, C, ld, rows):
         compare(g, o, w, rows)
 
 
-def test_true_false_patterns_agree_on_gpu():
+def test_true_false_patterns_agree_on_gpu(kernel):
     """One list: the three patterns give the same decisions (list 0 / its mask) and losses."""
     import torch
     import synth
