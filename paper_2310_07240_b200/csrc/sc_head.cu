@@ -58,6 +58,7 @@ struct HeadParams {
   int32_t chunk;            // columns per MMA (n_cols or n_cols / 2)
   int32_t n_chunks;
   int32_t acc_bufs;         // 2: double-buffered accumulators
+  int32_t tiles;            // row tiles per unit sharing every W stage (1, or 2 for lone CTAs)
   int32_t kbs;              // k-blocks per x stage (one 3-D TMA box of kbs x [128 x 64])
   int32_t n_xb;             // x stages per unit = ceil(n_kb / kbs)
   int32_t x_stages, w_stages;
@@ -260,7 +261,8 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
   uint64_t* tempty = tfull + 2;               // [2]         (PAIR: the leader's counts both CTAs)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
-  constexpr int kUnit = PAIR ? 2 * kBM : kBM;
+  // rows per unit: a CTA pair's two tiles, or p.tiles tiles of one CTA that share each W stage
+  const int kUnit = PAIR ? 2 * kBM : p.tiles * kBM;
 
   for (int i = tid; i < p.n_cols; i += blockDim.x) {
     s_keys[i] = __ldg(p.keys + i);
@@ -325,8 +327,11 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
           const uint32_t fb = xfull_l + 8u * s;
           if (rank == 0) mbar_arrive_expect_tx(xfull + s, tx);
           else mbar_arrive_expect_tx_cl(fb, tx);
-          if (p.x3d) tma_3d<PAIR>(stg, &map_x, 0, row0, xb * p.kbs, fb, pol_x);
-          else tma_2d<PAIR>(stg, &map_x, xb * kBK, row0, fb, pol_x);
+          for (int t = 0; t < (PAIR ? 1 : p.tiles); ++t) {  // tile t: kbs k-blocks at t * kbs * 16 KB
+            uint8_t* dst = stg + static_cast<size_t>(t) * p.kbs * (kBM * kBK * 2);
+            if (p.x3d) tma_3d<PAIR>(dst, &map_x, 0, row0 + t * kBM, xb * p.kbs, fb, pol_x);
+            else tma_2d<PAIR>(dst, &map_x, xb * kBK, row0 + t * kBM, fb, pol_x);
+          }
           if (++s == p.x_stages) {
             s = 0;
             ph ^= 1u;
@@ -371,6 +376,8 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
       const uint64_t w_step = static_cast<uint32_t>(p.w_stage_bytes) >> 4;
       const uint64_t c_step = static_cast<uint32_t>((PAIR ? p.chunk / 2 : p.chunk) * kBK * 2) >> 4;
       const bool two = p.n_chunks == 2;
+      const bool tile2 = !PAIR && p.tiles == 2;                               // n_chunks == 1 then
+      const uint64_t t_step = static_cast<uint32_t>(p.kbs * a_bytes) >> 4;  // tile 1 in an x stage
       const bool no_mma = (p.probe & 2) != 0;
       int xs = 0, ws = 0, b = 0;
       uint32_t xph = 0, wph = 0, tph[2] = {0, 0};
@@ -396,6 +403,8 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
                 const uint32_t accum = (first && k == 0) ? 0u : 1u;
                 umma_bf16<PAIR>(acc, ad + 2 * k, bd + 2 * k, idesc, accum);
                 if (two) umma_bf16<PAIR>(acc + p.chunk, ad + 2 * k, bd + c_step + 2 * k, idesc, accum);
+                if (tile2)  // the second row tile: same W stage, its own accumulator
+                  umma_bf16<PAIR>(acc + p.n_cols, ad + t_step + 2 * k, bd + 2 * k, idesc, accum);
               }
             }
             umma_commit<PAIR>(wempty + ws);  // W stage free (in both CTAs) once read
@@ -425,87 +434,113 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
     uint32_t tph[2] = {0, 0};
     RowBatch rb;
     rb.n = 0;
+    const int ntile = PAIR ? 1 : p.tiles;
     for (int64_t st = 0; st < n_steps; ++st) {
-      const int64_t first = (unit0 + st * n_grid_units) * kUnit + rank * kBM + 32 * q;
-      const int64_t row = first + lane;
-      const bool active = row < p.rows;
-      // G_i before waiting on the accumulator (overlaps the MMA)
-      uint32_t G = 0;
-      if (active) {
-        if (ep.gt_mask) {
-          G = __ldg(ep.gt_mask + row);
-        } else if (ep.gt_off) {
-          const int64_t g0 = __ldg(ep.gt_off + row), g1 = __ldg(ep.gt_off + row + 1);
-          for (int64_t i = g0; i < g1; ++i) G |= label_lists(__ldg(cat + __ldg(ep.gt_lab + i)), kApiOutput);
+      const int64_t first0 = (unit0 + st * n_grid_units) * kUnit + rank * kBM + 32 * q;
+      // G_i of each tile's row before waiting on the accumulator (overlaps the MMA)
+      uint32_t Gt[2] = {0u, 0u};
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const int64_t row = first0 + t * kBM + lane;
+        if (t < ntile && row < p.rows) {
+          uint32_t G = 0;
+          if (ep.gt_mask) {
+            G = __ldg(ep.gt_mask + row);
+          } else if (ep.gt_off) {
+            const int64_t g0 = __ldg(ep.gt_off + row), g1 = __ldg(ep.gt_off + row + 1);
+            for (int64_t i = g0; i < g1; ++i) G |= label_lists(__ldg(cat + __ldg(ep.gt_lab + i)), kApiOutput);
+          }
+          Gt[t] = G;
         }
       }
       mbar_wait(tfull + b, tph[b]);
       tph[b] ^= 1u;
       tc_fence_after();
-      const uint32_t acc = tmem_base + lane_base + static_cast<uint32_t>(b * p.n_cols);
-      // per-list arg max over the list's 16-column groups; the next group's load is in
-      // flight while the current one is reduced
-      float lz[kMaxLists];
-      int lc[kMaxLists];
+      float zpt[2], zmt[2];
+      uint32_t kpt[2], kmt[2];
 #pragma unroll
-      for (int j = 0; j < kMaxLists; ++j) {
-        lz[j] = -CUDART_INF_F;
-        lc[j] = -1;
-      }
-      uint32_t v[16], vn[16];
-      int j = 0, g = 0;  // list, group within the list
-      while (j < D && p.list_nch[j] == 0) ++j;
-      if (p.probe & 1) j = D;
-      if (j < D) {
-        tmem_ld16(acc + p.list_col0[j], v);
-        tmem_wait_ld(v);
-      }
-      float run_z = -CUDART_INF_F;
-      int run_c = -1;
-      while (j < D) {
-        const int col = p.list_col0[j] + 16 * g;
-        // next group (warp-uniform)
-        int jn = j, gn = g + 1;
-        if (gn == p.list_nch[jn]) {
-          gn = 0;
-          ++jn;
-          while (jn < D && p.list_nch[jn] == 0) ++jn;
-        }
-        if (jn < D) tmem_ld16(acc + p.list_col0[jn] + 16 * gn, vn);
-        float z[16];
-        const float4* b4 = reinterpret_cast<const float4*>(s_bias + col);
+      for (int t = 0; t < 2; ++t) {
+        if (t >= ntile) break;
+        const uint32_t acc = tmem_base + lane_base + static_cast<uint32_t>((b + t) * p.n_cols);
+        // per-list arg max over the list's 16-column groups; the next group's load is in
+        // flight while the current one is reduced
+        float lz[kMaxLists];
+        int lc[kMaxLists];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float4 bb = b4[i];
-          z[4 * i + 0] = __uint_as_float(v[4 * i + 0]) + bb.x;
-          z[4 * i + 1] = __uint_as_float(v[4 * i + 1]) + bb.y;
-          z[4 * i + 2] = __uint_as_float(v[4 * i + 2]) + bb.z;
-          z[4 * i + 3] = __uint_as_float(v[4 * i + 3]) + bb.w;
+        for (int j = 0; j < kMaxLists; ++j) {
+          lz[j] = -CUDART_INF_F;
+          lc[j] = -1;
         }
-        float zc;
-        int ic;
-        argmax16(z, zc, ic);
-        if (zc > run_z) {  // strict: an earlier group (smaller labels) keeps ties
-          run_z = zc;
-          run_c = col + ic;
-        }
-        if (jn != j) {  // list j done
-#pragma unroll
-          for (int jj = 0; jj < kMaxLists; ++jj)
-            if (jj == j) {
-              lz[jj] = run_z;
-              lc[jj] = run_c;
-            }
-          run_z = -CUDART_INF_F;
-          run_c = -1;
-        }
-        j = jn;
-        g = gn;
+        uint32_t v[16], vn[16];
+        int j = 0, g = 0;  // list, group within the list
+        while (j < D && p.list_nch[j] == 0) ++j;
+        if (p.probe & 1) j = D;
         if (j < D) {
-          tmem_wait_ld(vn);
-#pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] = vn[i];
+          tmem_ld16(acc + p.list_col0[j], v);
+          tmem_wait_ld(v);
         }
+        float run_z = -CUDART_INF_F;
+        int run_c = -1;
+        while (j < D) {
+          const int col = p.list_col0[j] + 16 * g;
+          // next group (warp-uniform)
+          int jn = j, gn = g + 1;
+          if (gn == p.list_nch[jn]) {
+            gn = 0;
+            ++jn;
+            while (jn < D && p.list_nch[jn] == 0) ++jn;
+          }
+          if (jn < D) tmem_ld16(acc + p.list_col0[jn] + 16 * gn, vn);
+          float z[16];
+          const float4* b4 = reinterpret_cast<const float4*>(s_bias + col);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float4 bb = b4[i];
+            z[4 * i + 0] = __uint_as_float(v[4 * i + 0]) + bb.x;
+            z[4 * i + 1] = __uint_as_float(v[4 * i + 1]) + bb.y;
+            z[4 * i + 2] = __uint_as_float(v[4 * i + 2]) + bb.z;
+            z[4 * i + 3] = __uint_as_float(v[4 * i + 3]) + bb.w;
+          }
+          float zc;
+          int ic;
+          argmax16(z, zc, ic);
+          if (zc > run_z) {  // strict: an earlier group (smaller labels) keeps ties
+            run_z = zc;
+            run_c = col + ic;
+          }
+          if (jn != j) {  // list j done
+#pragma unroll
+            for (int jj = 0; jj < kMaxLists; ++jj)
+              if (jj == j) {
+                lz[jj] = run_z;
+                lc[jj] = run_c;
+              }
+            run_z = -CUDART_INF_F;
+            run_c = -1;
+          }
+          j = jn;
+          g = gn;
+          if (j < D) {
+            tmem_wait_ld(vn);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] = vn[i];
+          }
+        }
+        // split maxima over the list winners: P⁺ over lists in G_i, P⁻ over the rest (A8)
+        float zp = -CUDART_INF_F, zm = -CUDART_INF_F;
+        uint32_t kp = kNone, km = kNone;
+#pragma unroll
+        for (int jj = 0; jj < kMaxLists; ++jj) {
+          if (lc[jj] >= 0) {
+            const uint32_t key = s_keys[lc[jj]];
+            if ((Gt[t] >> jj) & 1u) {
+              if (beats(lz[jj], key, zp, kp)) { zp = lz[jj]; kp = key; }
+            } else {
+              if (beats(lz[jj], key, zm, km)) { zm = lz[jj]; km = key; }
+            }
+          }
+        }
+        zpt[t] = zp; kpt[t] = kp; zmt[t] = zm; kmt[t] = km;
       }
       tc_fence_before();
       __syncwarp();
@@ -514,25 +549,17 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
         else mbar_arrive_cl(tempty_l + 8u * b);
       }
       if (p.acc_bufs == 2) b ^= 1;
-      // split maxima over the list winners: P⁺ over lists in G_i, P⁻ over the rest (A8)
-      float zp = -CUDART_INF_F, zm = -CUDART_INF_F;
-      uint32_t kp = kNone, km = kNone;
 #pragma unroll
-      for (int jj = 0; jj < kMaxLists; ++jj) {
-        if (lc[jj] >= 0) {
-          const uint32_t key = s_keys[lc[jj]];
-          if ((G >> jj) & 1u) {
-            if (beats(lz[jj], key, zp, kp)) { zp = lz[jj]; kp = key; }
-          } else {
-            if (beats(lz[jj], key, zm, km)) { zm = lz[jj]; km = key; }
-          }
+      for (int t = 0; t < 2; ++t) {
+        if (t >= ntile) break;
+        const int64_t first = first0 + t * kBM;
+        const int64_t nrow = p.rows - first;
+        if (nrow > 0) {
+          rb.zp = zpt[t]; rb.kp = kpt[t]; rb.zm = zmt[t]; rb.km = kmt[t]; rb.G = Gt[t]; rb.app = 0;
+          rb.row = first + lane;
+          rb.n = nrow < 32 ? static_cast<int>(nrow) : 32;
+          finish_batch(ep, rb, nullptr, lane);
         }
-      }
-      const int64_t nrow = p.rows - first;
-      if (nrow > 0) {
-        rb.zp = zp; rb.kp = kp; rb.zm = zm; rb.km = km; rb.G = G; rb.app = 0; rb.row = row;
-        rb.n = nrow < 32 ? static_cast<int>(nrow) : 32;
-        finish_batch(ep, rb, nullptr, lane);
       }
     }
   }
@@ -852,6 +879,10 @@ sc_status sc_head_loss_fwd_bwd(sc_context ctx, sc_head head, const sc_head_batch
   p.chunk = head->chunk;
   p.n_chunks = head->n_chunks;
   p.acc_bufs = 2 * head->n_cols <= sc::kMaxCols ? 2 : 1;
+  // lone CTAs: two 128-row tiles per unit share every W stage (W_𝕎, re-read from L2 for each
+  // unit, moves half the bytes per row) when both accumulators fit TMEM; then single-buffered
+  const char* t2env = std::getenv("SC_HEAD_T2");
+  const bool t2_ok = head->n_chunks == 1 && 2 * head->n_cols <= sc::kMaxCols && !(t2env && std::atoi(t2env) == 0);
   p.n_lists = head->n_lists;
   for (int j = 0; j < sc::kMaxLists; ++j) {
     p.list_col0[j] = head->list_col0[j];
@@ -873,6 +904,7 @@ sc_status sc_head_loss_fwd_bwd(sc_context ctx, sc_head head, const sc_head_batch
   for (int attempt = 0; attempt < 2; ++attempt) {
     const bool want_pair = attempt == 0;
     p.w_stage_bytes = (want_pair ? head->n_cols / 2 : head->n_cols) * sc::kBK * 2;
+    p.tiles = (!want_pair && t2_ok) ? 2 : 1;
     // x: 3-D boxes of kbs k-blocks (rows read kbs*128 B at a time) when d % 64 == 0; as many
     // x bytes in flight as fit next to >= 3 W stages (>= 2 for wide heads)
     x3d = head->d % sc::kBK == 0 && !(std::getenv("SC_HEAD_X2D"));
@@ -880,15 +912,19 @@ sc_status sc_head_loss_fwd_bwd(sc_context ctx, sc_head head, const sc_head_batch
     if (const char* e = std::getenv("SC_HEAD_KBS")) kbs_min = kbs_max = std::max(1, std::atoi(e));
     int64_t best_score = -1;
     int best_kbs = 1, best_xs = 0, best_ws = 0;
+    for (int tl = p.tiles; tl >= 1 && best_xs < 2; --tl) {  // two tiles per unit, else one
+    p.tiles = tl;
+    const int xa_bytes = tl * a_bytes;  // x bytes per k-block of a unit
     for (int kbs = kbs_min; kbs <= kbs_max; kbs *= 2) {
       if (kbs > p.n_kb && kbs > 1) break;
       for (int xs = 2; xs <= 16; ++xs) {
-        const int64_t xbytes = static_cast<int64_t>(xs) * kbs * a_bytes;
+        const int64_t xbytes = static_cast<int64_t>(xs) * kbs * xa_bytes;
         const int64_t rest = budget - xbytes;
         if (rest < 0) break;
         const int ws = static_cast<int>(std::min<int64_t>(16, rest / p.w_stage_bytes));
-        // measured (cfg2, d = 2048): 5-6 W stages next to ~96 KB of x beat deeper x rings
-        int ws_min = p.w_stage_bytes > 32 * 1024 ? 2 : 5;
+        // measured (cfg2, d = 2048): 5-6 W stages next to ~96 KB of x beat deeper x rings for
+        // one tile per unit; two tiles consume W half as fast per x byte
+        int ws_min = p.w_stage_bytes > 32 * 1024 ? 2 : (tl == 2 ? 3 : 5);
         if (const char* e = std::getenv("SC_HEAD_WSTAGES")) ws_min = std::max(ws_min, std::atoi(e));
         if (ws < ws_min) break;
         // prefer more x bytes in flight, then longer contiguous runs, then more W stages
@@ -901,13 +937,14 @@ sc_status sc_head_loss_fwd_bwd(sc_context ctx, sc_head head, const sc_head_batch
         }
       }
     }
+    }
     if (best_xs < 2) return sc::set_error(SC_ERR_UNSUPPORTED, "sc_head_loss_fwd_bwd: head too wide for the ring");
     if (best_kbs == 1) x3d = false;
     p.kbs = best_kbs;
     p.n_xb = (p.n_kb + p.kbs - 1) / p.kbs;
     p.x_stages = best_xs;
     p.w_stages = best_ws;
-    p.x_stage_bytes = p.kbs * a_bytes;
+    p.x_stage_bytes = p.kbs * p.tiles * a_bytes;
     p.w_ring_off = p.x_stages * p.x_stage_bytes;
     p.tab_off = p.w_ring_off + p.w_stages * p.w_stage_bytes;
     p.bar_off = (p.tab_off + tab_bytes + 7) / 8 * 8;
@@ -927,7 +964,8 @@ sc_status sc_head_loss_fwd_bwd(sc_context ctx, sc_head head, const sc_head_batch
     pair = want_pair;
     break;
   }
-  p.n_units = pair ? (b.rows + 2 * sc::kBM - 1) / (2 * sc::kBM) : n_tiles;
+  if (!pair && p.tiles == 2) p.acc_bufs = 1;  // both accumulators of a unit in TMEM at once
+  p.n_units = pair ? (b.rows + 2 * sc::kBM - 1) / (2 * sc::kBM) : (n_tiles + p.tiles - 1) / p.tiles;
   CUtensorMap map_x;
   p.x3d = x3d ? 1 : 0;
   if (x3d ? !make_map3(&map_x, b.x, head->d, b.rows, b.ldx, p.kbs)
