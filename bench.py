@@ -164,7 +164,7 @@ def load_traffic(cfg, dtype, kernel, rows):
     path = os.path.join(ROOT, "profiles", f"ncu_eval_cfg{cfg}_{dtype}_{kernel}.json")
     try:
         d = json.load(open(path))
-        return d["dram_bytes_per_row"] * rows, path
+        return d["dram_bytes_per_row"] * rows, os.path.relpath(path, ROOT)
     except Exception:
         return None, None
 

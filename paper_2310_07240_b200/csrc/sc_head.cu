@@ -21,6 +21,9 @@
 //               a time (the next load in flight while the current one is reduced), adds the
 //               bias, per-list arg max, split maxima by G_i, then finish_batch (decision,
 //               counters, loss, gradient).
+//   warps 7-10  the same for the unit's second row tile: lone CTAs run two 128-row tiles per
+//               unit that share every W stage (two accumulators in TMEM, single-buffered),
+//               so W_𝕎 — re-read from L2 for every unit — moves half the bytes per row.
 // PAIR (opt-in, SC_HEAD_CLUSTER=2): CTA pairs run M = 256 MMAs with cta_group::2, each CTA
 // streaming its own 128 rows of x and half of W_𝕎; the leader's barriers count both CTAs'
 // bytes and a multicast tcgen05.commit frees the stages of both.
@@ -43,7 +46,7 @@ namespace {
 
 constexpr int kBM = 128;           // rows per tile (UMMA M)
 constexpr int kBK = 64;            // bf16 elements per k-block = one 128-B swizzle row
-constexpr int kHeadThreads = 224;  // 7 warps
+constexpr int kHeadThreads = 352;  // 11 warps: x / MMA / 4 epilogue / W / 4 epilogue (second tile)
 constexpr int kMaxCols = 512;      // TMEM columns
 constexpr int kMaxLists = 8;
 
@@ -279,7 +282,7 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(tfull + b, 1);
-      mbar_init(tempty + b, PAIR ? 8 : 4);  // one arrive per epilogue warp (of both CTAs)
+      mbar_init(tempty + b, PAIR ? 8 : 4 * p.tiles);  // one arrive per working epilogue warp (of both CTAs)
     }
     fence_mbar_init();
   }
@@ -423,7 +426,7 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
         if (p.acc_bufs == 2) b ^= 1;
       }
     }
-  } else if (warp <= 5) {
+  } else if (warp <= 5 || (warp >= 7 && warp <= 10 && !PAIR && p.tiles == 2)) {
     // ---------------- epilogue: one row per thread
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const uint32_t lane_base = static_cast<uint32_t>(32 * q) << 16;
@@ -435,6 +438,9 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
     RowBatch rb;
     rb.n = 0;
     const int ntile = PAIR ? 1 : p.tiles;
+    // two tiles per unit: warps 2-5 drain tile 0, warps 7-10 tile 1 (lane quarters 3,0,1,2)
+    const int t_lo = ntile == 2 ? (warp >= 7 ? 1 : 0) : 0;
+    const int t_hi = ntile == 2 ? t_lo + 1 : 1;
     for (int64_t st = 0; st < n_steps; ++st) {
       const int64_t first0 = (unit0 + st * n_grid_units) * kUnit + rank * kBM + 32 * q;
       // G_i of each tile's row before waiting on the accumulator (overlaps the MMA)
@@ -442,7 +448,7 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
 #pragma unroll
       for (int t = 0; t < 2; ++t) {
         const int64_t row = first0 + t * kBM + lane;
-        if (t < ntile && row < p.rows) {
+        if (t >= t_lo && t < t_hi && row < p.rows) {
           uint32_t G = 0;
           if (ep.gt_mask) {
             G = __ldg(ep.gt_mask + row);
@@ -460,7 +466,7 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
       uint32_t kpt[2], kmt[2];
 #pragma unroll
       for (int t = 0; t < 2; ++t) {
-        if (t >= ntile) break;
+        if (t < t_lo || t >= t_hi) continue;
         const uint32_t acc = tmem_base + lane_base + static_cast<uint32_t>((b + t) * p.n_cols);
         // per-list arg max over the list's 16-column groups; the next group's load is in
         // flight while the current one is reduced
@@ -551,7 +557,7 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
       if (p.acc_bufs == 2) b ^= 1;
 #pragma unroll
       for (int t = 0; t < 2; ++t) {
-        if (t >= ntile) break;
+        if (t < t_lo || t >= t_hi) continue;
         const int64_t first = first0 + t * kBM;
         const int64_t nrow = p.rows - first;
         if (nrow > 0) {
