@@ -533,6 +533,16 @@ static sc_status run_hist(sc_context ctx, const sc_batch* b, uint64_t* hist_gt, 
   p.done_counter = ctx->d_done;
   const size_t hbytes = static_cast<size_t>(ctx->n_apps) * 256 * 8;
   p.smem_hist = hbytes <= 32 * 1024;
+  // single application: one row per thread, the category table in shared memory
+  const char* hk = std::getenv("SC_HIST");
+  const bool rows_kernel = ctx->n_apps == 1 && ctx->C <= 128 * 1024 && !(hk && std::string(hk) == "warp");
+  if (rows_kernel) {
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((b->rows + 255) / 256, static_cast<int64_t>(di.sms) * 8));
+    if (cudaError_t e = sc::launch_hist_rows(p, static_cast<int>(blocks), static_cast<cudaStream_t>(stream)))
+      return cuda_fail(e, "hist kernel launch");
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return SC_OK;
+  }
   const int64_t per_block = 8 * 32 * 2;  // 8 warps x kHB blocks of 32 rows
   // persistent: one wave (3 CTAs/SM at <= 85 registers), warps loop with a prefetch pipeline
   const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((b->rows + per_block - 1) / per_block,

@@ -129,6 +129,7 @@ cudaError_t launch_eval(const EvalParams& p, int epl, int pat, int grid, size_t 
 // pat 0: split maxima (API-output order); pat 1: per-list maxima (application-choice, Multi-Select).
 cudaError_t launch_gather(const EvalParams& p, int epl, int pat, int sms, cudaStream_t st);
 cudaError_t launch_hist(const HistParams& p, int grid, size_t smem, cudaStream_t st);
+cudaError_t launch_hist_rows(const HistParams& p, int grid, cudaStream_t st);  // single app, C <= 128K
 cudaError_t launch_weights(const unsigned long long* hist, float* w, int n_apps, cudaStream_t st);
 cudaError_t set_eval_smem_limit(size_t smem);
 // Smallest compiled lane-resident entry capacity for max_ent mapped labels (-1: none fits).

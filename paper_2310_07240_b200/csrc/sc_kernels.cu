@@ -1044,6 +1044,52 @@ __global__ void __launch_bounds__(256, 3) hist_kernel(const HistParams p) {
   }
 }
 
+// One row per thread for single-application contexts (the one-GPU step's pre-pass): the
+// category table sits in shared memory, so a row is two coalesced offset loads, its labels
+// (adjacent rows' labels are adjacent in the CSR) and shared-memory lookups; occupancy, not a
+// software pipeline, hides the dependent loads.  Same outputs as hist_kernel.
+__global__ void __launch_bounds__(256) hist_rows_kernel(const HistParams p) {
+  extern __shared__ __align__(16) uint8_t hsm[];
+  unsigned long long* sh_hist = reinterpret_cast<unsigned long long*>(hsm);  // [256]
+  uint8_t* cat_s = hsm + 256 * 8;                                          // [C]
+  __shared__ bool last_block;
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) sh_hist[i] = 0;
+  for (int c = threadIdx.x; c < p.ctx.C; c += blockDim.x) cat_s[c] = __ldg(p.ctx.cat + c);
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t r0 = static_cast<int64_t>(blockIdx.x) * blockDim.x; r0 < p.rows; r0 += stride) {
+    const int64_t row = r0 + threadIdx.x;
+    const bool act = row < p.rows;
+    uint32_t G = 0;
+    if (act) {
+      const int64_t lo = __ldg(p.gt_off + row), hi = __ldg(p.gt_off + row + 1);
+      for (int64_t t = lo; t < hi; ++t) G |= label_lists(cat_s[__ldg(p.gt_lab + t)], p.ctx.order);
+      if (p.gt_mask_out) p.gt_mask_out[row] = static_cast<uint8_t>(G);
+    }
+    const unsigned am = __ballot_sync(kFull, act);
+    if (p.hist_gt && act) {
+      const unsigned peers = __match_any_sync(am, G);
+      if (lane == __ffs(peers) - 1) atomicAdd(sh_hist + G, static_cast<unsigned long long>(__popc(peers)));
+    }
+  }
+  __syncthreads();
+  if (p.hist_gt)
+    for (int i = threadIdx.x; i < 256; i += blockDim.x)
+      if (sh_hist[i]) atomicAdd(p.hist_gt + i, sh_hist[i]);
+  if (p.w_out) {  // last CTA done: weights from the finished histogram
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last_block = atomicAdd(p.done_counter, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (last_block) {
+      __threadfence();
+      weights_from_hist_block(p.hist_gt, p.w_out, 1);
+      if (threadIdx.x == 0) *p.done_counter = 0;  // ready for the next call
+    }
+  }
+}
+
 // ------------------------------------------------------------------ weights (a7)
 
 // One CTA per app.  F = subset-sum (zeta) transform of H over 8 bits, so
@@ -1183,6 +1229,20 @@ cudaError_t launch_gather(const EvalParams& p, int epl, int pat, int sms, cudaSt
 
 cudaError_t launch_hist(const HistParams& p, int grid, size_t smem, cudaStream_t st) {
   hist_kernel<<<grid, 256, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_hist_rows(const HistParams& p, int grid, cudaStream_t st) {
+  const size_t smem = 256 * 8 + static_cast<size_t>(p.ctx.C);
+  if (smem > 48 * 1024) {
+    static bool attr = false;
+    if (!attr) {
+      if (cudaError_t e = cudaFuncSetAttribute(hist_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024))
+        return e;
+      attr = true;
+    }
+  }
+  hist_rows_kernel<<<grid, 256, smem, st>>>(p);
   return cudaGetLastError();
 }
 
