@@ -68,3 +68,37 @@ def test_true_false_patterns_agree_on_gpu(kernel):
     for o in (APP_CHOICE, MULTI_SELECT):
         np.testing.assert_allclose(res[o]["loss_row"], res[0]["loss_row"], rtol=1e-6, atol=0)
         np.testing.assert_array_equal(res[o]["n_incorrect"], res[0]["n_incorrect"])
+
+
+@pytest.mark.parametrize("order", [APP_CHOICE, MULTI_SELECT])
+@pytest.mark.parametrize("sizes,shared", [
+    ((32, 32, 32, 32, 32, 32, 32, 32), 0),   # exactly 8 list-major slots: the TMA ring's limit
+    ((33, 1, 64, 31, 30), 0),                # 2 + 1 + 2 + 1 + 1 = 7 slots, ragged padding
+    ((40, 40, 40, 40, 40), 0),               # 10 slots: falls back to the gather kernel
+    ((30, 30, 30), 20),                      # overlapping lists: Multi-Select labels in several slots
+])
+def test_patterns_slot_layouts(order, sizes, shared, monkeypatch):
+    """List-major slots (DevContext::lent): lists padded to 32 labels per slot, <= 8 slots on
+    the TMA ring, more on the gather kernel; overlaps follow each pattern's membership rule."""
+    import paper_2310_07240_b200 as sc
+    import synth
+    monkeypatch.setenv("SC_KERNEL", "tma")
+    rng = np.random.default_rng(sum(sizes) * 7 + shared + order)
+    C, rows = 700, 1500
+    perm = rng.permutation(C)
+    lists, pos = [], 0
+    common = sorted(perm[:shared].tolist())
+    pos = shared
+    for n in sizes:
+        own = perm[pos:pos + n].tolist()
+        pos += n
+        lists.append(sorted(set(own) | set(common)))
+    spec = synth.ContextSpec(C, [lists], tau=0.0, k=10.0)
+    b = tie_heavy_batch(rng, C, rows, C, lists, 0.0)
+    g = run_gpu(spec, to_dev(b, "f32"), order=order)
+    o, w = run_oracle(spec, b, g["grad_scale"], order=order)
+    compare(g, o, w, rows)
+    n_slots = sum((len(l) + 31) // 32 for l in lists) if order == MULTI_SELECT else None
+    if order == MULTI_SELECT:
+        want = "tma_ring_lists" if n_slots <= 8 else "gather_lists"
+        assert sc.sc_last_kernel().startswith(want), (sc.sc_last_kernel(), n_slots)
