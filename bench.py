@@ -43,9 +43,10 @@ def parse():
     ap.add_argument("--config", type=int, default=CFG, choices=[1, 2, 3, 4, 5],
                     help="BASELINE.json config (default 2, the metric's config; others for characterisation)")
     ap.add_argument("--kernel", default=None, choices=["tma", "gather"], help="force an eval kernel (default: auto)")
-    ap.add_argument("--mode", default="step", choices=["step", "all_apps", "head"],
+    ap.add_argument("--mode", default="step", choices=["step", "all_apps", "head", "sample", "ranges"],
                     help="step: the hot path; all_apps: one read, every application (NEXT f3, config 4); "
-                         "head: classifier-head GEMM fused with the evaluation (NEXT f4)")
+                         "head: classifier-head GEMM fused with the evaluation (NEXT f4); sample: the "
+                         "rebalanced sampler (NEXT f2); ranges: the value-ranges pattern (NEXT f1)")
     ap.add_argument("--d", type=int, default=2048, help="--mode head: feature width (ResNet-50 penultimate = 2048)")
     ap.add_argument("--order", default="api_output", choices=["api_output", "app_choice", "multi_select"],
                     help="decision pattern (default: the north star's API-output order)")
@@ -310,6 +311,11 @@ def run_ours(args):
         return run_head(args, sc, ctx, spec, gt_off, gt_lab, B, dev, stream, rank, data)
     if args.mode == "all_apps":
         return run_all_apps(args, sc, ctx, logits, gt_off, gt_lab, B, dev, stream, rank)
+    if args.mode == "sample":
+        return run_sample(args, sc, ev, logits, gt_off, gt_lab, B, dev, stream, rank)
+    if args.mode == "ranges":
+        del data, logits, gt_off, gt_lab
+        return run_ranges(args, sc, dev, stream, rank)
     for _ in range(args.warmup):
         ev.step(logits, gt_off, gt_lab, app=app, global_rows=global_rows)
     torch.cuda.synchronize(dev)
@@ -436,6 +442,92 @@ def run_all_apps(args, sc, ctx, logits, gt_off, gt_lab, B, dev, stream, rank):
                           "value": B * A / (ms / 1e3), "unit": "evaluations/s", "ms_per_step": ms, "rows": B,
                           "apps": A, "dtype": args.dtype, "config": {"workload": workload_name(args.config, args.dtype)},
                           "reread_equivalent_ms": None}), flush=True)
+    return 0
+
+
+def _peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    return json.load(open(path)).get("hbm_gbs", 6650.0) if os.path.exists(path) else 6650.0
+
+
+def _timed(fn, steps, warmup, stream, dev):
+    import torch
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize(dev)
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record(stream)
+    for _ in range(steps):
+        fn()
+    e.record(stream)
+    torch.cuda.synchronize(dev)
+    return s.elapsed_time(e) / steps
+
+
+def run_sample(args, sc, ev, logits, gt_off, gt_lab, B, dev, stream, rank):
+    """Rebalanced training-data sampler (NEXT f2): B draws with probability
+    proportional to w[G_i] over the batch's B rows (G_i and w from one step of the hot path)."""
+    import torch
+    o = ev.step(logits, gt_off, gt_lab)
+    g = torch.Generator(device=dev)
+    g.manual_seed(args.config)
+    n = B
+    u = torch.rand(2 * n, dtype=torch.float64, device=dev, generator=g)
+    out = torch.empty(n, dtype=torch.int64, device=dev)
+    ws = torch.empty(sc.sc_sample_workspace_bytes(B), dtype=torch.uint8, device=dev)
+    gm = o.gt_mask[:B]
+    ms = _timed(lambda: sc.sc_rebalance_sample(gm, o.w, u, out, workspace=ws), args.steps, args.warmup, stream, dev)
+    per = B * 1 + n * (16 + 8)  # masks read + uniforms read + indices written (algorithmic bytes)
+    peak = _peak()
+    ach = per / (ms / 1e3) / 1e9
+    if rank == 0:
+        print(json.dumps({"metric": "rebalanced draws/s (NEXT f2)", "value": n / (ms / 1e3), "unit": "draws/s",
+                          "ms_per_step": ms, "rows": B, "draws": n, "steps": args.steps, "warmup": args.warmup,
+                          "config": {"workload": workload_name(args.config, args.dtype) + ", G_i / w from the step"},
+                          "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                                       "algorithmic_bytes": per},
+                          "gpu_launches_per_step": 4}), flush=True)
+    return 0
+
+
+def run_ranges(args, sc, dev, stream, rank):
+    """Value-ranges pattern (NEXT f1): GT pre-pass + weights + fused loss
+    pass over 2^26 scores (7 ranges over [-1, 1]; uniform scores and ground-truth scores)."""
+    import torch
+    rows = args.rows or (1 << 26)
+    m = 7
+    edges = torch.linspace(-1.0, 1.0, m + 1)
+    r = sc.Ranges(edges[:-1].numpy().astype("float32"), edges[1:].numpy().astype("float32"), 10.0)
+    g = torch.Generator(device=dev)
+    g.manual_seed(args.config)
+    score = (torch.rand(rows, device=dev, generator=g) * 2.4 - 1.2).float()
+    gt = (torch.rand(rows, device=dev, generator=g) * 2.4 - 1.2).float()
+    hist = torch.zeros(m + 1, dtype=torch.int64, device=dev)
+    gtr = torch.empty(rows, dtype=torch.uint8, device=dev)
+    w = torch.empty(m + 1, dtype=torch.float32, device=dev)
+    out = dict(loss_sum=torch.zeros(1, dtype=torch.float64, device=dev),
+               loss_row=torch.empty(rows, dtype=torch.float32, device=dev),
+               grad=torch.empty(rows, dtype=torch.float32, device=dev),
+               decision=torch.empty(rows, dtype=torch.uint8, device=dev),
+               n_incorrect=torch.zeros(1, dtype=torch.int64, device=dev),
+               hist_pred=torch.zeros(m + 1, dtype=torch.int64, device=dev))
+
+    def step():
+        hist.zero_()
+        sc.sc_ranges_hist(r, gt, hist_gt=hist, gt_range_out=gtr)
+        sc.sc_ranges_weights(r, hist, w)
+        sc.sc_ranges_loss_fwd_bwd(r, score, gtr, w=w, grad_scale=1.0 / rows, **out)
+
+    ms = _timed(step, args.steps, args.warmup, stream, dev)
+    per_row = (4 + 1) + (4 + 1 + 4 + 4 + 1)  # pre-pass: gt score in, range out; loss: score, range in, loss, grad, decision out
+    peak = _peak()
+    ach = rows * per_row / (ms / 1e3) / 1e9
+    if rank == 0:
+        print(json.dumps({"metric": "samples/s, value-ranges decide+loss fwd/bwd (NEXT f1)", "value": rows / (ms / 1e3),
+                          "unit": "samples/s", "ms_per_step": ms, "rows": rows, "ranges": m, "steps": args.steps,
+                          "warmup": args.warmup, "dtype": "f32",
+                          "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                                       "algorithmic_bytes_per_row": per_row}}), flush=True)
     return 0
 
 

@@ -6,7 +6,8 @@
 //   L_i = w[r_i] ( S(l_{r_i} − O_i) + S(O_i − h_{r_i}) ),  w[r] = M / N_r,
 // r_i = the range the ground-truth score lies in (no target range -> L_i = 0).
 // HBM-bound element-wise pass: 4 B score + 1 B ground-truth range in, 1 B decision + 4 B
-// gradient out per row; counters aggregated per warp.
+// loss + 4 B gradient out per row, four rows per thread (128-bit / 32-bit accesses);
+// histograms of <= 32 bins counted with warp ballots into lane-owned registers.
 #include "sc.h"
 
 #include <cuda_runtime.h>
@@ -35,25 +36,67 @@ sc_status rfail(sc_status st, const char* msg) {
   return st;
 }
 
-__device__ __forceinline__ int range_of(const float* lo, const float* hi, int m, float s) {
-  int r = m;
-  for (int j = m - 1; j >= 0; --j)
-    if (s >= lo[j] && s <= hi[j]) r = j;  // the first containing range in code order
-  return r;
+// σ and σ' in overflow-free, branch-free forms (e = e^{-|z|} in (0, 1], so 1 + e in (1, 2]),
+// fast reciprocal divisions (<= 2 ulp) keep the element-wise pass memory-bound.
+// σ(z) and σ'(z) from one exponential: e = e^{-|z|}, r = 1/(1+e); σ = r or e·r, σ' = e·r².
+__device__ __forceinline__ void sig_dsig(float z, float& s, float& ds) {
+  const float e = expf(-fabsf(z));
+  const float r = __fdividef(1.f, 1.f + e);
+  s = z >= 0.f ? r : e * r;
+  ds = e * r * r;
 }
 
-__device__ __forceinline__ float sig(float z) {
-  if (z >= 0.f) return 1.f / (1.f + expf(-z));
-  const float e = expf(z);
-  return e / (1.f + e);
+// Eight consecutive rows per thread per pass (2 x float4 / uint2 accesses when aligned): two
+// 128-bit loads in flight per thread keep enough bytes in flight for an element-wise pass.
+constexpr int kV = 8;
+
+__device__ __forceinline__ uint32_t pack4(int a, int b, int c, int d) {
+  return static_cast<uint32_t>(a) | static_cast<uint32_t>(b) << 8 | static_cast<uint32_t>(c) << 16 |
+         static_cast<uint32_t>(d) << 24;
 }
 
-__device__ __forceinline__ float dsig(float z) {
-  const float t = expf(-fabsf(z));
-  const float d = 1.f + t;
-  return t / (d * d);
+// Histogram counters, by number of bins:
+//   <= 8 (PACKED): each thread counts its own rows in 16-bit fields of two registers (bins
+//     0-3 / 4-7), reduced over the warp at the end — one shift and add per row;
+//   <= 32 (SMALL): lane j of each warp owns bin j and adds the popcount of the warp's ballot;
+//   more: match + shared atomics.
+template <bool SMALL>
+__device__ __forceinline__ void count_bins(int nb, bool act, int v, int lane, unsigned long long& mine,
+                                           unsigned long long* h_s, bool packed, unsigned long long (&pk)[2]) {
+  if (packed) {  // uniform
+    if (act) {
+      const unsigned long long inc = 1ull << (16 * (v & 3));
+      if (v < 4) pk[0] += inc;
+      else pk[1] += inc;
+    }
+    return;
+  }
+  if constexpr (SMALL) {
+    for (int j = 0; j < nb; ++j) {  // nb is uniform
+      const unsigned c = __popc(__ballot_sync(kFull, act && v == j));
+      if (lane == j) mine += c;
+    }
+  } else {
+    const unsigned a = __ballot_sync(kFull, act);
+    if (act) {
+      const unsigned peers = __match_any_sync(a, v);
+      if (lane == __ffs(peers) - 1) atomicAdd(h_s + v, static_cast<unsigned long long>(__popc(peers)));
+    }
+  }
 }
 
+// Packed per-thread counters -> warp sums -> lane j owns bin j (mine); fields never overflow:
+// the host caps a thread's rows per launch below 2^16 (grid_for).
+__device__ __forceinline__ void flush_packed(const unsigned long long (&pk)[2], int lane, unsigned long long& mine) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    unsigned c = static_cast<unsigned>((pk[j >> 2] >> (16 * (j & 3))) & 0xFFFFull);
+    c = __reduce_add_sync(kFull, c);
+    if (lane == j) mine += c;
+  }
+}
+
+template <bool SMALL>
 __global__ void __launch_bounds__(256) ranges_hist_kernel(const float* lo_g, const float* hi_g, int m,
                                                          const float* gt_score, int64_t rows,
                                                          unsigned long long* hist, uint8_t* gt_range) {
@@ -63,24 +106,50 @@ __global__ void __launch_bounds__(256) ranges_hist_kernel(const float* lo_g, con
   for (int j = threadIdx.x; j <= m; j += blockDim.x) h[j] = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  unsigned long long mine = 0;
+  const bool packed = SMALL && m + 1 <= 8;
+  unsigned long long pk[2] = {0ull, 0ull};
+  const bool vec = (reinterpret_cast<uintptr_t>(gt_score) % 16 == 0) &&
+                   (!gt_range || reinterpret_cast<uintptr_t>(gt_range) % 8 == 0);
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x * kV;
   const int64_t iters = (rows + stride - 1) / stride;
   for (int64_t it = 0; it < iters; ++it) {
-    const int64_t i = it * stride + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const bool act = i < rows;
-    int r = 0;
-    if (act) {
-      r = range_of(lo, hi, m, __ldg(gt_score + i));
-      if (gt_range) gt_range[i] = static_cast<uint8_t>(r);
+    const int64_t i0 = it * stride + (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * kV;
+    float sv[kV];
+    int r[kV];
+    if (vec && i0 + kV <= rows) {
+      const float4 f = __ldg(reinterpret_cast<const float4*>(gt_score + i0));
+      const float4 f2 = __ldg(reinterpret_cast<const float4*>(gt_score + i0 + 4));
+      sv[0] = f.x; sv[1] = f.y; sv[2] = f.z; sv[3] = f.w;
+      sv[4] = f2.x; sv[5] = f2.y; sv[6] = f2.z; sv[7] = f2.w;
+    } else {
+#pragma unroll
+      for (int q = 0; q < kV; ++q) sv[q] = i0 + q < rows ? __ldg(gt_score + i0 + q) : 0.f;
     }
-    if (hist) {
-      const unsigned a = __ballot_sync(kFull, act);
-      if (act) {
-        const unsigned peers = __match_any_sync(a, r);
-        if (lane == __ffs(peers) - 1) atomicAdd(h + r, static_cast<unsigned long long>(__popc(peers)));
+#pragma unroll
+    for (int q = 0; q < kV; ++q) r[q] = m;
+    for (int j = m - 1; j >= 0; --j) {  // the first containing range in code order
+      const float l = lo[j], u = hi[j];
+#pragma unroll
+      for (int q = 0; q < kV; ++q)
+        if (sv[q] >= l && sv[q] <= u) r[q] = j;
+    }
+    if (gt_range) {
+      if (vec && i0 + kV <= rows) {
+        *reinterpret_cast<uint2*>(gt_range + i0) = make_uint2(pack4(r[0], r[1], r[2], r[3]), pack4(r[4], r[5], r[6], r[7]));
+      } else {
+#pragma unroll
+        for (int q = 0; q < kV; ++q)
+          if (i0 + q < rows) gt_range[i0 + q] = static_cast<uint8_t>(r[q]);
       }
     }
+    if (hist) {
+#pragma unroll
+      for (int q = 0; q < kV; ++q) count_bins<SMALL>(m + 1, i0 + q < rows, r[q], lane, mine, h, packed, pk);
+    }
   }
+  if (packed && hist) flush_packed(pk, lane, mine);
+  if (SMALL && hist && lane <= m && mine) atomicAdd(h + lane, mine);
   __syncthreads();
   if (hist)
     for (int j = threadIdx.x; j <= m; j += blockDim.x)
@@ -99,6 +168,7 @@ __global__ void ranges_weights_kernel(const unsigned long long* hist, int m, flo
     w[j] = hist[j] ? static_cast<float>(static_cast<double>(M) / static_cast<double>(hist[j])) : 0.f;
 }
 
+template <bool SMALL>
 __global__ void __launch_bounds__(256) ranges_loss_kernel(const float* lo_g, const float* hi_g, int m, float k,
                                                          const float* score, const uint8_t* gt_range, int64_t rows,
                                                          const float* w, float grad_scale, double* loss_sum,
@@ -114,38 +184,91 @@ __global__ void __launch_bounds__(256) ranges_loss_kernel(const float* lo_g, con
   if (threadIdx.x == 0) { ninc = 0; lsum = 0.0; }
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const bool vec = (reinterpret_cast<uintptr_t>(score) % 16 == 0) && (reinterpret_cast<uintptr_t>(gt_range) % 8 == 0) &&
+                   (!decision || reinterpret_cast<uintptr_t>(decision) % 8 == 0) &&
+                   (!loss_row || reinterpret_cast<uintptr_t>(loss_row) % 16 == 0) &&
+                   (!grad || reinterpret_cast<uintptr_t>(grad) % 16 == 0);
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x * kV;
   const int64_t iters = (rows + stride - 1) / stride;
   double my_loss = 0.0;
-  unsigned my_inc = 0;
+  unsigned long long my_inc = 0, mine = 0;
+  const bool packed = SMALL && m + 1 <= 8;
+  unsigned long long pk[2] = {0ull, 0ull};
   for (int64_t it = 0; it < iters; ++it) {
-    const int64_t i = it * stride + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const bool act = i < rows;
-    int d = 0;
-    if (act) {
-      const float s = __ldg(score + i);
-      const int r = __ldg(gt_range + i);
-      d = range_of(lo, hi, m, s);
-      my_inc += d != r;
-      float L = 0.f, g = 0.f;
-      if (r < m) {
-        const float a = k * (lo[r] - s), b = k * (s - hi[r]);
-        L = ws[r] * (sig(a) + sig(b));
-        g = ws[r] * k * (dsig(b) - dsig(a)) * grad_scale;
+    const int64_t i0 = it * stride + (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * kV;
+    const bool full = vec && i0 + kV <= rows;
+    float sv[kV];
+    int r[kV], d[kV];
+    if (full) {
+      const float4 f = __ldg(reinterpret_cast<const float4*>(score + i0));
+      const float4 f2 = __ldg(reinterpret_cast<const float4*>(score + i0 + 4));
+      const uint2 g = __ldg(reinterpret_cast<const uint2*>(gt_range + i0));
+      sv[0] = f.x; sv[1] = f.y; sv[2] = f.z; sv[3] = f.w;
+      sv[4] = f2.x; sv[5] = f2.y; sv[6] = f2.z; sv[7] = f2.w;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        r[q] = (g.x >> (8 * q)) & 0xFFu;
+        r[4 + q] = (g.y >> (8 * q)) & 0xFFu;
       }
-      my_loss += L;
-      if (decision) decision[i] = static_cast<uint8_t>(d);
-      if (loss_row) loss_row[i] = L;
-      if (grad) grad[i] = g;
+    } else {
+#pragma unroll
+      for (int q = 0; q < kV; ++q) {
+        sv[q] = i0 + q < rows ? __ldg(score + i0 + q) : 0.f;
+        r[q] = i0 + q < rows ? __ldg(gt_range + i0 + q) : m;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kV; ++q) d[q] = m;
+    for (int j = m - 1; j >= 0; --j) {  // Decision(API(x)): the first containing range in code order
+      const float l = lo[j], u = hi[j];
+#pragma unroll
+      for (int q = 0; q < kV; ++q)
+        if (sv[q] >= l && sv[q] <= u) d[q] = j;
+    }
+    float L[kV], g[kV];
+#pragma unroll
+    for (int q = 0; q < kV; ++q) {
+      const bool act = i0 + q < rows;
+      L[q] = 0.f;
+      g[q] = 0.f;
+      if (act && r[q] < m) {
+        const float a = k * (lo[r[q]] - sv[q]), b = k * (sv[q] - hi[r[q]]);
+        float sa, da, sb, db;
+        sig_dsig(a, sa, da);
+        sig_dsig(b, sb, db);
+        L[q] = ws[r[q]] * (sa + sb);
+        g[q] = ws[r[q]] * k * (db - da) * grad_scale;
+      }
+      my_loss += L[q];
+      my_inc += (act && d[q] != r[q]) ? 1u : 0u;
+    }
+    if (full) {
+      if (decision)
+        *reinterpret_cast<uint2*>(decision + i0) = make_uint2(pack4(d[0], d[1], d[2], d[3]), pack4(d[4], d[5], d[6], d[7]));
+      if (loss_row) {
+        *reinterpret_cast<float4*>(loss_row + i0) = make_float4(L[0], L[1], L[2], L[3]);
+        *reinterpret_cast<float4*>(loss_row + i0 + 4) = make_float4(L[4], L[5], L[6], L[7]);
+      }
+      if (grad) {
+        *reinterpret_cast<float4*>(grad + i0) = make_float4(g[0], g[1], g[2], g[3]);
+        *reinterpret_cast<float4*>(grad + i0 + 4) = make_float4(g[4], g[5], g[6], g[7]);
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < kV; ++q) {
+        if (i0 + q >= rows) continue;
+        if (decision) decision[i0 + q] = static_cast<uint8_t>(d[q]);
+        if (loss_row) loss_row[i0 + q] = L[q];
+        if (grad) grad[i0 + q] = g[q];
+      }
     }
     if (hist_pred) {
-      const unsigned a = __ballot_sync(kFull, act);
-      if (act) {
-        const unsigned peers = __match_any_sync(a, d);
-        if (lane == __ffs(peers) - 1) atomicAdd(hp + d, static_cast<unsigned long long>(__popc(peers)));
-      }
+#pragma unroll
+      for (int q = 0; q < kV; ++q) count_bins<SMALL>(m + 1, i0 + q < rows, d[q], lane, mine, hp, packed, pk);
     }
   }
+  if (packed && hist_pred) flush_packed(pk, lane, mine);
+  if (SMALL && hist_pred && lane <= m && mine) atomicAdd(hp + lane, mine);
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
     my_loss += __shfl_xor_sync(kFull, my_loss, off);
@@ -153,7 +276,7 @@ __global__ void __launch_bounds__(256) ranges_loss_kernel(const float* lo_g, con
   }
   if (lane == 0) {
     atomicAdd(&lsum, my_loss);
-    atomicAdd(&ninc, static_cast<unsigned long long>(my_inc));
+    atomicAdd(&ninc, my_inc);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -169,8 +292,11 @@ int grid_for(int64_t rows) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int64_t g = (rows + 255) / 256;
+  int64_t g = (rows + 256 * kV - 1) / (256 * kV);
   if (g > static_cast<int64_t>(sms) * 8) g = static_cast<int64_t>(sms) * 8;
+  // packed 16-bit per-thread counters: < 2^16 rows per thread per launch
+  const int64_t g_min = (rows + 256LL * 65535 - 1) / (256LL * 65535);
+  if (g < g_min) g = g_min;
   return g < 1 ? 1 : static_cast<int>(g);
 }
 
@@ -219,7 +345,8 @@ sc_status sc_ranges_hist(sc_ranges r, const float* gt_score, int64_t rows, uint6
   if (rows < 0) return rfail(SC_ERR_INVALID_ARG, "rows < 0");
   if (rows == 0 || (!hist_gt && !gt_range_out)) return SC_OK;
   if (!gt_score) return rfail(SC_ERR_INVALID_ARG, "gt_score is NULL");
-  ranges_hist_kernel<<<grid_for(rows), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+  auto kern = r->m + 1 <= 32 ? ranges_hist_kernel<true> : ranges_hist_kernel<false>;
+  kern<<<grid_for(rows), 256, 0, static_cast<cudaStream_t>(stream)>>>(
       r->d_lo, r->d_hi, r->m, gt_score, rows, reinterpret_cast<unsigned long long*>(hist_gt), gt_range_out);
   if (cudaError_t e = cudaGetLastError()) return rfail(SC_ERR_CUDA, cudaGetErrorString(e));
   return SC_OK;
@@ -240,7 +367,8 @@ sc_status sc_ranges_loss_fwd_bwd(sc_ranges r, const float* score, const uint8_t*
   if (rows < 0) return rfail(SC_ERR_INVALID_ARG, "rows < 0");
   if (rows == 0) return SC_OK;
   if (!score || !gt_range) return rfail(SC_ERR_INVALID_ARG, "score / gt_range is NULL");
-  ranges_loss_kernel<<<grid_for(rows), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+  auto kern = r->m + 1 <= 32 ? ranges_loss_kernel<true> : ranges_loss_kernel<false>;
+  kern<<<grid_for(rows), 256, 0, static_cast<cudaStream_t>(stream)>>>(
       r->d_lo, r->d_hi, r->m, r->k, score, gt_range, rows, w, grad_scale, loss_sum, loss_row, grad, decision,
       reinterpret_cast<unsigned long long*>(n_incorrect), reinterpret_cast<unsigned long long*>(hist_pred));
   if (cudaError_t e = cudaGetLastError()) return rfail(SC_ERR_CUDA, cudaGetErrorString(e));
