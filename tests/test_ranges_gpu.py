@@ -7,8 +7,9 @@ from conftest import gpu_available
 pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device")]
 
 
-@pytest.mark.parametrize("m,rows", [(1, 1), (3, 100003), (7, 5000), (40, 20000)])
-def test_ranges_parity(m, rows):
+@pytest.mark.parametrize("m,rows,off", [(1, 1, 0), (3, 100003, 0), (7, 5000, 0), (7, 5000, 1), (20, 70001, 0),
+                                        (40, 20000, 0), (40, 20000, 3)])  # 2-8 bins packed, 21 ballot, 41 match;
+def test_ranges_parity(m, rows, off):                                     # off: unaligned (scalar) accesses
     import torch
     import paper_2310_07240_b200 as sc
     from oracle import RangesOracle
@@ -27,16 +28,19 @@ def test_ranges_parity(m, rows):
     ref = orc.eval(score, gt, w=w_ref, grad_scale=1.0 / rows)
 
     r = sc.Ranges(lo, hi, k)
-    d_score, d_gt = torch.from_numpy(score).cuda(), torch.from_numpy(gt).cuda()
+    # off > 0: the device arrays start `off` elements into a larger allocation (not 16-B aligned)
+    d_score = torch.cat([torch.zeros(off), torch.from_numpy(score)]).cuda()[off:]
+    d_gt = torch.cat([torch.zeros(off), torch.from_numpy(gt)]).cuda()[off:]
     hist = torch.zeros(m + 1, dtype=torch.int64, device="cuda")
-    gtr = torch.empty(rows, dtype=torch.uint8, device="cuda")
+    def buf(dt):  # outputs shifted by `off` elements as well
+        return torch.empty(rows + off, dtype=dt, device="cuda")[off:]
+
+    gtr = buf(torch.uint8)
     sc.sc_ranges_hist(r, d_gt, hist_gt=hist, gt_range_out=gtr)
     w = torch.empty(m + 1, dtype=torch.float32, device="cuda")
     sc.sc_ranges_weights(r, hist, w)
     out = dict(loss_sum=torch.zeros(1, dtype=torch.float64, device="cuda"),
-               loss_row=torch.empty(rows, dtype=torch.float32, device="cuda"),
-               grad=torch.empty(rows, dtype=torch.float32, device="cuda"),
-               decision=torch.empty(rows, dtype=torch.uint8, device="cuda"),
+               loss_row=buf(torch.float32), grad=buf(torch.float32), decision=buf(torch.uint8),
                n_incorrect=torch.zeros(1, dtype=torch.int64, device="cuda"),
                hist_pred=torch.zeros(m + 1, dtype=torch.int64, device="cuda"))
     sc.sc_ranges_loss_fwd_bwd(r, d_score, gtr, w=w, grad_scale=1.0 / rows, **out)
