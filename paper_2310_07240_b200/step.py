@@ -40,18 +40,29 @@ def allreduce_(t: torch.Tensor, group=None):
 
 
 def allreduce_many_(tensors, group=None):
-    """Several sum-allreduces issued as one NCCL group when the backend supports coalescing."""
+    """Several sum-allreduces; tensors of one dtype are issued as one NCCL group."""
     if not _pg_active(group):
         return tensors
+    return _allreduce_list_(tensors, group)
+
+
+def _allreduce_list_(tensors, group=None):
+    # NCCL's coalesced allreduce requires identical dtypes ("Tensors must have identical
+    # type", measured with NCCL 2.28 / torch 2.11): coalesce per dtype, int64 counters and
+    # the fp64 loss go as separate collectives.
     import torch.distributed as dist
     cm = getattr(dist, "_coalescing_manager", None)
-    if cm is not None and tensors[0].is_cuda and dist.get_backend(group) == "nccl":
-        with cm(group=group, device=tensors[0].device):
-            for t in tensors:
+    by_dtype = {}
+    for t in tensors:
+        by_dtype.setdefault(t.dtype, []).append(t)
+    for ts in by_dtype.values():
+        if len(ts) > 1 and cm is not None and ts[0].is_cuda and dist.get_backend(group) == "nccl":
+            with cm(group=group, device=ts[0].device):
+                for t in ts:
+                    dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+        else:
+            for t in ts:
                 dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
-    else:
-        for t in tensors:
-            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
     return tensors
 
 
