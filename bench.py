@@ -59,6 +59,11 @@ def parse():
 
 # ------------------------------------------------------------------ helpers
 
+def dist_on(world: int) -> bool:
+    """Collectives in play: N > 1, or SC_FORCE_DIST=1 (the N > 1 path with one rank)."""
+    return world > 1 or os.environ.get("SC_FORCE_DIST") == "1"
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -280,7 +285,8 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     group = None
-    if world > 1:
+    # SC_FORCE_DIST=1: a process group (and the N > 1 step) even for one rank
+    if dist_on(world):
         import torch.distributed as dist
         if share:
             dist.init_process_group("gloo")
@@ -302,7 +308,7 @@ def run_ours(args):
     global_rows = B * world
 
     def barrier():
-        if world > 1:
+        if dist_on(world):
             import torch.distributed as dist
             dist.barrier()
 
@@ -360,7 +366,7 @@ def run_ours(args):
                 for ph in phases if ph in called}
     ms = t_start.elapsed_time(t_end)
     k_ms = sum(a.elapsed_time(b) for a, b in zip(k_start, k_end)) / args.steps
-    if world > 1:
+    if dist_on(world):
         import torch.distributed as dist
         t = torch.tensor([ms, k_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -414,7 +420,7 @@ def run_ours(args):
                                 "sample": smp.describe(dt)}
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist_on(world):
         import torch.distributed as dist
         dist.destroy_process_group()
     return 0
@@ -640,7 +646,7 @@ def run_e2e(args, ev, data, global_rows, dev, barrier, world):
         ev.step_host(h_logits, h_off, h_lab, host_out, h_app=h_app, global_rows=global_rows)
     torch.cuda.synchronize(dev)
     dt = time.perf_counter() - t0
-    if world > 1:
+    if dist_on(world):
         import torch.distributed as dist
         t = torch.tensor([dt], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

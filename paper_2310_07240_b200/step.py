@@ -27,8 +27,14 @@ def shard_range(rows: int, rank: int, world: int):
 
 
 def _pg_active(group) -> bool:
+    """A process group with > 1 rank is active (SC_FORCE_DIST=1: any initialised group, so the
+    N > 1 step — collectives included — can be run with one rank on one GPU)."""
+    import os
+
     import torch.distributed as dist
-    return dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1
+    if not (dist.is_available() and dist.is_initialized()):
+        return False
+    return dist.get_world_size(group) > 1 or os.environ.get("SC_FORCE_DIST") == "1"
 
 
 def allreduce_(t: torch.Tensor, group=None):
