@@ -492,7 +492,7 @@ def run_sample(args, sc, ev, logits, gt_off, gt_lab, B, dev, stream, rank):
                           "config": {"workload": workload_name(args.config, args.dtype) + ", G_i / w from the step"},
                           "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
                                        "algorithmic_bytes": per},
-                          "gpu_launches_per_step": 4}), flush=True)
+                          "gpu_launches_per_step": 5}), flush=True)
     return 0
 
 

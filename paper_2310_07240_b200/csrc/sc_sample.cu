@@ -8,9 +8,10 @@
 // ascending m; bucket = first m with u1·ΣW < cumulative W; row = number
 // min(count_m − 1, floor(u2·count_m)) of the bucket.
 //
-// Four launches: per-chunk mask counts, one-CTA scans (bucket starts, per-chunk offsets,
-// CDF in the oracle's summation order), a stable scatter (one warp per chunk, rows in
-// order), and the draws (one thread per draw, CDF in shared memory).
+// Five launches: per-chunk mask counts; per-mask scans over the chunks (one CTA per mask);
+// bucket starts and the CDF in the oracle's summation order (one CTA); a stable scatter
+// (one warp per 1024-row chunk, rows in order); the draws (one thread per draw, CDF in
+// shared memory).
 #include "sc.h"
 
 #include <cuda_runtime.h>
@@ -20,7 +21,8 @@
 namespace {
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
-constexpr int64_t kChunk = 4096;  // rows per chunk of the counting sort
+constexpr int64_t kChunk = 1024;  // rows per chunk of the counting sort (one scatter warp each)
+constexpr int kScatterWarps = 8;  // chunks per scatter CTA
 
 thread_local std::string g_serr;
 
@@ -31,7 +33,7 @@ sc_status sfail(sc_status st, const char* msg) {
 
 struct Workspace {  // carved from the caller's buffer
   unsigned* chunk_cnt;   // [nchunks][256]
-  int64_t* chunk_off;    // [nchunks][256]  first slot of (chunk, mask) in bucket order
+  int64_t* chunk_off;    // [nchunks][256]  first slot of (chunk, mask) within mask m's bucket
   int64_t* count;        // [256]
   int64_t* start;        // [256]
   double* cum;           // [256]
@@ -78,17 +80,41 @@ __global__ void __launch_bounds__(256) chunk_count_kernel(const uint8_t* gt_mask
   chunk_cnt[static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x] = h[threadIdx.x];
 }
 
-// One CTA of 256 threads (a thread per mask).
-__global__ void __launch_bounds__(256) scan_kernel(const unsigned* chunk_cnt, int64_t nch, const float* w,
-                                                   Workspace ws) {
-  __shared__ int64_t cnt[256];
-  const int m = threadIdx.x;
-  int64_t c = 0;
-  for (int64_t k = 0; k < nch; ++k) c += chunk_cnt[k * 256 + m];
-  cnt[m] = c;
-  ws.count[m] = c;
+// One CTA per mask m: exclusive scan of chunk_cnt[., m] over the chunks (256 at a time,
+// warp shuffles + one shared-memory pass), total count of m.
+__global__ void __launch_bounds__(256) chunk_scan_kernel(const unsigned* chunk_cnt, int64_t nch, Workspace ws) {
+  __shared__ int64_t warp_sum[8];
+  __shared__ int64_t carry_s;
+  const int m = blockIdx.x, lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (threadIdx.x == 0) carry_s = 0;
   __syncthreads();
-  if (m == 0) {  // sequential, ascending m: the oracle's summation order
+  for (int64_t k0 = 0; k0 < nch; k0 += 256) {
+    const int64_t k = k0 + threadIdx.x;
+    const int64_t v = k < nch ? static_cast<int64_t>(chunk_cnt[k * 256 + m]) : 0;
+    int64_t x = v;  // inclusive warp scan
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int64_t y = __shfl_up_sync(kFull, x, off);
+      if (lane >= off) x += y;
+    }
+    if (lane == 31) warp_sum[wid] = x;
+    __syncthreads();
+    int64_t before = carry_s;
+    for (int q = 0; q < wid; ++q) before += warp_sum[q];
+    if (k < nch) ws.chunk_off[k * 256 + m] = before + x - v;
+    __syncthreads();
+    if (threadIdx.x == 255) carry_s = before + x;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) ws.count[m] = carry_s;
+}
+
+// One CTA: bucket starts and the CDF, sequential in ascending m (the oracle's summation order).
+__global__ void __launch_bounds__(256) starts_kernel(const float* w, Workspace ws) {
+  __shared__ int64_t cnt[256];
+  cnt[threadIdx.x] = ws.count[threadIdx.x];
+  __syncthreads();
+  if (threadIdx.x == 0) {
     int64_t s = 0;
     double tot = 0.0;
     for (int q = 0; q < 256; ++q) {
@@ -99,21 +125,19 @@ __global__ void __launch_bounds__(256) scan_kernel(const unsigned* chunk_cnt, in
     }
     *ws.status = tot > 0.0 ? 0 : 1;
   }
-  __syncthreads();
-  int64_t run = ws.start[m];
-  for (int64_t k = 0; k < nch; ++k) {
-    ws.chunk_off[k * 256 + m] = run;
-    run += chunk_cnt[k * 256 + m];
-  }
 }
 
 // One warp per chunk walks its rows in order: stable rank among equal masks.
-__global__ void __launch_bounds__(32) scatter_kernel(const uint8_t* gt_mask, int64_t rows, Workspace ws) {
-  __shared__ int64_t next[256];
-  const int lane = threadIdx.x;
-  for (int m = lane; m < 256; m += 32) next[m] = ws.chunk_off[static_cast<int64_t>(blockIdx.x) * 256 + m];
+__global__ void __launch_bounds__(32 * kScatterWarps) scatter_kernel(const uint8_t* gt_mask, int64_t rows,
+                                                                    int64_t nch, Workspace ws) {
+  __shared__ int64_t next_s[kScatterWarps][256];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t chunk = static_cast<int64_t>(blockIdx.x) * kScatterWarps + wid;
+  if (chunk >= nch) return;  // whole warps only: no CTA-wide barrier below
+  int64_t* next = next_s[wid];
+  for (int m = lane; m < 256; m += 32) next[m] = ws.start[m] + ws.chunk_off[chunk * 256 + m];
   __syncwarp();
-  const int64_t lo = static_cast<int64_t>(blockIdx.x) * kChunk;
+  const int64_t lo = chunk * kChunk;
   const int64_t hi = lo + kChunk < rows ? lo + kChunk : rows;
   for (int64_t i0 = lo; i0 < hi; i0 += 32) {
     const int64_t i = i0 + lane;
@@ -175,8 +199,10 @@ sc_status sc_rebalance_sample(const uint8_t* gt_mask, int64_t rows, const float*
   const int64_t nch = (rows + kChunk - 1) / kChunk;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   chunk_count_kernel<<<static_cast<unsigned>(nch), 256, 0, st>>>(gt_mask, rows, ws.chunk_cnt);
-  scan_kernel<<<1, 256, 0, st>>>(ws.chunk_cnt, nch, w, ws);
-  scatter_kernel<<<static_cast<unsigned>(nch), 32, 0, st>>>(gt_mask, rows, ws);
+  chunk_scan_kernel<<<256, 256, 0, st>>>(ws.chunk_cnt, nch, ws);
+  starts_kernel<<<1, 256, 0, st>>>(w, ws);
+  scatter_kernel<<<static_cast<unsigned>((nch + kScatterWarps - 1) / kScatterWarps), 32 * kScatterWarps, 0, st>>>(
+      gt_mask, rows, nch, ws);
   if (n > 0) {
     int64_t g = (n + 255) / 256;
     if (g > 148 * 16) g = 148 * 16;
