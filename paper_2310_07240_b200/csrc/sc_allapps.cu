@@ -11,7 +11,9 @@
 // G for all applications from the row's ground-truth labels and a label-major copy of
 // the category table (one coalesced 256-B read per label for 256 apps), then its 32 warps
 // take the applications round-robin: split maxima over the app's labels, two REDUX pairs,
-// decision, correctness, shared-memory counters; counters flushed once per CTA.
+// the app's maxima parked in one lane so decision, correctness and the shared-memory
+// counters run lane-parallel once per row; the next row's G is built while this row is
+// evaluated; counters flushed once per CTA.
 #include "sc_internal.cuh"
 
 #include <cuda_runtime.h>
@@ -73,8 +75,8 @@ __global__ void __launch_bounds__(kAAWarps * 32, 1) all_apps_kernel(const AllApp
   int32_t* eoff = reinterpret_cast<int32_t*>(ents + p.n_ent_total);
   unsigned* cnt_inc = reinterpret_cast<unsigned*>(eoff + A + 1);
   unsigned* cnt_pred = cnt_inc + A;                       // [A][16]
-  uint8_t* gs = reinterpret_cast<uint8_t*>(cnt_pred + A * 16);   // [A] G of the current row per app
-  uint8_t* nl = gs + A;                                   // [A] D'
+  uint8_t* gs2 = reinterpret_cast<uint8_t*>(cnt_pred + A * 16);  // [2][A] G per app, double-buffered by row
+  uint8_t* nl = gs2 + 2 * A;                              // [A] D'
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + p.bar_off);  // [2]
   for (int i = tid; i < p.n_ent_total; i += blockDim.x) ents[i] = __ldg(p.ctx.ent + i);
   for (int i = tid; i <= A; i += blockDim.x) eoff[i] = __ldg(p.ctx.ent_off + i);
@@ -84,21 +86,9 @@ __global__ void __launch_bounds__(kAAWarps * 32, 1) all_apps_kernel(const AllApp
   __syncthreads();
 
   const int64_t first = blockIdx.x, step = gridDim.x;
-  // prefetch the first row
-  if (tid == 0 && first < p.rows) {
-    mbar_expect(bar, p.copy_bytes);
-    bulk_copy(rowbuf[0], p.logits + first * p.ld_bytes, p.copy_bytes, bar);
-  }
-  uint32_t phase[2] = {0, 0};
-  int buf = 0;
-  for (int64_t row = first; row < p.rows; row += step, buf ^= 1) {
-    // next row into the other buffer (its previous row was fully consumed: barrier below)
-    const int64_t nxt = row + step;
-    if (tid == 0 && nxt < p.rows) {
-      mbar_expect(bar + (buf ^ 1), p.copy_bytes);
-      bulk_copy(rowbuf[buf ^ 1], p.logits + nxt * p.ld_bytes, p.copy_bytes, bar + (buf ^ 1));
-    }
-    // G for every app from the row's ground truth (label-major category table)
+  // G for every app from a row's ground truth (label-major category table)
+  auto build_g = [&](int64_t row, uint8_t* gs) {
+    if (row >= p.rows) return;
     const int64_t g0 = __ldg(p.gt_off + row), g1 = __ldg(p.gt_off + row + 1);
     for (int a = tid; a < A; a += blockDim.x) {
       uint32_t G = 0;
@@ -108,11 +98,35 @@ __global__ void __launch_bounds__(kAAWarps * 32, 1) all_apps_kernel(const AllApp
       }
       gs[a] = static_cast<uint8_t>(G);
     }
+  };
+  // prefetch the first row and its G
+  if (tid == 0 && first < p.rows) {
+    mbar_expect(bar, p.copy_bytes);
+    bulk_copy(rowbuf[0], p.logits + first * p.ld_bytes, p.copy_bytes, bar);
+  }
+  build_g(first, gs2);
+  __syncthreads();
+  uint32_t phase[2] = {0, 0};
+  int buf = 0;
+  for (int64_t row = first; row < p.rows; row += step, buf ^= 1) {
+    // next row into the other buffer (its previous row was fully consumed: barrier below),
+    // and the next row's G (its loads overlap this row's evaluation)
+    const int64_t nxt = row + step;
+    if (tid == 0 && nxt < p.rows) {
+      mbar_expect(bar + (buf ^ 1), p.copy_bytes);
+      bulk_copy(rowbuf[buf ^ 1], p.logits + nxt * p.ld_bytes, p.copy_bytes, bar + (buf ^ 1));
+    }
+    build_g(nxt, gs2 + (buf ^ 1) * A);
     mbar_wait_parity(bar + buf, phase[buf]);
     phase[buf] ^= 1u;
-    __syncthreads();
     const uint8_t* rb = rowbuf[buf];
-    for (int a = warp; a < A; a += kAAWarps) {
+    const uint8_t* gs = gs2 + buf * A;
+    // this warp's apps a = warp + 32 j: the split maxima of app j park in lane j, and the
+    // decision / counters run lane-parallel once per row
+    float pzp = 0.f, pzm = 0.f;
+    uint32_t pkp = kNone, pkm = kNone;
+    int pa = -1, j = 0;
+    for (int a = warp; a < A; a += kAAWarps, ++j) {
       const uint32_t G = gs[a];
       float zp = -CUDART_INF_F, zm = -CUDART_INF_F;
       uint32_t kp = kNone, km = kNone;
@@ -129,20 +143,25 @@ __global__ void __launch_bounds__(kAAWarps * 32, 1) all_apps_kernel(const AllApp
       }
       argmax_warp(zp, kp);
       argmax_warp(zm, km);
-      if (lane == 0) {
-        const uint32_t D = nl[a];
-        const bool hp = kp != kNone, hm = km != kNone;
-        const bool take_p = hp && (!hm || zp > zm || (zp == zm && kp < km));
-        const float zs = take_p ? zp : zm;
-        const uint32_t ks = take_p ? kp : km;
-        const uint32_t dec = ((hp || hm) && zs > p.ctx.tau) ? (ks & 0xFFu) : D;
-        const bool ok = G ? (dec < D && ((G >> dec) & 1u)) : (dec == D);
-        if (!ok) atomicAdd(cnt_inc + a, 1u);
-        atomicAdd(cnt_pred + a * 16 + dec, 1u);
-        if (p.decision) p.decision[row * A + a] = static_cast<uint8_t>(dec);
+      if (lane == (j & 31)) { pzp = zp; pkp = kp; pzm = zm; pkm = km; pa = a; }
+      if ((j & 31) == 31 || a + kAAWarps >= A) {  // warp-uniform: flush the parked apps
+        if (pa >= 0) {
+          const uint32_t Ga = gs[pa];
+          const uint32_t D = nl[pa];
+          const bool hp = pkp != kNone, hm = pkm != kNone;
+          const bool take_p = hp && (!hm || pzp > pzm || (pzp == pzm && pkp < pkm));
+          const float zs = take_p ? pzp : pzm;
+          const uint32_t ks = take_p ? pkp : pkm;
+          const uint32_t dec = ((hp || hm) && zs > p.ctx.tau) ? (ks & 0xFFu) : D;
+          const bool ok = Ga ? (dec < D && ((Ga >> dec) & 1u)) : (dec == D);
+          if (!ok) atomicAdd(cnt_inc + pa, 1u);
+          atomicAdd(cnt_pred + pa * 16 + dec, 1u);
+          if (p.decision) p.decision[row * A + pa] = static_cast<uint8_t>(dec);
+        }
+        pa = -1;
       }
     }
-    __syncthreads();  // row buffer and gs are reused
+    __syncthreads();  // row buffer, gs and the next row's G are reused / complete
   }
   for (int i = tid; i < A; i += blockDim.x)
     if (cnt_inc[i] && p.n_incorrect) atomicAdd(p.n_incorrect + i, static_cast<unsigned long long>(cnt_inc[i]));

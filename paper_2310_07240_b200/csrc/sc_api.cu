@@ -597,7 +597,7 @@ sc_status sc_decide_all_apps(sc_context ctx, const sc_batch* b, uint64_t* n_inco
   p.hist_pred = reinterpret_cast<unsigned long long*>(hist_pred);
   p.decision = decision;
   const int64_t A = ctx->n_apps;
-  int64_t off = 2 * static_cast<int64_t>(p.row_bytes_pad) + 4 * p.n_ent_total + 4 * (A + 1) + 4 * A + 64 * A + 2 * A;
+  int64_t off = 2 * static_cast<int64_t>(p.row_bytes_pad) + 4 * p.n_ent_total + 4 * (A + 1) + 4 * A + 64 * A + 3 * A;
   p.bar_off = static_cast<int32_t>(round_up(off, 8));
   const size_t smem = static_cast<size_t>(p.bar_off + 16);
   if (smem > kSmemMax) return fail(SC_ERR_UNSUPPORTED, "contexts too large for the all-apps pass (shared memory)");
