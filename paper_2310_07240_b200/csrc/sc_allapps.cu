@@ -65,19 +65,39 @@ __device__ __forceinline__ void argmax_warp(float& z, uint32_t& k) {
   z = om ? __uint_as_float((om & 0x80000000u) ? (om ^ 0x80000000u) : ~om) : -CUDART_INF_F;
 }
 
+// Split maxima of one app over one row, both classes (P⁺ over 𝒲_i, P⁻ over the rest).
+struct Split {
+  float zp, zm;
+  uint32_t kp, km;
+};
+
+// Decision and correctness of one (row, app) from its reduced split maxima.
+__device__ __forceinline__ void aa_decide(const Split& m, uint32_t G, uint32_t D, float tau, uint32_t& dec, bool& ok) {
+  const bool hp = m.kp != kNone, hm = m.km != kNone;
+  const bool take_p = hp && (!hm || m.zp > m.zm || (m.zp == m.zm && m.kp < m.km));
+  const float zs = take_p ? m.zp : m.zm;
+  const uint32_t ks = take_p ? m.kp : m.km;
+  dec = ((hp || hm) && zs > tau) ? (ks & 0xFFu) : D;
+  ok = G ? (dec < D && ((G >> dec) & 1u)) : (dec == D);
+}
+
+// Units of kAARows consecutive rows: one barrier interval evaluates every app on all of
+// them (the app's keys are read once per unit, kAARows rows' loads in flight per entry).
+constexpr int kAARows = kAllAppsRows;
+
 __global__ void __launch_bounds__(kAAWarps * 32, 1) all_apps_kernel(const AllAppsParams p) {
   extern __shared__ __align__(128) uint8_t sm[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int A = p.ctx.n_apps;
-  // carve shared memory
-  uint8_t* rowbuf[2] = {sm, sm + p.row_bytes_pad};
-  uint32_t* ents = reinterpret_cast<uint32_t*>(sm + 2 * p.row_bytes_pad);
+  // carve shared memory: [2 units][kAARows rows] row buffers
+  uint8_t* rowbuf = sm;
+  uint32_t* ents = reinterpret_cast<uint32_t*>(sm + 2 * kAARows * p.row_bytes_pad);
   int32_t* eoff = reinterpret_cast<int32_t*>(ents + p.n_ent_total);
   unsigned* cnt_inc = reinterpret_cast<unsigned*>(eoff + A + 1);
-  unsigned* cnt_pred = cnt_inc + A;                       // [A][16]
-  uint8_t* gs2 = reinterpret_cast<uint8_t*>(cnt_pred + A * 16);  // [2][A] G per app, double-buffered by row
-  uint8_t* nl = gs2 + 2 * A;                              // [A] D'
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + p.bar_off);  // [2]
+  unsigned* cnt_pred = cnt_inc + A;                                   // [A][16]
+  uint8_t* gs2 = reinterpret_cast<uint8_t*>(cnt_pred + A * 16);      // [2 units][kAARows][A] G per app
+  uint8_t* nl = gs2 + 2 * kAARows * A;                                // [A] D'
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + p.bar_off);      // [2]
   for (int i = tid; i < p.n_ent_total; i += blockDim.x) ents[i] = __ldg(p.ctx.ent + i);
   for (int i = tid; i <= A; i += blockDim.x) eoff[i] = __ldg(p.ctx.ent_off + i);
   for (int i = tid; i < A; i += blockDim.x) { cnt_inc[i] = 0; nl[i] = __ldg(p.ctx.nlists + i); }
@@ -85,83 +105,112 @@ __global__ void __launch_bounds__(kAAWarps * 32, 1) all_apps_kernel(const AllApp
   if (tid == 0) { mbar_init1(bar); mbar_init1(bar + 1); }
   __syncthreads();
 
+  const int64_t n_units = (p.rows + kAARows - 1) / kAARows;
   const int64_t first = blockIdx.x, step = gridDim.x;
-  // G for every app from a row's ground truth (label-major category table)
-  auto build_g = [&](int64_t row, uint8_t* gs) {
-    if (row >= p.rows) return;
-    const int64_t g0 = __ldg(p.gt_off + row), g1 = __ldg(p.gt_off + row + 1);
-    for (int a = tid; a < A; a += blockDim.x) {
-      uint32_t G = 0;
-      for (int64_t t = g0; t < g1; ++t) {
-        const int32_t c = __ldg(p.gt_lab + t);
-        G |= label_lists(__ldg(p.catT + static_cast<int64_t>(c) * A + a), kApiOutput);
+  auto unit_rows = [&](int64_t u) {
+    const int64_t r0 = u * kAARows;
+    return static_cast<int>(p.rows - r0 < kAARows ? p.rows - r0 : kAARows);
+  };
+  // issue a unit's row copies (one barrier for all of them)
+  auto load_unit = [&](int64_t u, int b) {
+    const int nr = unit_rows(u);
+    mbar_expect(bar + b, p.copy_bytes * nr);
+    for (int r = 0; r < nr; ++r)
+      bulk_copy(rowbuf + (b * kAARows + r) * p.row_bytes_pad, p.logits + (u * kAARows + r) * p.ld_bytes,
+                p.copy_bytes, bar + b);
+  };
+  // G for every app from each row's ground truth (label-major category table)
+  auto build_g = [&](int64_t u, uint8_t* gs) {
+    if (u >= n_units) return;
+    const int nr = unit_rows(u);
+    for (int r = 0; r < nr; ++r) {
+      const int64_t row = u * kAARows + r;
+      const int64_t g0 = __ldg(p.gt_off + row), g1 = __ldg(p.gt_off + row + 1);
+      for (int a = tid; a < A; a += blockDim.x) {
+        uint32_t G = 0;
+        for (int64_t t = g0; t < g1; ++t) {
+          const int32_t c = __ldg(p.gt_lab + t);
+          G |= label_lists(__ldg(p.catT + static_cast<int64_t>(c) * A + a), kApiOutput);
+        }
+        gs[r * A + a] = static_cast<uint8_t>(G);
       }
-      gs[a] = static_cast<uint8_t>(G);
     }
   };
-  // prefetch the first row and its G
-  if (tid == 0 && first < p.rows) {
-    mbar_expect(bar, p.copy_bytes);
-    bulk_copy(rowbuf[0], p.logits + first * p.ld_bytes, p.copy_bytes, bar);
-  }
+  if (tid == 0 && first < n_units) load_unit(first, 0);
   build_g(first, gs2);
   __syncthreads();
   uint32_t phase[2] = {0, 0};
   int buf = 0;
-  for (int64_t row = first; row < p.rows; row += step, buf ^= 1) {
-    // next row into the other buffer (its previous row was fully consumed: barrier below),
-    // and the next row's G (its loads overlap this row's evaluation)
-    const int64_t nxt = row + step;
-    if (tid == 0 && nxt < p.rows) {
-      mbar_expect(bar + (buf ^ 1), p.copy_bytes);
-      bulk_copy(rowbuf[buf ^ 1], p.logits + nxt * p.ld_bytes, p.copy_bytes, bar + (buf ^ 1));
-    }
-    build_g(nxt, gs2 + (buf ^ 1) * A);
+  for (int64_t u = first; u < n_units; u += step, buf ^= 1) {
+    // the next unit's rows into the other buffers (consumed: barrier below), and its G
+    const int64_t nxt = u + step;
+    if (tid == 0 && nxt < n_units) load_unit(nxt, buf ^ 1);
+    build_g(nxt, gs2 + (buf ^ 1) * kAARows * A);
     mbar_wait_parity(bar + buf, phase[buf]);
     phase[buf] ^= 1u;
-    const uint8_t* rb = rowbuf[buf];
-    const uint8_t* gs = gs2 + buf * A;
-    // this warp's apps a = warp + 32 j: the split maxima of app j park in lane j, and the
-    // decision / counters run lane-parallel once per row
-    float pzp = 0.f, pzm = 0.f;
-    uint32_t pkp = kNone, pkm = kNone;
+    const int nr = unit_rows(u);
+    const uint8_t* rb = rowbuf + (buf * kAARows) * p.row_bytes_pad;
+    const uint8_t* gs = gs2 + buf * kAARows * A;
+    // this warp's apps a = warp + 32 j: app j's maxima park in lane j; the decisions and
+    // counters run lane-parallel once per unit
+    Split pk[kAARows];
     int pa = -1, j = 0;
     for (int a = warp; a < A; a += kAAWarps, ++j) {
-      const uint32_t G = gs[a];
-      float zp = -CUDART_INF_F, zm = -CUDART_INF_F;
-      uint32_t kp = kNone, km = kNone;
+      uint32_t G[kAARows];
+      Split m[kAARows];
+#pragma unroll
+      for (int r = 0; r < kAARows; ++r) {
+        G[r] = gs[r * A + a];
+        m[r] = Split{-CUDART_INF_F, -CUDART_INF_F, kNone, kNone};
+      }
       for (int e = eoff[a] + lane; e < eoff[a + 1]; e += 32) {
         const uint32_t key = ents[e];
-        const float z = p.bf16 ? __uint_as_float(static_cast<uint32_t>(
-                                     *reinterpret_cast<const uint16_t*>(rb + 2u * (key >> 8))) << 16)
-                               : *reinterpret_cast<const float*>(rb + 4u * (key >> 8));
-        if ((G >> (key & 0xFFu)) & 1u) {
-          if (z > zp) { zp = z; kp = key; }
-        } else {
-          if (z > zm) { zm = z; km = key; }
+        const uint32_t cat = key & 0xFFu;
+        float z[kAARows];
+#pragma unroll
+        for (int r = 0; r < kAARows; ++r)
+          z[r] = p.bf16 ? __uint_as_float(static_cast<uint32_t>(*reinterpret_cast<const uint16_t*>(
+                              rb + r * p.row_bytes_pad + 2u * (key >> 8))) << 16)
+                        : *reinterpret_cast<const float*>(rb + r * p.row_bytes_pad + 4u * (key >> 8));
+#pragma unroll
+        for (int r = 0; r < kAARows; ++r) {
+          if ((G[r] >> cat) & 1u) {
+            if (z[r] > m[r].zp) { m[r].zp = z[r]; m[r].kp = key; }
+          } else {
+            if (z[r] > m[r].zm) { m[r].zm = z[r]; m[r].km = key; }
+          }
         }
       }
-      argmax_warp(zp, kp);
-      argmax_warp(zm, km);
-      if (lane == (j & 31)) { pzp = zp; pkp = kp; pzm = zm; pkm = km; pa = a; }
+#pragma unroll
+      for (int r = 0; r < kAARows; ++r) {
+        if (r < nr) {  // warp-uniform
+          argmax_warp(m[r].zp, m[r].kp);
+          argmax_warp(m[r].zm, m[r].km);
+        }
+      }
+      if (lane == (j & 31)) {
+#pragma unroll
+        for (int r = 0; r < kAARows; ++r) pk[r] = m[r];
+        pa = a;
+      }
       if ((j & 31) == 31 || a + kAAWarps >= A) {  // warp-uniform: flush the parked apps
         if (pa >= 0) {
-          const uint32_t Ga = gs[pa];
           const uint32_t D = nl[pa];
-          const bool hp = pkp != kNone, hm = pkm != kNone;
-          const bool take_p = hp && (!hm || pzp > pzm || (pzp == pzm && pkp < pkm));
-          const float zs = take_p ? pzp : pzm;
-          const uint32_t ks = take_p ? pkp : pkm;
-          const uint32_t dec = ((hp || hm) && zs > p.ctx.tau) ? (ks & 0xFFu) : D;
-          const bool ok = Ga ? (dec < D && ((Ga >> dec) & 1u)) : (dec == D);
-          if (!ok) atomicAdd(cnt_inc + pa, 1u);
-          atomicAdd(cnt_pred + pa * 16 + dec, 1u);
-          if (p.decision) p.decision[row * A + pa] = static_cast<uint8_t>(dec);
+#pragma unroll
+          for (int r = 0; r < kAARows; ++r) {
+            if (r >= nr) break;
+            uint32_t dec;
+            bool ok;
+            aa_decide(pk[r], gs[r * A + pa], D, p.ctx.tau, dec, ok);
+            if (!ok) atomicAdd(cnt_inc + pa, 1u);
+            atomicAdd(cnt_pred + pa * 16 + dec, 1u);
+            if (p.decision) p.decision[(u * kAARows + r) * A + pa] = static_cast<uint8_t>(dec);
+          }
         }
         pa = -1;
       }
     }
-    __syncthreads();  // row buffer, gs and the next row's G are reused / complete
+    __syncthreads();  // row buffers, gs and the next unit's G are reused / complete
   }
   for (int i = tid; i < A; i += blockDim.x)
     if (cnt_inc[i] && p.n_incorrect) atomicAdd(p.n_incorrect + i, static_cast<unsigned long long>(cnt_inc[i]));

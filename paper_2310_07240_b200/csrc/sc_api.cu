@@ -597,11 +597,14 @@ sc_status sc_decide_all_apps(sc_context ctx, const sc_batch* b, uint64_t* n_inco
   p.hist_pred = reinterpret_cast<unsigned long long*>(hist_pred);
   p.decision = decision;
   const int64_t A = ctx->n_apps;
-  int64_t off = 2 * static_cast<int64_t>(p.row_bytes_pad) + 4 * p.n_ent_total + 4 * (A + 1) + 4 * A + 64 * A + 3 * A;
+  // [2 units x kAARows] row buffers, entries, offsets, counters, G [2 units x kAARows][A], D'
+  const int64_t ur = sc::kAllAppsRows;
+  int64_t off = 2 * ur * static_cast<int64_t>(p.row_bytes_pad) + 4 * p.n_ent_total + 4 * (A + 1) + 4 * A + 64 * A +
+                (2 * ur + 1) * A;
   p.bar_off = static_cast<int32_t>(round_up(off, 8));
   const size_t smem = static_cast<size_t>(p.bar_off + 16);
   if (smem > kSmemMax) return fail(SC_ERR_UNSUPPORTED, "contexts too large for the all-apps pass (shared memory)");
-  const int grid = static_cast<int>(std::min<int64_t>(b->rows, di.sms));
+  const int grid = static_cast<int>(std::min<int64_t>((b->rows + ur - 1) / ur, di.sms));  // kAARows-row units
   if (cudaError_t e = sc::launch_all_apps(p, grid, smem, static_cast<cudaStream_t>(stream)))
     return cuda_fail(e, "all-apps kernel launch");
   g_launches.fetch_add(1, std::memory_order_relaxed);

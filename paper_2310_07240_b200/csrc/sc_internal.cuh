@@ -120,6 +120,7 @@ struct AllAppsParams {
   unsigned long long* hist_pred;
   uint8_t* decision;        // [rows][n_apps] or NULL
 };
+constexpr int kAllAppsRows = 4;  // rows per barrier interval of the all-apps kernel
 cudaError_t launch_all_apps(const AllAppsParams& p, int grid, size_t smem, cudaStream_t st);
 
 // Launchers (sc_kernels.cu).  Return cudaError_t of the launch.

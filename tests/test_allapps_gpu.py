@@ -9,7 +9,7 @@ from conftest import gpu_available
 pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device")]
 
 
-@pytest.mark.parametrize("dtype,rows", [("f32", 600), ("bf16", 301)])
+@pytest.mark.parametrize("dtype,rows", [("f32", 600), ("bf16", 301), ("f32", 603)])  # 4-row units, ragged tails
 def test_all_apps_parity(dtype, rows):
     import torch
     import paper_2310_07240_b200 as sc
