@@ -657,6 +657,8 @@ def run_e2e(args, ev, data, global_rows, dev, barrier, world):
     del h_logits
     return {"value": global_rows * args.e2e_steps / dt, "unit": "samples/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "steps": args.e2e_steps,
+            "h2d_gbs_per_gpu": round(h2d * args.e2e_steps / dt / 1e9, 2),  # PCIe-bound: the step moves 4.2 GB host->device
+            "bound": "pcie (host->device copy of the step's logits)",
             "api": "Evaluator.step_host (pinned host inputs -> chunked H2D overlapped with sc_loss_fwd_bwd -> D2H)"}
 
 
