@@ -102,3 +102,35 @@ def test_patterns_slot_layouts(order, sizes, shared, monkeypatch):
     if order == MULTI_SELECT:
         want = "tma_ring_lists" if n_slots <= 8 else "gather_lists"
         assert sc.sc_last_kernel().startswith(want), (sc.sc_last_kernel(), n_slots)
+
+
+@pytest.mark.parametrize("order", [0, APP_CHOICE, MULTI_SELECT])
+@pytest.mark.parametrize("cfg,dtype,rows", [(2, "f32", 3000), (2, "bf16", 2001), (4, "f32", 1500)])
+def test_decide_only_all_patterns(order, cfg, dtype, rows, kernel):
+    """sc_decide (no loss): decisions and counters of every pattern on both kernels, with the
+    ground truth as CSR (G built in the pass) — the epilogues' want_loss = 0 branch."""
+    import torch
+    import paper_2310_07240_b200 as sc
+    import synth
+    from oracle import Oracle
+    spec = synth.config_context(cfg)
+    wl = synth.Workload(spec, seed=cfg, dtype=dtype)
+    b = wl.host_batch((1 << 18) - 500 if cfg == 4 else 99, rows)
+    d = to_dev(b, dtype)
+    multi = spec.n_apps > 1
+    ctx = sc.Context(spec.C, spec.lists, spec.tau, spec.k, order=order, multi_app=True)
+    na = spec.n_apps
+    dec = torch.full((rows,), 77, dtype=torch.uint8, device="cuda")
+    ni = torch.zeros(na, dtype=torch.int64, device="cuda")
+    hp = torch.zeros(na * 256, dtype=torch.int64, device="cuda")
+    hg = torch.zeros(na * 256, dtype=torch.int64, device="cuda")
+    sc.sc_decide(ctx, sc.Batch(logits=d["logits"], gt_off=d["gt_off"], gt_lab=d["gt_lab"],
+                               app=d.get("app") if multi else None),
+                 decision=dec, n_incorrect=ni, hist_pred=hp, hist_gt=hg)
+    torch.cuda.synchronize()
+    ref = Oracle.from_spec(spec, order).eval(b["logits"], b["gt_off"], b["gt_lab"], app=b["app"] if multi else None,
+                                             want_loss=False)
+    np.testing.assert_array_equal(dec.cpu().numpy(), ref["decision"])
+    np.testing.assert_array_equal(ni.cpu().numpy().astype(np.uint64), ref["n_incorrect"])
+    np.testing.assert_array_equal(hp.cpu().numpy().astype(np.uint64), ref["hist_pred"])
+    np.testing.assert_array_equal(hg.cpu().numpy().astype(np.uint64), ref["hist_gt"])
