@@ -1196,11 +1196,11 @@ cudaError_t launch_eval(const EvalParams& p, int epl, int pat, int grid, size_t 
 
 template <int EPL, int G, bool BF16, int PAT>
 static cudaError_t launch_gather_t(const EvalParams& p, int sms, cudaStream_t st) {
-  static int blocks_per_sm = 0;
-  if (blocks_per_sm == 0) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, gather_kernel<EPL, G, BF16, PAT>, 256, 0);
-    if (blocks_per_sm < 1) blocks_per_sm = 1;
-  }
+  static const int blocks_per_sm = [] {  // thread-safe one-time occupancy query
+    int n = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, gather_kernel<EPL, G, BF16, PAT>, 256, 0);
+    return n < 1 ? 1 : n;
+  }();
   const int64_t warps_needed = (p.rows + G - 1) / G;
   int64_t grid = static_cast<int64_t>(sms) * blocks_per_sm;
   const int64_t max_grid = (warps_needed + 7) / 8;
@@ -1235,12 +1235,10 @@ cudaError_t launch_hist(const HistParams& p, int grid, size_t smem, cudaStream_t
 cudaError_t launch_hist_rows(const HistParams& p, int grid, cudaStream_t st) {
   const size_t smem = 256 * 8 + static_cast<size_t>(p.ctx.C);
   if (smem > 48 * 1024) {
-    static bool attr = false;
-    if (!attr) {
-      if (cudaError_t e = cudaFuncSetAttribute(hist_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024))
-        return e;
-      attr = true;
-    }
+    // thread-safe one-time opt-in to large dynamic shared memory (C > ~46K labels)
+    static const cudaError_t attr =
+        cudaFuncSetAttribute(hist_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (attr) return attr;
   }
   hist_rows_kernel<<<grid, 256, smem, st>>>(p);
   return cudaGetLastError();
