@@ -60,17 +60,17 @@ __device__ __forceinline__ uint32_t pack4(int a, int b, int c, int d) {
 //     0-3 / 4-7), reduced over the warp at the end — one shift and add per row;
 //   <= 32 (SMALL): lane j of each warp owns bin j and adds the popcount of the warp's ballot;
 //   more: match + shared atomics.
+__device__ __forceinline__ void count_packed(bool act, int v, unsigned long long (&pk)[2]) {
+  if (act) {
+    const unsigned long long inc = 1ull << (16 * (v & 3));
+    if (v < 4) pk[0] += inc;
+    else pk[1] += inc;
+  }
+}
+
 template <bool SMALL>
 __device__ __forceinline__ void count_bins(int nb, bool act, int v, int lane, unsigned long long& mine,
-                                           unsigned long long* h_s, bool packed, unsigned long long (&pk)[2]) {
-  if (packed) {  // uniform
-    if (act) {
-      const unsigned long long inc = 1ull << (16 * (v & 3));
-      if (v < 4) pk[0] += inc;
-      else pk[1] += inc;
-    }
-    return;
-  }
+                                           unsigned long long* h_s) {
   if constexpr (SMALL) {
     for (int j = 0; j < nb; ++j) {  // nb is uniform
       const unsigned c = __popc(__ballot_sync(kFull, act && v == j));
@@ -117,14 +117,16 @@ __global__ void __launch_bounds__(256) ranges_hist_kernel(const float* lo_g, con
     const int64_t i0 = it * stride + (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * kV;
     float sv[kV];
     int r[kV];
-    if (vec && i0 + kV <= rows) {
+    // rows of this pass held by the thread (32-bit: one compare per row below)
+    const int nv = i0 >= rows ? 0 : (rows - i0 < kV ? static_cast<int>(rows - i0) : kV);
+    if (vec && nv == kV) {
       const float4 f = __ldg(reinterpret_cast<const float4*>(gt_score + i0));
       const float4 f2 = __ldg(reinterpret_cast<const float4*>(gt_score + i0 + 4));
       sv[0] = f.x; sv[1] = f.y; sv[2] = f.z; sv[3] = f.w;
       sv[4] = f2.x; sv[5] = f2.y; sv[6] = f2.z; sv[7] = f2.w;
     } else {
 #pragma unroll
-      for (int q = 0; q < kV; ++q) sv[q] = i0 + q < rows ? __ldg(gt_score + i0 + q) : 0.f;
+      for (int q = 0; q < kV; ++q) sv[q] = q < nv ? __ldg(gt_score + i0 + q) : 0.f;
     }
 #pragma unroll
     for (int q = 0; q < kV; ++q) r[q] = m;
@@ -135,17 +137,22 @@ __global__ void __launch_bounds__(256) ranges_hist_kernel(const float* lo_g, con
         if (sv[q] >= l && sv[q] <= u) r[q] = j;
     }
     if (gt_range) {
-      if (vec && i0 + kV <= rows) {
+      if (vec && nv == kV) {
         *reinterpret_cast<uint2*>(gt_range + i0) = make_uint2(pack4(r[0], r[1], r[2], r[3]), pack4(r[4], r[5], r[6], r[7]));
       } else {
 #pragma unroll
         for (int q = 0; q < kV; ++q)
-          if (i0 + q < rows) gt_range[i0 + q] = static_cast<uint8_t>(r[q]);
+          if (q < nv) gt_range[i0 + q] = static_cast<uint8_t>(r[q]);
       }
     }
     if (hist) {
+      if (packed) {
 #pragma unroll
-      for (int q = 0; q < kV; ++q) count_bins<SMALL>(m + 1, i0 + q < rows, r[q], lane, mine, h, packed, pk);
+        for (int q = 0; q < kV; ++q) count_packed(q < nv, r[q], pk);
+      } else {
+#pragma unroll
+        for (int q = 0; q < kV; ++q) count_bins<SMALL>(m + 1, q < nv, r[q], lane, mine, h);
+      }
     }
   }
   if (packed && hist) flush_packed(pk, lane, mine);
@@ -196,7 +203,8 @@ __global__ void __launch_bounds__(256) ranges_loss_kernel(const float* lo_g, con
   unsigned long long pk[2] = {0ull, 0ull};
   for (int64_t it = 0; it < iters; ++it) {
     const int64_t i0 = it * stride + (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * kV;
-    const bool full = vec && i0 + kV <= rows;
+    const int nv = i0 >= rows ? 0 : (rows - i0 < kV ? static_cast<int>(rows - i0) : kV);
+    const bool full = vec && nv == kV;
     float sv[kV];
     int r[kV], d[kV];
     if (full) {
@@ -213,8 +221,8 @@ __global__ void __launch_bounds__(256) ranges_loss_kernel(const float* lo_g, con
     } else {
 #pragma unroll
       for (int q = 0; q < kV; ++q) {
-        sv[q] = i0 + q < rows ? __ldg(score + i0 + q) : 0.f;
-        r[q] = i0 + q < rows ? __ldg(gt_range + i0 + q) : m;
+        sv[q] = q < nv ? __ldg(score + i0 + q) : 0.f;
+        r[q] = q < nv ? __ldg(gt_range + i0 + q) : m;
       }
     }
 #pragma unroll
@@ -226,9 +234,10 @@ __global__ void __launch_bounds__(256) ranges_loss_kernel(const float* lo_g, con
         if (sv[q] >= l && sv[q] <= u) d[q] = j;
     }
     float L[kV], g[kV];
+    float part = 0.f;  // this pass's 8 losses in fp32, then one fp64 add (rel. error ~5e-7)
 #pragma unroll
     for (int q = 0; q < kV; ++q) {
-      const bool act = i0 + q < rows;
+      const bool act = q < nv;
       L[q] = 0.f;
       g[q] = 0.f;
       if (act && r[q] < m) {
@@ -239,9 +248,10 @@ __global__ void __launch_bounds__(256) ranges_loss_kernel(const float* lo_g, con
         L[q] = ws[r[q]] * (sa + sb);
         g[q] = ws[r[q]] * k * (db - da) * grad_scale;
       }
-      my_loss += L[q];
+      part += L[q];
       my_inc += (act && d[q] != r[q]) ? 1u : 0u;
     }
+    my_loss += static_cast<double>(part);
     if (full) {
       if (decision)
         *reinterpret_cast<uint2*>(decision + i0) = make_uint2(pack4(d[0], d[1], d[2], d[3]), pack4(d[4], d[5], d[6], d[7]));
@@ -256,15 +266,20 @@ __global__ void __launch_bounds__(256) ranges_loss_kernel(const float* lo_g, con
     } else {
 #pragma unroll
       for (int q = 0; q < kV; ++q) {
-        if (i0 + q >= rows) continue;
+        if (q >= nv) continue;
         if (decision) decision[i0 + q] = static_cast<uint8_t>(d[q]);
         if (loss_row) loss_row[i0 + q] = L[q];
         if (grad) grad[i0 + q] = g[q];
       }
     }
     if (hist_pred) {
+      if (packed) {
 #pragma unroll
-      for (int q = 0; q < kV; ++q) count_bins<SMALL>(m + 1, i0 + q < rows, d[q], lane, mine, hp, packed, pk);
+        for (int q = 0; q < kV; ++q) count_packed(q < nv, d[q], pk);
+      } else {
+#pragma unroll
+        for (int q = 0; q < kV; ++q) count_bins<SMALL>(m + 1, q < nv, d[q], lane, mine, hp);
+      }
     }
   }
   if (packed && hist_pred) flush_packed(pk, lane, mine);
