@@ -22,6 +22,7 @@ struct sc_ranges_s {
   float* d_lo = nullptr;  // [m]
   float* d_hi = nullptr;  // [m]
   int device = 0;
+  int sorted = 0;         // lo[j] < lo[j+1] and hi[j] <= lo[j+1] for all j (see range_lookup)
 };
 
 namespace {
@@ -53,6 +54,43 @@ constexpr int kV = 8;
 __device__ __forceinline__ uint32_t pack4(int a, int b, int c, int d) {
   return static_cast<uint32_t>(a) | static_cast<uint32_t>(b) << 8 | static_cast<uint32_t>(c) << 16 |
          static_cast<uint32_t>(d) << 24;
+}
+
+// The range each of kV scores lies in: the first containing range in code order (reading
+// A22), else m.  sorted (lo strictly ascending, hi[j] <= lo[j+1]: ranges in code order that
+// at most touch): the last range whose lo <= s, found by a branch-free binary search
+// (ceil(log2 m) steps, the same trip count in every lane), or the one before it when s
+// sits on their shared bound; otherwise a scan of every range.
+template <int V>
+__device__ __forceinline__ void range_lookup(const float (&sv)[V], int (&r)[V], const float* lo, const float* hi,
+                                             int m, bool sorted) {
+  if (sorted) {
+    int base[V];
+#pragma unroll
+    for (int q = 0; q < V; ++q) base[q] = 0;
+    for (int n = m; n > 1;) {  // uniform
+      const int half = n >> 1;
+#pragma unroll
+      for (int q = 0; q < V; ++q) base[q] = lo[base[q] + half] <= sv[q] ? base[q] + half : base[q];
+      n -= half;
+    }
+#pragma unroll
+    for (int q = 0; q < V; ++q) {
+      int b = base[q];  // the last range with lo[b] <= s (when s >= lo[0])
+      // ranges may touch (hi[b-1] == lo[b]): a score on the shared bound is in b-1 first
+      if (b > 0 && sv[q] <= hi[b - 1]) b -= 1;
+      r[q] = (lo[b] <= sv[q] && sv[q] <= hi[b]) ? b : m;
+    }
+    return;
+  }
+#pragma unroll
+  for (int q = 0; q < V; ++q) r[q] = m;
+  for (int j = m - 1; j >= 0; --j) {
+    const float l = lo[j], u = hi[j];
+#pragma unroll
+    for (int q = 0; q < V; ++q)
+      if (sv[q] >= l && sv[q] <= u) r[q] = j;
+  }
 }
 
 // Histogram counters, by number of bins:
@@ -97,7 +135,7 @@ __device__ __forceinline__ void flush_packed(const unsigned long long (&pk)[2], 
 }
 
 template <bool SMALL>
-__global__ void __launch_bounds__(256) ranges_hist_kernel(const float* lo_g, const float* hi_g, int m,
+__global__ void __launch_bounds__(256) ranges_hist_kernel(const float* lo_g, const float* hi_g, int m, int sorted,
                                                          const float* gt_score, int64_t rows,
                                                          unsigned long long* hist, uint8_t* gt_range) {
   __shared__ float lo[kMaxRanges], hi[kMaxRanges];
@@ -128,14 +166,7 @@ __global__ void __launch_bounds__(256) ranges_hist_kernel(const float* lo_g, con
 #pragma unroll
       for (int q = 0; q < kV; ++q) sv[q] = q < nv ? __ldg(gt_score + i0 + q) : 0.f;
     }
-#pragma unroll
-    for (int q = 0; q < kV; ++q) r[q] = m;
-    for (int j = m - 1; j >= 0; --j) {  // the first containing range in code order
-      const float l = lo[j], u = hi[j];
-#pragma unroll
-      for (int q = 0; q < kV; ++q)
-        if (sv[q] >= l && sv[q] <= u) r[q] = j;
-    }
+    range_lookup<kV>(sv, r, lo, hi, m, sorted);  // the first containing range in code order
     if (gt_range) {
       if (vec && nv == kV) {
         *reinterpret_cast<uint2*>(gt_range + i0) = make_uint2(pack4(r[0], r[1], r[2], r[3]), pack4(r[4], r[5], r[6], r[7]));
@@ -176,7 +207,7 @@ __global__ void ranges_weights_kernel(const unsigned long long* hist, int m, flo
 }
 
 template <bool SMALL>
-__global__ void __launch_bounds__(256) ranges_loss_kernel(const float* lo_g, const float* hi_g, int m, float k,
+__global__ void __launch_bounds__(256) ranges_loss_kernel(const float* lo_g, const float* hi_g, int m, int sorted, float k,
                                                          const float* score, const uint8_t* gt_range, int64_t rows,
                                                          const float* w, float grad_scale, double* loss_sum,
                                                          float* loss_row, float* grad, uint8_t* decision,
@@ -225,14 +256,7 @@ __global__ void __launch_bounds__(256) ranges_loss_kernel(const float* lo_g, con
         r[q] = q < nv ? __ldg(gt_range + i0 + q) : m;
       }
     }
-#pragma unroll
-    for (int q = 0; q < kV; ++q) d[q] = m;
-    for (int j = m - 1; j >= 0; --j) {  // Decision(API(x)): the first containing range in code order
-      const float l = lo[j], u = hi[j];
-#pragma unroll
-      for (int q = 0; q < kV; ++q)
-        if (sv[q] >= l && sv[q] <= u) d[q] = j;
-    }
+    range_lookup<kV>(sv, d, lo, hi, m, sorted);  // Decision(API(x)): the first containing range in code order
     float L[kV], g[kV];
     float part = 0.f;  // this pass's 8 losses in fp32, then one fp64 add (rel. error ~5e-7)
 #pragma unroll
@@ -331,6 +355,12 @@ sc_status sc_ranges_load(int32_t m, const float* lo, const float* hi, float k, s
   auto* r = new sc_ranges_s();
   r->m = m;
   r->k = k;
+  // binary-search lookup only pays for many ranges: a scan loads each bound once for all
+  // of a thread's rows, the search needs a dependent shared-memory load per row and step
+  // (B200, 7 ranges: 0.460 ms either way; the hist kernel is ALU-bound at ~65 instr/row)
+  r->sorted = m > 16 ? 1 : 0;
+  for (int j = 0; j + 1 < m; ++j)
+    if (!(lo[j] < lo[j + 1] && hi[j] <= lo[j + 1])) r->sorted = 0;
   cudaError_t e = cudaGetDevice(&r->device);
   if (!e) e = cudaMalloc(&r->d_lo, m * sizeof(float));
   if (!e) e = cudaMalloc(&r->d_hi, m * sizeof(float));
@@ -362,7 +392,7 @@ sc_status sc_ranges_hist(sc_ranges r, const float* gt_score, int64_t rows, uint6
   if (!gt_score) return rfail(SC_ERR_INVALID_ARG, "gt_score is NULL");
   auto kern = r->m + 1 <= 32 ? ranges_hist_kernel<true> : ranges_hist_kernel<false>;
   kern<<<grid_for(rows), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      r->d_lo, r->d_hi, r->m, gt_score, rows, reinterpret_cast<unsigned long long*>(hist_gt), gt_range_out);
+      r->d_lo, r->d_hi, r->m, r->sorted, gt_score, rows, reinterpret_cast<unsigned long long*>(hist_gt), gt_range_out);
   if (cudaError_t e = cudaGetLastError()) return rfail(SC_ERR_CUDA, cudaGetErrorString(e));
   return SC_OK;
 }
@@ -384,7 +414,7 @@ sc_status sc_ranges_loss_fwd_bwd(sc_ranges r, const float* score, const uint8_t*
   if (!score || !gt_range) return rfail(SC_ERR_INVALID_ARG, "score / gt_range is NULL");
   auto kern = r->m + 1 <= 32 ? ranges_loss_kernel<true> : ranges_loss_kernel<false>;
   kern<<<grid_for(rows), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      r->d_lo, r->d_hi, r->m, r->k, score, gt_range, rows, w, grad_scale, loss_sum, loss_row, grad, decision,
+      r->d_lo, r->d_hi, r->m, r->sorted, r->k, score, gt_range, rows, w, grad_scale, loss_sum, loss_row, grad, decision,
       reinterpret_cast<unsigned long long*>(n_incorrect), reinterpret_cast<unsigned long long*>(hist_pred));
   if (cudaError_t e = cudaGetLastError()) return rfail(SC_ERR_CUDA, cudaGetErrorString(e));
   return SC_OK;

@@ -7,16 +7,20 @@ from conftest import gpu_available
 pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device")]
 
 
-@pytest.mark.parametrize("m,rows,off", [(1, 1, 0), (3, 100003, 0), (7, 5000, 0), (7, 5000, 1), (20, 70001, 0),
-                                        (40, 20000, 0), (40, 20000, 3)])  # 2-8 bins packed, 21 ballot, 41 match;
-def test_ranges_parity(m, rows, off):                                     # off: unaligned (scalar) accesses
+@pytest.mark.parametrize("m,rows,off,overlap", [(1, 1, 0, False), (3, 100003, 0, False), (7, 5000, 0, True),
+                                                (7, 5000, 1, True), (7, 30001, 0, False), (20, 70001, 0, True),
+                                                (20, 70001, 0, False), (40, 20000, 0, True), (40, 20000, 3, False),
+                                                (200, 9000, 0, False)])
+def test_ranges_parity(m, rows, off, overlap):
+    # 2-8 bins: packed counters, 21: ballot, 41: match; off: unaligned (scalar) accesses;
+    # overlap False: ranges in ascending order that touch (binary-search lookup when m > 16)
     import torch
     import paper_2310_07240_b200 as sc
     from oracle import RangesOracle
     rng = np.random.default_rng(m * 1000 + rows)
     edges = np.sort(rng.uniform(-1, 1, size=m + 1)).astype(np.float32)
     lo, hi = edges[:-1].copy(), edges[1:].copy()
-    if m > 3:  # overlapping ranges too: the first containing range wins
+    if overlap:  # overlapping ranges: the first containing range wins
         hi[1] = np.float32(min(1.0, hi[1] + 0.2))
     k = 10.0
     score = rng.uniform(-1.2, 1.2, rows).astype(np.float32)
