@@ -10,22 +10,36 @@ pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not gpu_available(), reason="n
 @pytest.mark.parametrize("m,rows,off,overlap", [(1, 1, 0, False), (3, 100003, 0, False), (7, 5000, 0, True),
                                                 (7, 5000, 1, True), (7, 30001, 0, False), (20, 70001, 0, True),
                                                 (20, 70001, 0, False), (40, 20000, 0, True), (40, 20000, 3, False),
-                                                (200, 9000, 0, False)])
+                                                (200, 9000, 0, False), (7, 30001, 0, "gaps"), (7, 30001, 0, "cluster"),
+                                                (200, 9000, 0, "cluster"), (1, 5000, 0, "point")])
 def test_ranges_parity(m, rows, off, overlap):
     # 2-8 bins: packed counters, 21: ballot, 41: match; off: unaligned (scalar) accesses;
-    # overlap False: ranges in ascending order that touch (binary-search lookup when m > 16)
+    # overlap False: ranges in ascending order that touch (binary-search lookup when m > 16);
+    # "gaps": ascending ranges with holes between them; "cluster": most bounds packed into
+    # [0, 1e-3]; "point": one degenerate range lo == hi
     import torch
     import paper_2310_07240_b200 as sc
     from oracle import RangesOracle
     rng = np.random.default_rng(m * 1000 + rows)
     edges = np.sort(rng.uniform(-1, 1, size=m + 1)).astype(np.float32)
     lo, hi = edges[:-1].copy(), edges[1:].copy()
-    if overlap:  # overlapping ranges: the first containing range wins
+    if overlap is True:  # overlapping ranges: the first containing range wins
         hi[1] = np.float32(min(1.0, hi[1] + 0.2))
+    elif overlap == "gaps":  # hi[j] < lo[j+1]
+        hi = (lo + np.float32(0.6) * (hi - lo)).astype(np.float32)
+    elif overlap == "cluster":  # m - 1 tiny touching ranges in [0, 1e-3], then one up to 1
+        edges = np.concatenate([np.sort(rng.uniform(0, 1e-3, size=m)), [1.0]]).astype(np.float32)
+        lo, hi = edges[:-1].copy(), edges[1:].copy()
+    elif overlap == "point":
+        lo = hi = np.array([0.25], dtype=np.float32)
     k = 10.0
     score = rng.uniform(-1.2, 1.2, rows).astype(np.float32)
     score[: rows // 10] = lo[rng.integers(0, m, rows // 10)]  # exactly on a bound
+    score[rows // 10: rows // 5] = hi[rng.integers(0, m, rows // 5 - rows // 10)]
+    if overlap == "cluster":
+        score[rows // 5: rows // 2] = rng.uniform(-1e-4, 1.1e-3, rows // 2 - rows // 5).astype(np.float32)
     gt = rng.uniform(-1.2, 1.2, rows).astype(np.float32)
+    gt[: rows // 2] = rng.permutation(score[: rows // 2])  # GT on bounds / inside the clusters as well
     orc = RangesOracle(lo.astype(np.float64), hi.astype(np.float64), k)
     pre = orc.eval(score, gt)
     w_ref = orc.weights(pre["hist_gt"])
