@@ -39,6 +39,32 @@ MUTATIONS = [
     ("sampler: position from u1", "int64_t pos = (int64_t)floor(u2[i] * (double)c);", "int64_t pos = (int64_t)floor(u1[i] * (double)c);"),
     ("multi-select: shared label first list only", "if (x->list_labels[t] == c) { m |= 1u << j; break; }",
      "if (x->list_labels[t] == c) { m |= 1u << j; return m; }"),
+    # batch drivers (orc_eval / orc_gt_hist / orc_ranges_eval), pinned by tests/test_oracle_batch.py
+    ("eval: n_incorrect counts correct rows", "if (n_incorrect) n_incorrect[a] += (uint64_t)!ok;",
+     "if (n_incorrect) n_incorrect[a] += (uint64_t)ok;"),
+    ("eval: hist_pred ignores the app", "if (hist_pred) hist_pred[(int64_t)a * 256 + d] += 1;",
+     "if (hist_pred) hist_pred[d] += 1;"),
+    ("eval: grad_scale dropped", "if (grad_val) grad_val[S_ * i + q] = gs[q] * grad_scale;",
+     "if (grad_val) grad_val[S_ * i + q] = gs[q];"),
+    ("eval: loss_row = ell", "if (loss_sum) loss_sum[a] += L;\n      if (loss_row) loss_row[i] = L;",
+     "if (loss_sum) loss_sum[a] += L;\n      if (loss_row) loss_row[i] = ell;"),
+    ("eval: loss_sum += ell", "if (loss_sum) loss_sum[a] += L;", "if (loss_sum) loss_sum[a] += ell;"),
+    ("eval: gradient slots swapped", "orc_loss_row(x, ca, z, G, wi, &ell, &L, &cs[0], &gs[0], &cs[1], &gs[1]);",
+     "orc_loss_row(x, ca, z, G, wi, &ell, &L, &cs[1], &gs[1], &cs[0], &gs[0]);"),
+    ("eval: weight of app 0", "const double wi = w ? w[(int64_t)a * 256 + G] : 1.0;", "const double wi = w ? w[G] : 1.0;"),
+    ("eval: ld ignored", "z[c] = load_z(logits, dtype, i * ld + c);", "z[c] = load_z(logits, dtype, i * C + c);"),
+    ("eval: hist_gt by decision", "if (hist_gt) hist_gt[(int64_t)a * 256 + G] += 1;\n    if (loss_sum ||",
+     "if (hist_gt) hist_gt[(int64_t)a * 256 + d] += 1;\n    if (loss_sum ||"),
+    ("eval: bf16 widened wrong", "uint32_t u = (uint32_t)((const uint16_t*)logits)[idx] << 16;",
+     "uint32_t u = (uint32_t)((const uint16_t*)logits)[idx] << 15;"),
+    ("gt_hist: Multi-Select uses the compiled map", "const uint32_t G = x->order == 2 ? orc_gt_set_raw",
+     "const uint32_t G = x->order == 9 ? orc_gt_set_raw"),
+    ("ranges: hist_gt by decision", "if (hist_gt) hist_gt[r] += 1;", "if (hist_gt) hist_gt[d] += 1;"),
+    ("ranges: n_incorrect inverted", "if (n_incorrect) n_incorrect[0] += (uint64_t)(d != r);",
+     "if (n_incorrect) n_incorrect[0] += (uint64_t)(d == r);"),
+    ("ranges: weight by decision", "(double)score[i], w ? w[r] : 1.0, &L, &dL);", "(double)score[i], w ? w[d] : 1.0, &L, &dL);"),
+    ("ranges: grad_scale dropped", "if (grad) grad[i] = dL * grad_scale;", "if (grad) grad[i] = dL;"),
+    ("ranges: loss_row holds dL", "if (loss_row) loss_row[i] = L;\n    if (grad)", "if (loss_row) loss_row[i] = dL;\n    if (grad)"),
 ]
 
 
@@ -56,7 +82,7 @@ def main():
                                 "tests/test_oracle_paper.py", "tests/test_oracle_bruteforce.py",
                                 "tests/test_oracle_loss.py", "tests/test_oracle_weights.py",
                                 "tests/test_oracle_patterns.py", "tests/test_oracle_ranges.py",
-                                "tests/test_oracle_sampler.py"],
+                                "tests/test_oracle_sampler.py", "tests/test_oracle_batch.py"],
                                cwd=ROOT, env=env, capture_output=True, text=True)
             killed = r.returncode != 0
             print(f"{'KILLED ' if killed else 'SURVIVED'}  {name}")
