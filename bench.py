@@ -34,7 +34,8 @@ ROWS_PER_GPU = 1 << 20
 
 def parse():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--gpus", type=int, default=None,
+                    help="ranks (GPUs); without torchrun, N > 1 re-launches this script under torch.distributed.run")
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -282,6 +283,11 @@ def run_ours(args):
     share = os.environ.get("SC_BENCH_SHARE_GPU") == "1"
     if share:
         local = 0
+    elif torch.cuda.device_count() < world:
+        print(json.dumps({"error": f"{world} ranks but {torch.cuda.device_count()} visible GPUs "
+                                   "(SC_BENCH_SHARE_GPU=1 runs every rank on cuda:0 over gloo)"}),
+              file=sys.stderr, flush=True)
+        return 2
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     group = None
@@ -662,8 +668,41 @@ def run_e2e(args, ev, data, global_rows, dev, barrier, world):
             "api": "Evaluator.step_host (pinned host inputs -> chunked H2D overlapped with sc_loss_fwd_bwd -> D2H)"}
 
 
+def _free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def launch_ranks(args):
+    """--gpus N: the run must have exactly N ranks.  Under torchrun WORLD_SIZE must equal N;
+    without it, N > 1 re-executes this command under torch.distributed.run (one process per
+    GPU, 127.0.0.1 rendezvous) and returns its exit code.  None = carry on in this process."""
+    if "WORLD_SIZE" in os.environ:
+        world = int(os.environ["WORLD_SIZE"])
+        if args.gpus is not None and args.gpus != world:
+            print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world}"}), file=sys.stderr, flush=True)
+            return 2
+        args.gpus = world
+        return None
+    if args.gpus is None:
+        args.gpus = 1
+    if args.gpus <= 1 or args.impl == "reference":
+        return None  # the reference arm runs on rank 0 only: no ranks to launch
+    import subprocess
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    rc = launch_ranks(args)
+    if rc is not None:
+        return rc
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

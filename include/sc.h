@@ -97,6 +97,25 @@ sc_status sc_context_load(int32_t C, int32_t n_apps, const int32_t* n_lists, con
                           const int32_t* list_labels, float tau, float k, sc_order order,
                           sc_context* out);
 
+/* sc_context_load_compact — the same context for COLUMN-COMPACTED logit rows (SURVEY.md
+ * §8(f)3, sparse contexts such as the OpenImages-shaped one: "applications
+ * heavily cluster on a small subset of labels").  Unmapped labels never affect a decision,
+ * a count or the loss, and their gradient is exactly 0 (Eq. api_output), so a
+ * producer that emits only the mapped columns (e.g. a classifier head restricted to those
+ * rows of W) hands over everything the path needs.  Batch rows then hold n_cols columns:
+ * column j is the logit of label cols[j], the union of the applications' mapped labels in
+ * ascending order (sc_context_columns); sc_batch.ld >= n_cols.  Ground truth (gt_off/gt_lab)
+ * stays in label ids [0, C).  Decisions, counters, loss and sparse gradient indices (label
+ * ids) are those of sc_context_load on the dense rows; grad_dense is laid out like the
+ * compacted rows.  Not accepted by sc_decide_all_apps (dense rows only). */
+sc_status sc_context_load_compact(int32_t C, int32_t n_apps, const int32_t* n_lists, const int64_t* list_off,
+                                  const int32_t* list_labels, float tau, float k, sc_order order,
+                                  sc_context* out);
+
+/* sc_context_columns — the logit columns a batch row of this context holds: *n_cols (C for
+ * a dense context) and, if cols != NULL (host [n_cols]), the label of each column. */
+sc_status sc_context_columns(sc_context ctx, int32_t* cols, int32_t* n_cols);
+
 /* sc_context_free — release the context's device tables (synchronises the device). NULL is a no-op. */
 sc_status sc_context_free(sc_context ctx);
 
@@ -114,11 +133,10 @@ sc_status sc_context_order(sc_context ctx, sc_order* order, int32_t* grad_slots)
  *   gt_off   [rows+1] int64 CSR offsets into gt_lab (any base, non-decreasing) —
  *   gt_lab   ... the ground-truth label ids ŷ_i of row i, in [0,C), duplicates allowed.
  *   gt_mask  [rows] uint8, optional: the precomputed G_i of each row, as written by
- *            sc_decision_hist.  When non-NULL it replaces gt_off/gt_lab.
- *            Bytes up to the next 16-B boundary past either end may be read (never
- *            crossing a page; contents ignored).
+ *            sc_decision_hist.  When non-NULL it replaces gt_off/gt_lab.  Any alignment;
+ *            only bytes of rows [0, rows) are read.
  *   app      [rows] uint16 application ids < n_apps, or NULL (every row is app 0);
- *            same 16-B-boundary over-read note as gt_mask.
+ *            2-B aligned; only rows [0, rows) are read.
  * A batch "has GT" iff gt_mask != NULL or gt_off != NULL. */
 typedef struct {
   const void*     logits;
@@ -155,7 +173,9 @@ sc_status sc_decision_hist(sc_context ctx, const sc_batch* batch, uint64_t* hist
 /* sc_decision_hist_weights — sc_decision_hist followed, in the same launch, by
  * sc_weights_from_hist on the histogram it produced (the last CTA to finish computes
  * w).  For a batch that is the whole dataset (one GPU): hist_gt must be zero on entry.
- * Calls sharing a context must not run concurrently (one completion counter per context).
+ * Safe across streams and host threads: the context keeps one completion counter per
+ * stream that has called it (64 preallocated; beyond that the call falls back to two
+ * launches, hist then weights, with identical results).  rows == 0: only w is computed.
  *   w  device [n_apps*256] float, overwritten. */
 sc_status sc_decision_hist_weights(sc_context ctx, const sc_batch* batch, uint64_t* hist_gt, uint8_t* gt_mask_out,
                                    float* w, sc_stream stream);
@@ -194,7 +214,12 @@ sc_status sc_weights_from_hist(sc_context ctx, const uint64_t* hist_gt, float* w
  *   grad_dense  [rows*ld] float: the full gradient (zeros + at most 2 entries),
  *               every element written, including the padding columns.
  *   decision, n_incorrect, hist_pred, hist_gt: as in sc_decide (same pass).
- * Needs GT.  Computes in fp32, accumulates loss_sum in fp64. */
+ * Needs GT.  Computes in fp32, accumulates loss_sum in fp64.
+ * Accuracy (the parity bar): decisions / counters / indices exact; loss_row
+ * and each gradient entry within 1e-5 of the fp64 value relative to max(|value|, 1e-30) —
+ * below 1e-30 the bound is absolute (σ'(z) of |z| > ~87 is subnormal in fp32, SURVEY.md
+ * §8(c)9).  Holds for k·|S argument| <= ~40 (k <= 40 with probabilities as arguments);
+ * larger k amplifies the fp32 rounding of the argument by k. */
 sc_status sc_loss_fwd_bwd(sc_context ctx, const sc_batch* batch, const float* w, float grad_scale,
                           double* loss_sum, float* loss_row, int32_t* grad_idx, float* grad_val,
                           float* grad_dense, uint8_t* decision, uint64_t* n_incorrect, uint64_t* hist_pred,

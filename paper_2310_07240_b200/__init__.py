@@ -19,7 +19,8 @@ from typing import Optional, Sequence
 from . import build as _build
 
 __all__ = [
-    "ScError", "Context", "Batch", "sc_context_load", "sc_context_free", "sc_decide", "sc_decision_hist",
+    "ScError", "Context", "Batch", "sc_context_load", "sc_context_load_compact", "sc_context_columns",
+    "sc_context_free", "sc_decide", "sc_decision_hist",
     "sc_weights_from_hist", "sc_decision_hist_weights", "sc_loss_fwd_bwd", "Head", "sc_head_load",
     "sc_head_loss_fwd_bwd", "sc_last_error", "sc_launch_count", "sc_last_kernel", "library_path",
 ]
@@ -73,6 +74,10 @@ def _load():
     P, I32, I64, F = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_float
     lib.sc_context_load.restype = ctypes.c_int
     lib.sc_context_load.argtypes = [I32, I32, P, P, P, F, F, ctypes.c_int, ctypes.POINTER(P)]
+    lib.sc_context_load_compact.restype = ctypes.c_int
+    lib.sc_context_load_compact.argtypes = [I32, I32, P, P, P, F, F, ctypes.c_int, ctypes.POINTER(P)]
+    lib.sc_context_columns.restype = ctypes.c_int
+    lib.sc_context_columns.argtypes = [P, P, ctypes.POINTER(I32)]
     lib.sc_context_free.restype = ctypes.c_int
     lib.sc_context_free.argtypes = [P]
     lib.sc_context_info.restype = ctypes.c_int
@@ -200,7 +205,7 @@ class Context:
     application ``lists`` may be given as a list of lists."""
 
     def __init__(self, C: int, lists, tau: float = 0.0, k: float = 10.0, order: int = SC_ORDER_API_OUTPUT,
-                 multi_app: Optional[bool] = None):
+                 multi_app: Optional[bool] = None, compact: bool = False):
         if multi_app is None:
             multi_app = _nesting(lists) >= 3
         if not multi_app:
@@ -221,9 +226,20 @@ class Context:
         a_off = (ctypes.c_int64 * max(1, len(off)))(*off)
         a_lab = (ctypes.c_int32 * max(1, len(labels)))(*labels)
         h = ctypes.c_void_p()
-        _check(_lib.sc_context_load(self.C, self.n_apps, a_n, a_off, a_lab, self.tau, self.k, order,
-                                    ctypes.byref(h)))
+        load = _lib.sc_context_load_compact if compact else _lib.sc_context_load
+        _check(load(self.C, self.n_apps, a_n, a_off, a_lab, self.tau, self.k, order, ctypes.byref(h)))
         self._h = h
+        self.compact = bool(compact)
+
+    def columns(self):
+        """Labels of the logit columns a batch row holds (sc_context_columns): arange(C) for a
+        dense context, the ascending union of the mapped labels for a compacted one."""
+        import numpy as np
+        n = ctypes.c_int32()
+        _check(_lib.sc_context_columns(self._h, None, ctypes.byref(n)))
+        cols = np.empty(max(n.value, 1), dtype=np.int32)
+        _check(_lib.sc_context_columns(self._h, cols.ctypes.data, ctypes.byref(n)))
+        return cols[: n.value]
 
     @property
     def handle(self):
@@ -261,6 +277,16 @@ class Context:
 def sc_context_load(C: int, lists, tau: float = 0.0, k: float = 10.0, order: int = SC_ORDER_API_OUTPUT,
                     multi_app: Optional[bool] = None) -> Context:
     return Context(C, lists, tau, k, order, multi_app)
+
+
+def sc_context_load_compact(C: int, lists, tau: float = 0.0, k: float = 10.0, order: int = SC_ORDER_API_OUTPUT,
+                            multi_app: Optional[bool] = None) -> Context:
+    """Context for column-compacted rows: column j = label Context.columns()[j]."""
+    return Context(C, lists, tau, k, order, multi_app, compact=True)
+
+
+def sc_context_columns(ctx: Context):
+    return ctx.columns()
 
 
 def sc_context_free(ctx: Context):

@@ -69,6 +69,7 @@ sc::DevContext dev_ctx(const sc_context_s* c) {
   d.lent = c->d_lent;
   d.lent_off = c->d_lent_off;
   d.lslot = c->d_lslot;
+  d.col_label = c->d_col_label;
   d.C = c->C;
   d.n_apps = c->n_apps;
   d.max_ent = c->max_ent;
@@ -115,7 +116,8 @@ sc_status run_eval(const sc_context_s* ctx, const sc_batch* b, const float* w, f
   if (b->rows == 0) return SC_OK;
   if (!b->logits) return fail(SC_ERR_INVALID_ARG, "logits is NULL");
   const int64_t elt = b->dtype == SC_F32 ? 4 : 2;
-  if (b->ld < ctx->C) return fail(SC_ERR_INVALID_ARG, "ld (%lld) < C (%d)", (long long)b->ld, ctx->C);
+  if (b->ld < ctx->ncols)
+    return fail(SC_ERR_INVALID_ARG, "ld (%lld) < logit columns (%d)", (long long)b->ld, ctx->ncols);
   if ((b->ld * elt) % 16) return fail(SC_ERR_INVALID_ARG, "ld*sizeof(elt) must be a multiple of 16");
   if (reinterpret_cast<uintptr_t>(b->logits) % 16) return fail(SC_ERR_INVALID_ARG, "logits not 16-B aligned");
   if (grad_dense && reinterpret_cast<uintptr_t>(grad_dense) % 16)
@@ -171,7 +173,7 @@ sc_status run_eval(const sc_context_s* ctx, const sc_batch* b, const float* w, f
     // so the sparse gather only pays when whole lines of the row stay untouched.  Multi-app
     // batches stream on the TMA ring with a blocked schedule (cfg4, B200: f32 2.38 ms vs
     // 2.96 ms gather, bf16 1.42 ms vs 5.17 ms).
-    const int64_t lines_row = (static_cast<int64_t>(ctx->C) * elt + 127) / 128;
+    const int64_t lines_row = (static_cast<int64_t>(std::max(ctx->ncols, 1)) * elt + 127) / 128;
     const double frac = static_cast<double>(ctx->touched_lines[dt]) / (static_cast<double>(lines_row) * ctx->n_apps);
     bool gather = ctx->max_ent <= 1024 && frac <= gather_threshold(ctx->n_apps);
     if (kenv && std::string(kenv) == "tma") gather = false;
@@ -210,7 +212,7 @@ sc_status run_eval(const sc_context_s* ctx, const sc_batch* b, const float* w, f
   // ---- schedule: stage = R rows (or R row-chunks) in shared memory
   const int W = sc::kConsumerWarps;
   const int64_t stage_cap = 64 * 1024;
-  p.copy_row_bytes = static_cast<int32_t>(round_up(static_cast<int64_t>(ctx->C) * elt, 16));
+  p.copy_row_bytes = static_cast<int32_t>(round_up(static_cast<int64_t>(std::max(ctx->ncols, 1)) * elt, 16));
   // mapped labels in registers when whole rows fit a stage and |W| <= 1024
   int epl = 0;
   // Lane-resident entries cut the per-row instruction count (bf16 cfg2: 1.6x faster than the
@@ -337,8 +339,9 @@ int device_sms() {
 
 extern "C" {
 
-sc_status sc_context_load(int32_t C, int32_t n_apps, const int32_t* n_lists, const int64_t* list_off,
-                          const int32_t* list_labels, float tau, float k, sc_order order, sc_context* out) {
+static sc_status load_context(int32_t C, int32_t n_apps, const int32_t* n_lists, const int64_t* list_off,
+                              const int32_t* list_labels, float tau, float k, sc_order order, bool compact,
+                              sc_context* out) {
   if (!out) return fail(SC_ERR_INVALID_ARG, "out is NULL");
   *out = nullptr;
   if (order != SC_ORDER_API_OUTPUT && order != SC_ORDER_APP_CHOICE && order != SC_ORDER_MULTI_SELECT)
@@ -412,6 +415,40 @@ sc_status sc_context_load(int32_t C, int32_t n_apps, const int32_t* n_lists, con
     ctx->n_mapped.push_back(ent_off[a + 1] - ent_off[a]);
     ctx->max_ent = std::max(ctx->max_ent, ent_off[a + 1] - ent_off[a]);
   }
+  ctx->ncols = C;
+  if (compact) {
+    // column-compacted rows: the union of the apps' mapped labels,
+    // ascending, one logit column each; entry keys hold the column, so the arg max ties
+    // (smaller key first) still break toward the smaller label
+    std::vector<int32_t> pos(C, -1);
+    for (uint32_t e : ent) pos[e >> 8] = 0;
+    for (int32_t c = 0; c < C; ++c)
+      if (pos[c] == 0) {
+        pos[c] = static_cast<int32_t>(ctx->cols.size());
+        ctx->cols.push_back(c);
+      }
+    for (uint32_t& e : ent) e = static_cast<uint32_t>(pos[e >> 8]) << 8 | (e & 0xFFu);
+    ctx->ncols = static_cast<int32_t>(ctx->cols.size());
+    ctx->compact = true;
+    for (int dt = 0; dt < 2; ++dt) {  // touched sectors / lines of the compacted rows
+      const int per_sector = dt == 0 ? 8 : 16;
+      ctx->touched_sectors[dt] = ctx->touched_lines[dt] = 0;
+      for (int32_t a = 0; a < n_apps; ++a) {
+        int64_t last = -1, last_line = -1;
+        for (int32_t e = ent_off[a]; e < ent_off[a + 1]; ++e) {
+          const int64_t col = ent[e] >> 8;
+          if (col / per_sector != last) {
+            last = col / per_sector;
+            ++ctx->touched_sectors[dt];
+          }
+          if (col / (4 * per_sector) != last_line) {
+            last_line = col / (4 * per_sector);
+            ++ctx->touched_lines[dt];
+          }
+        }
+      }
+    }
+  }
   if (ent.empty()) ent.push_back(0);
   // per-list patterns: list-major slots (DevContext::lent) — list j's members in ascending
   // label order, padded to 32 entries per slot, so a warp reduces one list per slot
@@ -448,18 +485,22 @@ sc_status sc_context_load(int32_t C, int32_t n_apps, const int32_t* n_lists, con
   if (!e) e = cudaMemcpy(ctx->d_lent, lent.data(), lent.size() * 4, cudaMemcpyHostToDevice);
   if (!e) e = cudaMemcpy(ctx->d_lent_off, lent_off.data(), lent_off.size() * 4, cudaMemcpyHostToDevice);
   if (!e) e = cudaMemcpy(ctx->d_lslot, lslot.data(), lslot.size() * 4, cudaMemcpyHostToDevice);
-  if (!e) e = cudaMalloc(&ctx->d_done, sizeof(unsigned int));
+  if (!e) e = cudaMalloc(&ctx->d_done, sizeof(unsigned int) * sc_context_s::kDonePool);
   std::vector<uint8_t> catT(static_cast<size_t>(n_apps) * C);
   for (int32_t a = 0; a < n_apps; ++a)
     for (int32_t c = 0; c < C; ++c) catT[static_cast<size_t>(c) * n_apps + a] = cat[static_cast<size_t>(a) * C + c];
   ctx->n_ent_total = ent_off[n_apps];
   if (!e) e = cudaMalloc(&ctx->d_catT, catT.size());
   if (!e) e = cudaMemcpy(ctx->d_catT, catT.data(), catT.size(), cudaMemcpyHostToDevice);
-  if (!e) e = cudaMemset(ctx->d_done, 0, sizeof(unsigned int));
+  if (!e) e = cudaMemset(ctx->d_done, 0, sizeof(unsigned int) * sc_context_s::kDonePool);
   if (!e) e = cudaMemcpy(ctx->d_cat, cat.data(), cat.size(), cudaMemcpyHostToDevice);
   if (!e) e = cudaMemcpy(ctx->d_ent, ent.data(), ent.size() * 4, cudaMemcpyHostToDevice);
   if (!e) e = cudaMemcpy(ctx->d_ent_off, ent_off.data(), ent_off.size() * 4, cudaMemcpyHostToDevice);
   if (!e) e = cudaMemcpy(ctx->d_nlists, nl.data(), nl.size(), cudaMemcpyHostToDevice);
+  if (!e && compact && !ctx->cols.empty()) {
+    e = cudaMalloc(&ctx->d_col_label, ctx->cols.size() * 4);
+    if (!e) e = cudaMemcpy(ctx->d_col_label, ctx->cols.data(), ctx->cols.size() * 4, cudaMemcpyHostToDevice);
+  }
   if (e) {
     sc_context_free(ctx);
     return cuda_fail(e, "context upload");
@@ -479,7 +520,26 @@ sc_status sc_context_free(sc_context ctx) {
   cudaFree(ctx->d_nlists);
   cudaFree(ctx->d_done);
   cudaFree(ctx->d_catT);
+  cudaFree(ctx->d_col_label);
   delete ctx;
+  return SC_OK;
+}
+
+sc_status sc_context_load(int32_t C, int32_t n_apps, const int32_t* n_lists, const int64_t* list_off,
+                          const int32_t* list_labels, float tau, float k, sc_order order, sc_context* out) {
+  return load_context(C, n_apps, n_lists, list_off, list_labels, tau, k, order, false, out);
+}
+
+sc_status sc_context_load_compact(int32_t C, int32_t n_apps, const int32_t* n_lists, const int64_t* list_off,
+                                  const int32_t* list_labels, float tau, float k, sc_order order, sc_context* out) {
+  return load_context(C, n_apps, n_lists, list_off, list_labels, tau, k, order, true, out);
+}
+
+sc_status sc_context_columns(sc_context ctx, int32_t* cols, int32_t* n_cols) {
+  if (!ctx) return fail(SC_ERR_INVALID_ARG, "ctx is NULL");
+  if (n_cols) *n_cols = ctx->ncols;
+  if (cols)
+    for (int32_t j = 0; j < ctx->ncols; ++j) cols[j] = ctx->compact ? ctx->cols[j] : j;
   return SC_OK;
 }
 
@@ -511,11 +571,24 @@ sc_status sc_loss_fwd_bwd(sc_context ctx, const sc_batch* batch, const float* w,
                   n_incorrect, hist_pred, hist_gt, true, static_cast<cudaStream_t>(stream));
 }
 
+// The fused pre-pass's completion counter for `stream`: a slot of the context's pool owned
+// by that stream from its first use on (nullptr once the pool is exhausted).
+static unsigned int* done_counter_for(sc_context ctx, sc_stream stream) {
+  std::lock_guard<std::mutex> lock(ctx->done_mu);
+  auto& v = ctx->done_streams;
+  for (size_t i = 0; i < v.size(); ++i)
+    if (v[i] == stream) return ctx->d_done + i;
+  if (static_cast<int>(v.size()) == sc_context_s::kDonePool) return nullptr;
+  v.push_back(stream);
+  return ctx->d_done + (v.size() - 1);
+}
+
 static sc_status run_hist(sc_context ctx, const sc_batch* b, uint64_t* hist_gt, uint8_t* gt_mask_out, float* w_out,
                           sc_stream stream) {
   if (sc_status s = check_batch_common(ctx, b)) return s;
   if (!b->gt_off || !b->gt_lab) return fail(SC_ERR_INVALID_ARG, "sc_decision_hist needs gt_off and gt_lab");
   if (w_out && !hist_gt) return fail(SC_ERR_INVALID_ARG, "weights need hist_gt");
+  if (b->rows == 0 && w_out) return sc_weights_from_hist(ctx, hist_gt, w_out, stream);  // w of the histogram as is
   if (b->rows == 0 || (!hist_gt && !gt_mask_out)) return SC_OK;
   int dev = 0;
   if (cudaError_t e = cudaGetDevice(&dev)) return cuda_fail(e, "cudaGetDevice");
@@ -530,7 +603,11 @@ static sc_status run_hist(sc_context ctx, const sc_batch* b, uint64_t* hist_gt, 
   p.hist_gt = reinterpret_cast<unsigned long long*>(hist_gt);
   p.gt_mask_out = gt_mask_out;
   p.w_out = w_out;
-  p.done_counter = ctx->d_done;
+  p.done_counter = w_out ? done_counter_for(ctx, stream) : nullptr;
+  if (w_out && !p.done_counter) {  // more streams than counters: two launches (hist, then weights)
+    if (sc_status s = run_hist(ctx, b, hist_gt, gt_mask_out, nullptr, stream)) return s;
+    return sc_weights_from_hist(ctx, hist_gt, w_out, stream);
+  }
   const size_t hbytes = static_cast<size_t>(ctx->n_apps) * 256 * 8;
   p.smem_hist = hbytes <= 32 * 1024;
   // single application: one row per thread, the category table in shared memory
@@ -570,6 +647,7 @@ sc_status sc_decide_all_apps(sc_context ctx, const sc_batch* b, uint64_t* n_inco
   if (sc_status s = check_batch_common(ctx, b)) return s;
   if (ctx->order != SC_ORDER_API_OUTPUT)
     return fail(SC_ERR_UNSUPPORTED, "sc_decide_all_apps supports the API-output order");
+  if (ctx->compact) return fail(SC_ERR_UNSUPPORTED, "sc_decide_all_apps reads dense rows (column c = label c)");
   if (!b->gt_off || !b->gt_lab) return fail(SC_ERR_INVALID_ARG, "sc_decide_all_apps needs gt_off and gt_lab");
   if (b->dtype != SC_F32 && b->dtype != SC_BF16) return fail(SC_ERR_INVALID_ARG, "unknown dtype");
   if (b->rows == 0) return SC_OK;

@@ -70,6 +70,21 @@ __device__ __forceinline__ void st_cs_f4(float* p, float4 v) {
                : "memory");
 }
 
+// Side band of rows [r0, r0 + nr) of a per-row array (elt bytes per row): the 16-B-aligned
+// interior [r0·elt + head, r0·elt + head + nb) is what a bulk copy may move (its source and
+// size must be 16-B multiples); the ragged head and tail rows are read from global memory,
+// so nothing outside the caller's array is ever read.  Byte offset o = j·elt of row r0 + j
+// lies in the window iff (o − head) < nb as unsigned.
+struct SideBand {
+  uint32_t head, nb;
+};
+__device__ __forceinline__ SideBand sb_window(const void* base, int64_t r0, int nr, uint32_t elt) {
+  const uintptr_t a0 = reinterpret_cast<uintptr_t>(base) + static_cast<uintptr_t>(r0) * elt;
+  const uintptr_t a1 = a0 + static_cast<uintptr_t>(nr) * elt;
+  const uintptr_t lo = (a0 + 15) & ~uintptr_t(15), hi = a1 & ~uintptr_t(15);
+  return SideBand{static_cast<uint32_t>(lo - a0), hi > lo ? static_cast<uint32_t>(hi - lo) : 0u};
+}
+
 // ------------------------------------------------------------------ math (fp32, no fast-math)
 
 // σ(z) = 1/(1+e^{-z}) without overflow (reading A2).
@@ -164,9 +179,9 @@ __device__ __forceinline__ void finish_batch(const EvalParams& p, RowBatch& b, c
         i1 = static_cast<int32_t>(b.km >> 8);
       }
       if (p.loss_row) p.loss_row[b.row] = L;
-      if (p.grad_idx) {
-        p.grad_idx[2 * b.row] = i0;
-        p.grad_idx[2 * b.row + 1] = i1;
+      if (p.grad_idx) {  // label ids (i0 / i1 are logit columns, which differ for compacted rows)
+        p.grad_idx[2 * b.row] = out_label(p.ctx, i0);
+        p.grad_idx[2 * b.row + 1] = out_label(p.ctx, i1);
       }
       if (p.grad_val) {
         p.grad_val[2 * b.row] = g0;

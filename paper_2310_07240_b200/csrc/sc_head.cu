@@ -746,7 +746,7 @@ sc_status sc_head_load(sc_context ctx, const uint16_t* weight, int64_t ldw, int6
     h->list_col0[j] = static_cast<int32_t>(col_label.size());
     for (int32_t t = 0; t < nm; ++t)
       if ((ent[t] & 0xFFu) == static_cast<uint32_t>(j)) {
-        col_label.push_back(static_cast<int32_t>(ent[t] >> 8));
+        col_label.push_back(ctx->compact ? ctx->cols[ent[t] >> 8] : static_cast<int32_t>(ent[t] >> 8));  // W row
         keys.push_back(ent[t]);
       }
     while (col_label.size() % 16) {
@@ -853,6 +853,7 @@ sc_status sc_head_loss_fwd_bwd(sc_context ctx, sc_head head, const sc_head_batch
   ep.ctx.ent = ctx->d_ent;
   ep.ctx.ent_off = ctx->d_ent_off;
   ep.ctx.nlists = ctx->d_nlists;
+  ep.ctx.col_label = ctx->d_col_label;  // compacted context: keys hold columns, gradients report labels
   ep.ctx.C = ctx->C;
   ep.ctx.n_apps = ctx->n_apps;
   ep.ctx.max_ent = ctx->max_ent;

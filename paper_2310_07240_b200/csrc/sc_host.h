@@ -3,10 +3,17 @@
 #include "sc.h"
 
 #include <cstdint>
+#include <mutex>
 #include <vector>
 
 struct sc_context_s {
   int32_t C = 0, n_apps = 0, max_ent = 0;
+  // logit columns a batch row holds: C (dense: column c = label c), or |union of the apps'
+  // mapped labels| for a column-compacted context (column j = label cols[j], ascending)
+  int32_t ncols = 0;
+  bool compact = false;
+  std::vector<int32_t> cols;        // compact: label of each column
+  int32_t* d_col_label = nullptr;   // compact: device copy of cols (gradient indices -> labels)
   int32_t order = 0;
   float tau = 0.f, theta = 0.5f, k = 1.f;
   int device = 0;
@@ -17,7 +24,13 @@ struct sc_context_s {
   uint32_t* d_ent = nullptr;
   int32_t* d_ent_off = nullptr;
   uint8_t* d_nlists = nullptr;
-  unsigned int* d_done = nullptr;  // completion counter of the fused hist+weights pre-pass
+  // completion counters of the fused hist+weights pre-pass: one per stream that has used
+  // this context (kDonePool preallocated at load, so calls on different streams never share
+  // one; each returns to 0 when its launch completes, so calls on one stream reuse it)
+  static constexpr int kDonePool = 64;
+  unsigned int* d_done = nullptr;  // [kDonePool]
+  std::mutex done_mu;
+  std::vector<void*> done_streams;  // stream handle of each slot in use
   uint8_t* d_catT = nullptr;       // [C][n_apps] label-major category table (all-apps pass)
   int32_t n_ent_total = 0;
   int32_t max_slots = 0;           // per-list patterns: most list-major 32-entry slots of an app

@@ -27,10 +27,18 @@ struct DevContext {
   const uint32_t* lent = nullptr;     // slot entries
   const int32_t* lent_off = nullptr;  // [n_apps+1]  (multiples of 32)
   const uint32_t* lslot = nullptr;    // [n_apps]  list of slot s in bits 4s..4s+3 (<= 8 slots)
+  // column-compacted contexts (sc_context_load_compact): entry keys hold column positions,
+  // col_label maps a position back to its label for the gradient indices; nullptr = dense
+  const int32_t* col_label = nullptr;
   int32_t C, n_apps, max_ent;
   float tau, theta, k;
   int32_t order;            // kApiOutput / kAppChoice / kMultiSelect
 };
+
+// Label id reported for the logit column `pos` of an entry key (identity for dense rows).
+__device__ __forceinline__ int32_t out_label(const DevContext& c, int32_t pos) {
+  return (c.col_label != nullptr && pos >= 0) ? __ldg(c.col_label + pos) : pos;
+}
 
 // Lists (bit set) label-table value v stands for.
 __host__ __device__ __forceinline__ uint32_t label_lists(uint8_t v, int order) {

@@ -405,7 +405,7 @@ __device__ __forceinline__ void finish_lists_core(const EvalParams& p, RowBatch&
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         if (q < S) {
-          if (p.grad_idx) p.grad_idx[S * b.row + q] = gi[q];
+          if (p.grad_idx) p.grad_idx[S * b.row + q] = out_label(p.ctx, gi[q]);  // gi: logit columns
           if (p.grad_val) p.grad_val[S * b.row + q] = gv[q];
         }
       }
@@ -540,17 +540,17 @@ __global__ void __launch_bounds__(kThreads, 1) eval_kernel(const EvalParams p) {
           const uint8_t* src_a = nullptr;
           uint32_t nb_m = 0, nb_a = 0;
           if (kc == 0) {
+            // side bands: only the 16-B-aligned interior of each window is bulk-copied (no
+            // byte outside the caller's array is touched); rows outside it read global memory
             if (p.gt_mask) {
-              const uintptr_t lo = reinterpret_cast<uintptr_t>(p.gt_mask + r0) & ~uintptr_t(15);
-              const uintptr_t hi = (reinterpret_cast<uintptr_t>(p.gt_mask + r0 + nr) + 15) & ~uintptr_t(15);
-              src_m = reinterpret_cast<const uint8_t*>(lo);
-              nb_m = static_cast<uint32_t>(hi - lo);
+              const SideBand w = sb_window(p.gt_mask, r0, nr, 1);
+              src_m = reinterpret_cast<const uint8_t*>(p.gt_mask + r0) + w.head;
+              nb_m = w.nb;
             }
             if (p.app) {
-              const uintptr_t lo = reinterpret_cast<uintptr_t>(p.app + r0) & ~uintptr_t(15);
-              const uintptr_t hi = (reinterpret_cast<uintptr_t>(p.app + r0 + nr) + 15) & ~uintptr_t(15);
-              src_a = reinterpret_cast<const uint8_t*>(lo);
-              nb_a = static_cast<uint32_t>(hi - lo);
+              const SideBand w = sb_window(p.app, r0, nr, 2);
+              src_a = reinterpret_cast<const uint8_t*>(p.app + r0) + w.head;
+              nb_a = w.nb;
             }
           }
           if (p.nchunks == 1) {
@@ -587,16 +587,18 @@ __global__ void __launch_bounds__(kThreads, 1) eval_kernel(const EvalParams p) {
   RowBatch b;
   b.n = 0; b.zp = b.zm = 0.f; b.kp = b.km = kNone; b.G = 0; b.app = 0; b.row = 0;
 
-  auto row_app_mask = [&](const uint8_t* st, int64_t r0, int64_t row, uint32_t& a, uint32_t& G) {
+  auto row_app_mask = [&](const uint8_t* st, int64_t r0, int nr, int64_t row, uint32_t& a, uint32_t& G) {
+    const uint32_t j = static_cast<uint32_t>(row - r0);
     a = 0;
     if (p.app) {
-      const uintptr_t lo = reinterpret_cast<uintptr_t>(p.app + r0) & ~uintptr_t(15);
-      a = *reinterpret_cast<const uint16_t*>(st + p.app_off + (reinterpret_cast<uintptr_t>(p.app + row) - lo));
+      const SideBand w = sb_window(p.app, r0, nr, 2);
+      a = 2u * j - w.head < w.nb ? *reinterpret_cast<const uint16_t*>(st + p.app_off + (2u * j - w.head))
+                                 : static_cast<uint32_t>(__ldg(p.app + row));
     }
     G = 0;
     if (p.gt_mask) {
-      const uintptr_t lo = reinterpret_cast<uintptr_t>(p.gt_mask + r0) & ~uintptr_t(15);
-      G = st[p.mask_off + (reinterpret_cast<uintptr_t>(p.gt_mask + row) - lo)];
+      const SideBand w = sb_window(p.gt_mask, r0, nr, 1);
+      G = j - w.head < w.nb ? st[p.mask_off + (j - w.head)] : static_cast<uint32_t>(__ldg(p.gt_mask + row));
     } else if (p.has_gt) {
       G = warp_gt_mask(p, row, a, lane);
     }
@@ -638,14 +640,17 @@ __global__ void __launch_bounds__(kThreads, 1) eval_kernel(const EvalParams p) {
       const int nr = static_cast<int>((p.rows - r0 < p.R ? p.rows - r0 : (int64_t)p.R));
       mbar_wait(full + st_idx, ph);
       const uint32_t st_off = static_cast<uint32_t>(st_idx) * p.stage_bytes;
-      // side-band windows start at the 16-B boundary below row r0
-      const uint32_t m_base = st_off + p.mask_off + (p.gt_mask ? (reinterpret_cast<uintptr_t>(p.gt_mask + r0) & 15u) : 0u);
-      const uint32_t a_base = st_off + p.app_off + (p.app ? (reinterpret_cast<uintptr_t>(p.app + r0) & 15u) : 0u);
+      // side-band windows: the aligned interior of rows [r0, r0 + nr) is in the stage
+      const SideBand wm = p.gt_mask ? sb_window(p.gt_mask, r0, nr, 1) : SideBand{0u, 0u};
+      const SideBand wa = p.app ? sb_window(p.app, r0, nr, 2) : SideBand{0u, 0u};
+      const uint32_t m_base = sbase + st_off + p.mask_off - wm.head;
+      const uint32_t a_base = sbase + st_off + p.app_off - wa.head;
       for (int j = wi; j < nr; j += wg) {
         const int64_t row = r0 + j;
-        const uint32_t a = p.app ? lds_u16(sbase + a_base + 2u * j) : 0u;
+        const uint32_t a = !p.app ? 0u
+                           : (2u * j - wa.head < wa.nb ? lds_u16(a_base + 2u * j) : static_cast<uint32_t>(__ldg(p.app + row)));
         uint32_t G = 0;
-        if (p.gt_mask) G = lds_u8(sbase + m_base + j);
+        if (p.gt_mask) G = static_cast<uint32_t>(j) - wm.head < wm.nb ? lds_u8(m_base + j) : static_cast<uint32_t>(__ldg(p.gt_mask + row));
         else if (p.has_gt) G = warp_gt_mask(p, row, a, lane);
         const uint32_t srow = sbase + st_off + static_cast<uint32_t>(j) * static_cast<uint32_t>(p.ld_bytes);
         float zs[EPL];
@@ -729,7 +734,7 @@ __global__ void __launch_bounds__(kThreads, 1) eval_kernel(const EvalParams p) {
         for (int j = cw; j < nr; j += kConsumerWarps) {
           const int64_t row = r0 + j;
           uint32_t a, G;
-          row_app_mask(st, r0, row, a, G);
+          row_app_mask(st, r0, nr, row, a, G);
           select_app(a);
           const uint8_t* rowp = st + static_cast<int64_t>(j) * p.ld_bytes;
           float zp = -CUDART_INF_F, zm = -CUDART_INF_F;
@@ -770,7 +775,7 @@ __global__ void __launch_bounds__(kThreads, 1) eval_kernel(const EvalParams p) {
           const uint8_t* st = smem + static_cast<size_t>(s) * p.stage_bytes;
           if (mine) {
             if (kc == 0) {
-              row_app_mask(st, r0, row, a, G);
+              row_app_mask(st, r0, nr, row, a, G);
               select_app(a);
             }
             const uint8_t* rowp = st + static_cast<int64_t>(cw) * p.chunk_bytes;

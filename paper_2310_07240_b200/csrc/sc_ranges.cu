@@ -41,12 +41,43 @@ sc_status rfail(sc_status st, const char* msg) {
 // fast reciprocal divisions (<= 2 ulp) keep the element-wise pass memory-bound.
 // σ(z) and σ'(z) from one exponential: e = e^{-|z|}, r = 1/(1+e); σ = r or e·r, σ' = e·r².
 // e^{-|z|} = 2^{-|z| log2 e}: one multiply + ex2.approx.f32 (2 ulp, subnormals kept) instead
-// of expf's range reduction; the rounded product adds |z| 2^-24 log2 e to the exponent, a
-// relative error <= 4e-6 for every |z| < 104 where e^{-|z|} is representable.
+// of expf's range reduction.  Relative error of e, by source: the rounded product and the
+// rounded log2 e constant move the exponent by <= |z|·(2^-24 + 1.3e-8)·log2 e (<= 6e-8·|z|
+// relative in e), ex2.approx <= 2.4e-7; and the caller's argument z = k·(x − y), rounded
+// twice in fp32, carries <= 1.2e-7·|z| more.  Total <= 1.9e-7·|z| + 5e-7, inside the 1e-5
+// bar for |z| <= kFastArg = 24; larger arguments take sig_dsig_arg's fp64 path.
 __device__ __forceinline__ void sig_dsig(float z, float& s, float& ds) {
   const float e = exp2f(__fmul_rn(-fabsf(z), 1.4426950408889634f));
   const float r = __fdividef(1.f, 1.f + e);
   s = z >= 0.f ? r : e * r;
+  ds = e * r * r;
+}
+
+constexpr float kFastArg = 24.f;
+
+// σ(z), σ'(z) for z = k(x − y) with |z| > kFastArg (a score deep inside or far outside its
+// ground-truth range; never in the bench's workload), in fp32 with error-free transforms:
+// x − y as an exact two-term sum (TwoSum), k times it as zh + zl (FMA residual), the exponent
+// −|z| log2 e as yh + yl with log2 e split in two floats, and e^{-|z|} = 2^yh (1 + yl ln 2).
+// Relative error of e <= ~5e-7 at any |z| (ex2.approx and the final roundings), subnormal
+// results keep their absolute accuracy.  Register-light, so the cold branch does not change
+// the hot loop's occupancy (an fp64 version took the kernel from 61 to 98 registers).
+__device__ __forceinline__ void sig_dsig_far(float k, float x, float y, float& s, float& ds) {
+  const float d = x - y;
+  const float bb = d - x;
+  const float dl = (x - (d - bb)) + (-y - bb);           // x − y = d + dl exactly
+  const float zh = k * d;
+  const float zl = fmaf(k, d, -zh) + k * dl;              // k(x − y) = zh + zl (to ~2^-48 |z|)
+  const float sg = zh >= 0.f ? 1.f : -1.f;                // |zl| << |zh| here: the sign is zh's
+  const float ah = fabsf(zh), al = sg * zl;               // |z| = ah + al
+  constexpr float kL2E = 1.44269502162933349609375f;      // log2 e rounded to float
+  constexpr float kL2ELo = 1.925963033500011e-8f;         // log2 e − kL2E
+  const float yh = -ah * kL2E;
+  const float yl = fmaf(-ah, kL2E, -yh) - ah * kL2ELo - al * kL2E;
+  const float e0 = exp2f(yh);
+  const float e = fmaf(e0, yl * 0.693147180559945f, e0);  // 2^yl = 1 + yl ln 2 (|yl| < 1e-5)
+  const float r = 1.f / (1.f + e);
+  s = zh >= 0.f ? r : e * r;
   ds = e * r * r;
 }
 
@@ -262,18 +293,20 @@ __global__ void __launch_bounds__(256) ranges_loss_kernel(const float* lo_g, con
     range_lookup<kV>(sv, d, lo, hi, m, sorted);  // Decision(API(x)): the first containing range in code order
     float L[kV], g[kV];
     float part = 0.f;  // this pass's 8 losses in fp32, then one fp64 add (rel. error ~5e-7)
+    bool far = false;  // some row's S argument leaves the fast path's accuracy range
 #pragma unroll
     for (int q = 0; q < kV; ++q) {
       const bool act = q < nv;
       L[q] = 0.f;
       g[q] = 0.f;
       if (act && r[q] < m) {
-        const float a = k * (lo[r[q]] - sv[q]), b = k * (sv[q] - hi[r[q]]);
+        const float a = k * (lo[r[q]] - sv[q]), b = k * (sv[q] - hi[r[q]]);  // S(l − O), S(O − h)
         float sa, da, sb, db;
         sig_dsig(a, sa, da);
         sig_dsig(b, sb, db);
         L[q] = ws[r[q]] * (sa + sb);
         g[q] = ws[r[q]] * k * (db - da) * grad_scale;
+        far |= fabsf(a) > kFastArg || fabsf(b) > kFastArg;
       }
       part += L[q];
       my_inc += (act && d[q] != r[q]) ? 1u : 0u;
@@ -306,6 +339,26 @@ __global__ void __launch_bounds__(256) ranges_loss_kernel(const float* lo_g, con
       } else {
 #pragma unroll
         for (int q = 0; q < kV; ++q) count_bins<SMALL>(m + 1, q < nv, d[q], lane, mine, hp);
+      }
+    }
+    if (far) {  // rare (see sig_dsig_far): this thread's rows again, operands re-read (L1-hot), results overwritten
+#pragma unroll 1
+      for (int q = 0; q < nv; ++q) {
+        const int r_q = __ldg(gt_range + i0 + q);
+        if (r_q >= m) continue;
+        const float s_q = __ldg(score + i0 + q);
+        const float a = k * (lo[r_q] - s_q), b = k * (s_q - hi[r_q]);
+        if (!(fabsf(a) > kFastArg || fabsf(b) > kFastArg)) continue;
+        float sa, da, sb, db;
+        sig_dsig(a, sa, da);
+        sig_dsig(b, sb, db);
+        my_loss -= static_cast<double>(ws[r_q] * (sa + sb));  // the fast value already in part
+        sig_dsig_far(k, lo[r_q], s_q, sa, da);
+        sig_dsig_far(k, s_q, hi[r_q], sb, db);
+        const float Lq = ws[r_q] * (sa + sb);
+        my_loss += static_cast<double>(Lq);
+        if (loss_row) loss_row[i0 + q] = Lq;
+        if (grad) grad[i0 + q] = ws[r_q] * k * (db - da) * grad_scale;
       }
     }
   }

@@ -173,7 +173,8 @@ class Evaluator:
         if self._d_off is None or self._d_off.numel() < rows + 1 or self._d_lab.numel() < h_gt_lab.numel():
             self._d_off = torch.empty(rows + 1, dtype=torch.int64, device=dev)
             self._d_lab = torch.empty(max(1, h_gt_lab.numel()), dtype=torch.int32, device=dev)
-            self._d_app = torch.empty(rows, dtype=torch.int16, device=dev) if h_app is not None else None
+        if h_app is not None and (getattr(self, "_d_app", None) is None or self._d_app.numel() < rows):
+            self._d_app = torch.empty(max(1, rows), dtype=torch.int16, device=dev)
         comp = torch.cuda.current_stream(dev)
         cp = self._copy_stream
         d_off = self._d_off[:rows + 1]
