@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--d", type=int, default=2048, help="--mode head: feature width (ResNet-50 penultimate = 2048)")
     ap.add_argument("--order", default="api_output", choices=["api_output", "app_choice", "multi_select"],
                     help="decision pattern (default: the north star's API-output order)")
+    ap.add_argument("--compact", action="store_true",
+                    help="column-compacted rows (sc_context_load_compact, NEXT f3): each row holds only the "
+                         "mapped labels' logits, as a producer restricted to those columns emits them")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -86,14 +89,17 @@ def workload_name(cfg, dtype):
     return f"{WORKLOADS[cfg]}, {dtype} logits"
 
 
-def touched_sector_bytes(spec, ld, elt, rows=None, layout_rows_per_app=1 << 18):
+def touched_sector_bytes(spec, ld, elt, rows=None, layout_rows_per_app=1 << 18, columns=None):
     """Mean bytes per row of the 32-B sectors holding at least one mapped label of the
-    row's application (SURVEY.md §8(d)'s algorithmic minimum), row base addresses r*ld*elt."""
+    row's application (SURVEY.md §8(d)'s algorithmic minimum), row base addresses r*ld*elt.
+    columns: the labels of a compacted row's columns (sc_context_columns), else column c = label c."""
     import numpy as np
     m = spec.mapped()
     per_app = []
     for a in range(spec.n_apps):
         cols = np.nonzero(m[a])[0]
+        if columns is not None:
+            cols = np.searchsorted(columns, cols)
         if len(cols) == 0:
             per_app.append(0.0)
             continue
@@ -165,10 +171,11 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
-def load_traffic(cfg, dtype, kernel, rows):
+def load_traffic(cfg, dtype, kernel, rows, compact=False):
     """dram read+write bytes per launch of the eval kernel from the committed ncu summary
-    (profiles/ncu_eval_cfg{cfg}_{dtype}_{kernel}.json), scaled to this launch's rows."""
-    path = os.path.join(ROOT, "profiles", f"ncu_eval_cfg{cfg}_{dtype}_{kernel}.json")
+    (profiles/ncu_eval_cfg{cfg}[_compact]_{dtype}_{kernel}.json), scaled to this launch's rows."""
+    tag = f"cfg{cfg}_compact" if compact else f"cfg{cfg}"
+    path = os.path.join(ROOT, "profiles", f"ncu_eval_{tag}_{dtype}_{kernel}.json")
     try:
         d = json.load(open(path))
         return d["dram_bytes_per_row"] * rows, os.path.relpath(path, ROOT)
@@ -230,6 +237,17 @@ class OracleSample:
     def describe(self, dt):
         return (f"{self.rows} rows of cfg2 (rows {self.first_row}..{self.first_row + self.rows - 1}), GT pre-pass + "
                 f"weights + full oracle pass, {self.threads} threads x {self.chunk}-row chunks, {dt:.2f} s wall")
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
 
 
 def cpu_oracle_rate(seconds: float, threads: int | None = None, seed_rows=0):
@@ -305,11 +323,16 @@ def run_ours(args):
     spec = synth.config_context(cfg)
     B = args.rows or DEFAULT_ROWS[cfg]
     wl = synth.Workload(spec, seed=cfg, dtype=args.dtype, rows_per_app=1 << 18)
-    data = wl.device_batch(rank * B, B, device=dev)  # this rank's rows of the global dataset
+    order = {"api_output": 0, "app_choice": 1, "multi_select": 2}[args.order]
+    ctx = sc.Context(spec.C, spec.lists, spec.tau, spec.k, order=order, multi_app=True, compact=args.compact)
+    columns = None
+    if args.compact:
+        columns = ctx.columns()
+        data = compact_device_batch(wl, rank * B, B, columns, dev)
+    else:
+        data = wl.device_batch(rank * B, B, device=dev)  # this rank's rows of the global dataset
     logits, gt_off, gt_lab = data["logits"], data["gt_off"], data["gt_lab"]
     app = data.get("app")
-    order = {"api_output": 0, "app_choice": 1, "multi_select": 2}[args.order]
-    ctx = sc.Context(spec.C, spec.lists, spec.tau, spec.k, order=order, multi_app=True)
     ev = Evaluator(ctx, B, device=dev, group=group)
     global_rows = B * world
 
@@ -387,14 +410,14 @@ def run_ours(args):
     # roofline of the dominant kernel (eval_kernel behind sc_loss_fwd_bwd)
     elt = 4 if args.dtype == "f32" else 2
     ld = logits.stride(0)
-    sect = touched_sector_bytes(spec, ld, elt, rows=B)
+    sect = touched_sector_bytes(spec, ld, elt, rows=B, columns=columns)
     per_row = sect + 1 + 1 + 8 * ctx.grad_slots + (2 if app is not None else 0)  # sectors + G_i + decision + sparse grad (+ app)
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     peak = peaks.get("hbm_gbs", 6650.0)
     achieved = B * per_row / (k_ms / 1e3) / 1e9
     kname = sc.sc_last_kernel()
-    traffic, tpath = load_traffic(cfg, args.dtype, kname, B)
+    traffic, tpath = load_traffic(cfg, args.dtype, kname, B, compact=args.compact)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "kernel": "eval_kernel (sc_loss_fwd_bwd)", "kernel_ms": k_ms,
                 "algorithmic_bytes_per_row": per_row, "dense_bytes_per_row": ld * elt + 18,
@@ -408,7 +431,9 @@ def run_ours(args):
         "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
         "config": {"workload": workload_name(cfg, args.dtype), "C": spec.C, "rows_per_gpu": B, "global_batch": global_rows,
                    "parallelism": f"dp{world}", "l2": f"no flush: {B * ld * elt / 1e9:.2f} GB of logits per step per GPU > 126 MB L2",
-                   "grad": f"sparse ({ctx.grad_slots} slots/row)", "order": args.order},
+                   "grad": f"sparse ({ctx.grad_slots} slots/row)", "order": args.order,
+                   "layout": (f"column-compacted: {len(columns)} of {spec.C} label columns per row (sc_context_load_compact)"
+                              if args.compact else "dense rows, column c = label c")},
         "roofline": roofline,
         "gpu_launches": int(launches),
         "phases_us": {k: round(v, 2) for k, v in phase_us.items()},
@@ -422,14 +447,49 @@ def run_ours(args):
     torch.cuda.empty_cache()
     if rank == 0 and not args.no_cpu_baseline:
         rate, rows, dt, threads, smp = cpu_oracle_rate(args.cpu_seconds)
+        rate1, rows1, dt1, _, smp1 = cpu_oracle_rate(min(4.0, args.cpu_seconds / 3), threads=1)
         line["cpu_baseline"] = {"value": rate, "unit": "samples/s", "cores": threads, "kind": "oracle",
-                                "sample": smp.describe(dt)}
+                                "sample": smp.describe(dt), "cpu_model": cpu_model(),
+                                "single_thread": {"value": rate1, "unit": "samples/s", "sample": smp1.describe(dt1)},
+                                "per_config": "profiles/r2_cpu_baseline_split.json (tools/cpu_baseline_split.py)"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist_on(world):
         import torch.distributed as dist
         dist.destroy_process_group()
     return 0
+
+
+def compact_device_batch(wl, row0, n, columns, dev, chunk=1 << 14):
+    """Rows [row0, row0+n) of the workload with only the given label columns kept (the rows a
+    producer restricted to the mapped labels emits): generated densely chunk by chunk on the
+    GPU, then column-gathered (input preparation, outside every timed region)."""
+    import torch
+    import synth
+    cols = torch.from_numpy(columns.astype("int64")).to(dev)
+    ldc = synth.default_ld(len(columns), wl.dtype)
+    tdt = torch.float32 if wl.dtype == "f32" else torch.bfloat16
+    logits = torch.full((max(n, 1), ldc), float("nan"), dtype=tdt, device=dev)
+    gt = wl.device_batch(row0, 0, device=dev) if n == 0 else None
+    offs, labs, apps, base = [], [], [], 0
+    for lo in range(0, n, chunk):
+        hi = min(n, lo + chunk)
+        b = wl.device_batch(row0 + lo, hi - lo, device=dev)
+        logits[lo:hi, :len(columns)] = b["logits"].index_select(1, cols)
+        offs.append(b["gt_off"][:-1] + base if lo + chunk < n else b["gt_off"] + base)
+        labs.append(b["gt_lab"])
+        base += int(b["gt_off"][-1])
+        if "app" in b:
+            apps.append(b["app"])
+        del b
+    out = dict(logits=logits[:n])
+    if n == 0:
+        out.update(gt_off=gt["gt_off"], gt_lab=gt["gt_lab"])
+    else:
+        out.update(gt_off=torch.cat(offs), gt_lab=torch.cat(labs))
+    if apps:
+        out["app"] = torch.cat(apps)
+    return out
 
 
 def run_all_apps(args, sc, ctx, logits, gt_off, gt_lab, B, dev, stream, rank):
@@ -557,9 +617,10 @@ def run_head(args, sc, ctx, spec, gt_off, gt_lab, B, dev, stream, rank, data):
     gm = torch.empty(B + 16, dtype=torch.uint8, device=dev)
     hg = torch.zeros(256, dtype=torch.int64, device=dev)
     w = torch.empty(256, dtype=torch.float32, device=dev)
+    S = ctx.grad_slots
     out = dict(decision=torch.empty(B, dtype=torch.uint8, device=dev),
-               grad_idx=torch.empty(2 * B, dtype=torch.int32, device=dev),
-               grad_val=torch.empty(2 * B, dtype=torch.float32, device=dev),
+               grad_idx=torch.empty(S * B, dtype=torch.int32, device=dev),
+               grad_val=torch.empty(S * B, dtype=torch.float32, device=dev),
                loss_sum=torch.zeros(1, dtype=torch.float64, device=dev),
                n_incorrect=torch.zeros(1, dtype=torch.int64, device=dev),
                hist_pred=torch.zeros(256, dtype=torch.int64, device=dev))
@@ -610,20 +671,30 @@ def run_head(args, sc, ctx, spec, gt_off, gt_lab, B, dev, stream, rank, data):
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     hbm = peaks.get("hbm_gbs", 6650.0)
     tc = peaks.get("bf16_tflops", 1662.7)
-    per_row = d * 2 + 1 + 1 + 16  # features + G_i + decision + sparse gradient
+    per_row = d * 2 + 1 + 1 + 8 * S  # features + G_i + decision + sparse gradient
     achieved = B * per_row / (k_ms / 1e3) / 1e9
     n_mapped = int(spec.mapped()[0].sum())
     tflops = B * 2.0 * d * n_mapped / (k_ms / 1e3) / 1e12
+    # the bound: whichever floor is higher — x bytes at the HBM peak, or the mapped columns'
+    # flops at the bf16 tensor peak (a wide context, e.g. cfg3's 1000 mapped labels)
+    t_hbm = B * per_row / (hbm * 1e9)
+    t_tc = B * 2.0 * d * n_mapped / (tc * 1e12)
+    if t_tc > t_hbm:
+        roof = {"bound": "tensor", "achieved": tflops, "peak": tc, "unit": "TFLOP/s", "frac": tflops / tc,
+                "hbm": {"achieved_gbs": achieved, "peak_gbs": hbm, "frac": achieved / hbm}}
+    else:
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                "tensor": {"achieved_tflops": tflops, "peak_tflops": tc, "frac": tflops / tc}}
+    roof.update({"kernel": kname, "kernel_ms": k_ms, "algorithmic_bytes_per_row": per_row,
+                 "flops_per_row": 2 * d * n_mapped, "traffic": None,
+                 "peak_source": "MEASURED_PEAKS.json (hbm_gbs copy, bf16_tflops cuBLAS burst)" if peaks else "fallback"})
     line = {
         "metric": "samples/s for the classifier head fused with decide+loss fwd/bwd (NEXT f4)",
         "value": B / (ms / 1e3), "unit": "samples/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms, "higher_is_better": True, "dtype": "bf16 operands, f32 accumulate", "data": "synthetic",
         "config": {"workload": f"{WORKLOADS[args.config]}, bf16 features d={d}, head over the {n_mapped} mapped "
-                               f"labels ({n_cols} columns)", "rows": B, "d": d},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                     "kernel": kname, "kernel_ms": k_ms, "algorithmic_bytes_per_row": per_row,
-                     "tensor": {"achieved_tflops": tflops, "peak_tflops": tc, "frac": tflops / tc,
-                                "flops_per_row": 2 * d * n_mapped}},
+                               f"labels ({n_cols} columns)", "rows": B, "d": d, "order": args.order},
+        "roofline": roof,
         "unfused": {"ms_per_step": un_ms, "what": f"cuBLAS addmm -> bf16 logits [B, {spec.C}] + sc_loss_fwd_bwd",
                     "speedup_fused": un_ms / ms},
         "gpu_launches": int(launches), "clocks": clk.summary(),
@@ -664,8 +735,11 @@ def run_e2e(args, ev, data, global_rows, dev, barrier, world):
     return {"value": global_rows * args.e2e_steps / dt, "unit": "samples/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "steps": args.e2e_steps,
             "h2d_gbs_per_gpu": round(h2d * args.e2e_steps / dt / 1e9, 2),  # PCIe-bound: the step moves 4.2 GB host->device
-            "bound": "pcie (host->device copy of the step's logits)",
-            "api": "Evaluator.step_host (pinned host inputs -> chunked H2D overlapped with sc_loss_fwd_bwd -> D2H)"}
+            "bound": "pcie (host->device transfer of the step's logits)",
+            "host_mode": {0: "auto", 1: "copy", 2: "zero_copy"}.get(getattr(ev, "host_mode_used", None)),
+            "api": "Evaluator.step_host: GT host->device, sc_decision_hist + sc_weights_from_hist, then "
+                   "sc_loss_fwd_bwd_host (C ABI, pinned host logits: chunked double-buffered H2D inside libsc, "
+                   "or zero copy for sparse contexts), results device->host"}
 
 
 def _free_port():

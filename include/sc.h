@@ -225,6 +225,44 @@ sc_status sc_loss_fwd_bwd(sc_context ctx, const sc_batch* batch, const float* w,
                           float* grad_dense, uint8_t* decision, uint64_t* n_incorrect, uint64_t* hist_pred,
                           uint64_t* hist_gt, sc_stream stream);
 
+/* ---- Host-resident batches ----------------------------------------------------------------
+ * The logits of a training set often live in host memory (a data loader's pinned buffers).
+ * sc_stager owns the device side of moving them: chunk_bytes of device staging twice over,
+ * a copy stream and its events, allocated once (hot calls never allocate).  One stager serves
+ * one call at a time (calls on different streams need different stagers).
+ *   chunk_bytes  bytes of logits per chunk (>= one row; e.g. 256 MiB); rounded up to 256.
+ * Errors: SC_ERR_INVALID_ARG (chunk_bytes < 1), SC_ERR_OOM, SC_ERR_CUDA. */
+typedef struct sc_stager_s* sc_stager;
+sc_status sc_stager_create(int64_t chunk_bytes, sc_stager* out);
+/* Waits for the stager's copies; NULL is a no-op. */
+sc_status sc_stager_free(sc_stager stager);
+
+typedef enum {
+  SC_HOST_AUTO = 0,       /* ZERO_COPY when the rows are page-locked and the context reads few
+                             128-B lines of a row (the sparse gather kernel's regime), else COPY */
+  SC_HOST_COPY = 1,       /* chunked host->device copies on the stager's copy stream, double-
+                             buffered: chunk i's pass overlaps chunk i+1's copy */
+  SC_HOST_ZERO_COPY = 2   /* the kernels read the page-locked host rows in place: only the lines
+                             holding mapped labels cross the host link */
+} sc_host_mode;
+
+/* sc_loss_fwd_bwd_host — sc_loss_fwd_bwd (the same pass, outputs and accumulation, Eq.
+ * api_output PAPER.md:2035 and the other patterns) over logits in HOST memory:
+ * batch->logits is a host pointer ([rows, ld] row-major, 16-B aligned, ld*elt % 16 == 0;
+ * page-locked — cudaHostAlloc / cudaHostRegister — for COPY to overlap and for ZERO_COPY at
+ * all).  Every other pointer (gt_mask / gt_off / gt_lab / app, w, all outputs) is a DEVICE
+ * pointer exactly as in sc_loss_fwd_bwd; per-row outputs are written for all `rows`.
+ * Asynchronous with respect to the host, stream-ordered on `stream` (the host rows must stay
+ * valid until it completes).
+ *   mode     sc_host_mode; *mode_used (may be NULL) receives the mode taken.
+ * Errors: as sc_loss_fwd_bwd; SC_ERR_INVALID_ARG for a NULL stager in COPY mode, a row wider
+ * than the stager's chunk, or ZERO_COPY on pageable memory. */
+sc_status sc_loss_fwd_bwd_host(sc_context ctx, sc_stager stager, const sc_batch* batch, int32_t mode,
+                               const float* w, float grad_scale, double* loss_sum, float* loss_row,
+                               int32_t* grad_idx, float* grad_val, float* grad_dense, uint8_t* decision,
+                               uint64_t* n_incorrect, uint64_t* hist_pred, uint64_t* hist_gt,
+                               int32_t* mode_used, sc_stream stream);
+
 /* ---- One read, many contexts (NEXT f3) ------------------------------------------------
  * sc_decide_all_apps — every row is evaluated under EVERY application of the context
  * (the provider's what-if: which applications would these outputs mislead), reading the
@@ -286,15 +324,17 @@ const char* sc_sample_last_error(void);
  * only reads maxima over 𝕎: the head is compiled down to the |𝕎|
  * mapped rows of W, computed on the tensor cores (tcgen05, bf16 operands, fp32
  * accumulation in TMEM), and the decision, counters, loss and gradient are produced in the
- * GEMM's epilogue.  The logits never reach HBM.  API-output order, one application.
+ * GEMM's epilogue.  The logits never reach HBM.  Every decision pattern (the context's
+ * order: API-output, application-choice, Multi-Select — PAPER.md:2022-2055), one application.
  *
  * sc_head_load — compile the head for ctx: copies the mapped rows of W (in label order),
  * their bias and keys into a device buffer the head owns (W and bias are not referenced
  * afterwards).
  *   weight  device bf16 (uint16 bit patterns) [C][ldw], ldw >= d;  d >= 1.
  *   bias    device float [C] or NULL (0).
- * SC_ERR_UNSUPPORTED: order != API_OUTPUT, n_apps != 1, or more than 512 head columns
- * (see sc_head_info).
+ * SC_ERR_UNSUPPORTED: n_apps != 1, or more than 4096 head columns (see sc_head_info).
+ * The head is compiled for the context's pattern (Multi-Select: a label in several lists has
+ * a column in each) and may only be used with contexts of that pattern (SC_ERR_INVALID_ARG).
  * The copy is enqueued on `stream`; the head is usable on that stream when this returns. */
 typedef struct sc_head_s* sc_head;
 sc_status sc_head_load(sc_context ctx, const uint16_t* weight, int64_t ldw, int64_t d, const float* bias,
@@ -302,7 +342,10 @@ sc_status sc_head_load(sc_context ctx, const uint16_t* weight, int64_t ldw, int6
 sc_status sc_head_free(sc_head head);
 /* d, and the number of head columns computed per row: the mapped labels grouped by list
  * (code order, ascending label id inside a list), each list padded to a multiple of 16,
- * the total to a multiple of 32.  SC_ERR_UNSUPPORTED from sc_head_load when that exceeds 512. */
+ * the total to a multiple of 32.  Up to 512 columns live in tensor memory at once; wider
+ * heads (e.g. the OpenImages-shaped 1000 mapped labels) run in equal
+ * column passes of <= 256 columns (padded to a multiple of the pass width), the features
+ * re-read from L2 per pass.  SC_ERR_UNSUPPORTED from sc_head_load above 4096. */
 sc_status sc_head_info(sc_head head, int64_t* d, int32_t* n_cols);
 
 typedef struct {
@@ -315,8 +358,8 @@ typedef struct {
 } sc_head_batch;
 
 /* sc_head_loss_fwd_bwd — z_i = x_i W_𝕎ᵀ + b_𝕎 (fp32 accumulation of bf16 products, then
- * + bias in fp32), then exactly sc_loss_fwd_bwd's outputs for those logits (S = 2 slots;
- * grad_idx holds label ids in [0, C), grad_val = dL_i/dz_c).  Every output may be NULL;
+ * + bias in fp32), then exactly sc_loss_fwd_bwd's outputs for those logits (S =
+ * sc_context_order's grad_slots; grad_idx holds label ids in [0, C), grad_val = dL_i/dz_c).  Every output may be NULL;
  * the loss is computed when loss_sum, loss_row, grad_idx or grad_val is given, which needs
  * the ground truth, as do n_incorrect and hist_gt.  The gradient w.r.t. x and W follows
  * from grad_idx/grad_val (at most two rows of W per sample) and is the caller's. */

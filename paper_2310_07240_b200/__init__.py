@@ -23,6 +23,7 @@ __all__ = [
     "sc_context_free", "sc_decide", "sc_decision_hist",
     "sc_weights_from_hist", "sc_decision_hist_weights", "sc_loss_fwd_bwd", "Head", "sc_head_load",
     "sc_head_loss_fwd_bwd", "sc_last_error", "sc_launch_count", "sc_last_kernel", "library_path",
+    "Stager", "sc_loss_fwd_bwd_host", "SC_HOST_AUTO", "SC_HOST_COPY", "SC_HOST_ZERO_COPY",
 ]
 
 SC_OK, SC_ERR_INVALID_ARG, SC_ERR_OOM, SC_ERR_CUDA, SC_ERR_UNSUPPORTED = range(5)
@@ -96,6 +97,13 @@ def _load():
     lib.sc_weights_from_hist.argtypes = [P, P, P, P]
     lib.sc_loss_fwd_bwd.restype = ctypes.c_int
     lib.sc_loss_fwd_bwd.argtypes = [P, ctypes.POINTER(_CBatch), P, F, P, P, P, P, P, P, P, P, P, P]
+    lib.sc_stager_create.restype = ctypes.c_int
+    lib.sc_stager_create.argtypes = [I64, ctypes.POINTER(P)]
+    lib.sc_stager_free.restype = ctypes.c_int
+    lib.sc_stager_free.argtypes = [P]
+    lib.sc_loss_fwd_bwd_host.restype = ctypes.c_int
+    lib.sc_loss_fwd_bwd_host.argtypes = [P, P, ctypes.POINTER(_CBatch), I32, P, F, P, P, P, P, P, P, P, P, P,
+                                         ctypes.POINTER(I32), P]
     lib.sc_last_error.restype = ctypes.c_char_p
     lib.sc_last_error.argtypes = []
     lib.sc_launch_count.restype = ctypes.c_uint64
@@ -415,6 +423,72 @@ def sc_loss_fwd_bwd(ctx: Context, batch: Batch, w=None, grad_scale: float = 1.0,
         _u64(hist_gt, "hist_gt", ctx.n_apps * 256), _stream(stream)))
 
 
+# ------------------------------------------------------------------ host-resident batches
+
+SC_HOST_AUTO, SC_HOST_COPY, SC_HOST_ZERO_COPY = 0, 1, 2
+
+
+class Stager:
+    """Handle to an ``sc_stager``: device staging (two chunks of ``chunk_bytes``), a copy
+    stream and its events, for sc_loss_fwd_bwd_host.  One call at a time per stager."""
+
+    def __init__(self, chunk_bytes: int = 256 << 20):
+        h = ctypes.c_void_p()
+        _check(_lib.sc_stager_create(int(chunk_bytes), ctypes.byref(h)))
+        self._h = h
+        self.chunk_bytes = int(chunk_bytes)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def free(self):
+        if getattr(self, "_h", None):
+            _lib.sc_stager_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def sc_loss_fwd_bwd_host(ctx: Context, stager: Optional[Stager], batch: Batch, mode: int = SC_HOST_AUTO, w=None,
+                         grad_scale: float = 1.0, loss_sum=None, loss_row=None, grad_idx=None, grad_val=None,
+                         grad_dense=None, decision=None, n_incorrect=None, hist_pred=None, hist_gt=None,
+                         stream=None) -> int:
+    """sc_loss_fwd_bwd over HOST logits (batch.logits: a pinned CPU tensor; everything else on
+    the device).  Returns the sc_host_mode taken (COPY: chunked, double-buffered H2D inside
+    libsc; ZERO_COPY: the kernels read the pinned rows in place)."""
+    torch = _torch()
+    lg = batch.logits
+    if lg is None or lg.is_cuda or lg.dim() != 2 or lg.stride(1) != 1:
+        raise ValueError("batch.logits must be a 2-D host tensor with unit column stride")
+    if lg.dtype not in (torch.float32, torch.bfloat16):
+        raise TypeError("logits dtype must be float32 or bfloat16")
+    gpu_part = Batch(logits=None, gt_off=batch.gt_off, gt_lab=batch.gt_lab, gt_mask=batch.gt_mask, app=batch.app,
+                     rows=lg.size(0))
+    cb = gpu_part._c()
+    cb.logits = lg.data_ptr()
+    cb.dtype = SC_F32 if lg.dtype == torch.float32 else SC_BF16
+    cb.ld = lg.stride(0) if lg.size(0) > 1 else max(lg.stride(0), lg.size(1))
+    used = ctypes.c_int32(-1)
+    _check(_lib.sc_loss_fwd_bwd_host(
+        ctx.handle, stager.handle if stager is not None else None, ctypes.byref(cb), int(mode),
+        _dev_ptr(w, "w", (torch.float32,), ctx.n_apps * 256), float(grad_scale),
+        _dev_ptr(loss_sum, "loss_sum", (torch.float64,), ctx.n_apps),
+        _dev_ptr(loss_row, "loss_row", (torch.float32,), cb.rows),
+        _dev_ptr(grad_idx, "grad_idx", (torch.int32,), ctx.grad_slots * cb.rows),
+        _dev_ptr(grad_val, "grad_val", (torch.float32,), ctx.grad_slots * cb.rows),
+        _dev_ptr(grad_dense, "grad_dense", (torch.float32,), cb.rows * cb.ld),
+        _dev_ptr(decision, "decision", (torch.uint8,), cb.rows),
+        _u64(n_incorrect, "n_incorrect", ctx.n_apps),
+        _u64(hist_pred, "hist_pred", ctx.n_apps * 256),
+        _u64(hist_gt, "hist_gt", ctx.n_apps * 256), ctypes.byref(used), _stream(stream)))
+    return used.value
+
+
 # ------------------------------------------------------------------ classifier head (NEXT f4)
 
 class Head:
@@ -479,8 +553,8 @@ def sc_head_loss_fwd_bwd(ctx: Context, head: Head, x, gt_off=None, gt_lab=None, 
         _dev_ptr(w, "w", (torch.float32,), 256), float(grad_scale),
         _dev_ptr(loss_sum, "loss_sum", (torch.float64,), 1),
         _dev_ptr(loss_row, "loss_row", (torch.float32,), rows),
-        _dev_ptr(grad_idx, "grad_idx", (torch.int32,), 2 * rows),
-        _dev_ptr(grad_val, "grad_val", (torch.float32,), 2 * rows),
+        _dev_ptr(grad_idx, "grad_idx", (torch.int32,), ctx.grad_slots * rows),
+        _dev_ptr(grad_val, "grad_val", (torch.float32,), ctx.grad_slots * rows),
         _dev_ptr(decision, "decision", (torch.uint8,), rows),
         _u64(n_incorrect, "n_incorrect", 1), _u64(hist_pred, "hist_pred", 256), _u64(hist_gt, "hist_gt", 256),
         _stream(stream)))

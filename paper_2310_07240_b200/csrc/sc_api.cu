@@ -4,6 +4,7 @@
 #include "sc_host.h"
 #include "sc_internal.cuh"
 
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstdarg>
@@ -696,6 +697,130 @@ sc_status sc_weights_from_hist(sc_context ctx, const uint64_t* hist_gt, float* w
                                          static_cast<cudaStream_t>(stream)))
     return cuda_fail(e, "weights kernel launch");
   g_launches.fetch_add(1, std::memory_order_relaxed);
+  return SC_OK;
+}
+
+}  // extern "C"
+
+struct sc_stager_s {
+  int device = 0;
+  int64_t chunk_bytes = 0;
+  void* buf[2] = {nullptr, nullptr};
+  cudaStream_t copy = nullptr;
+  cudaEvent_t ready[2] = {nullptr, nullptr};  // chunk copied (copy stream)
+  cudaEvent_t free_[2] = {nullptr, nullptr};  // the pass that read the buffer is done (caller's stream)
+};
+
+extern "C" {
+
+sc_status sc_stager_create(int64_t chunk_bytes, sc_stager* out) {
+  if (!out) return fail(SC_ERR_INVALID_ARG, "out is NULL");
+  *out = nullptr;
+  if (chunk_bytes < 1) return fail(SC_ERR_INVALID_ARG, "chunk_bytes < 1");
+  sc_stager s = new sc_stager_s;
+  s->chunk_bytes = round_up(chunk_bytes, 256);
+  cudaError_t e = cudaGetDevice(&s->device);
+  for (int i = 0; i < 2 && !e; ++i) e = cudaMalloc(&s->buf[i], static_cast<size_t>(s->chunk_bytes));
+  if (!e) e = cudaStreamCreateWithFlags(&s->copy, cudaStreamNonBlocking);
+  for (int i = 0; i < 2 && !e; ++i) e = cudaEventCreateWithFlags(&s->ready[i], cudaEventDisableTiming);
+  for (int i = 0; i < 2 && !e; ++i) e = cudaEventCreateWithFlags(&s->free_[i], cudaEventDisableTiming);
+  if (e) {
+    sc_stager_free(s);
+    return cuda_fail(e, "sc_stager_create");
+  }
+  *out = s;
+  return SC_OK;
+}
+
+sc_status sc_stager_free(sc_stager s) {
+  if (!s) return SC_OK;
+  if (s->copy) cudaStreamSynchronize(s->copy);
+  for (int i = 0; i < 2; ++i) {
+    if (s->free_[i]) cudaEventSynchronize(s->free_[i]);
+    cudaFree(s->buf[i]);
+    if (s->ready[i]) cudaEventDestroy(s->ready[i]);
+    if (s->free_[i]) cudaEventDestroy(s->free_[i]);
+  }
+  if (s->copy) cudaStreamDestroy(s->copy);
+  delete s;
+  return SC_OK;
+}
+
+sc_status sc_loss_fwd_bwd_host(sc_context ctx, sc_stager stg, const sc_batch* batch, int32_t mode, const float* w,
+                               float grad_scale, double* loss_sum, float* loss_row, int32_t* grad_idx,
+                               float* grad_val, float* grad_dense, uint8_t* decision, uint64_t* n_incorrect,
+                               uint64_t* hist_pred, uint64_t* hist_gt, int32_t* mode_used, sc_stream stream) {
+  if (sc_status s = check_batch_common(ctx, batch)) return s;
+  if (mode < SC_HOST_AUTO || mode > SC_HOST_ZERO_COPY) return fail(SC_ERR_INVALID_ARG, "unknown host mode %d", mode);
+  if (batch->dtype != SC_F32 && batch->dtype != SC_BF16) return fail(SC_ERR_INVALID_ARG, "unknown dtype");
+  const int64_t elt = batch->dtype == SC_F32 ? 4 : 2;
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // page-locked host rows have a device address (UVA): the kernels can read them in place
+  void* dev_alias = nullptr;
+  if (batch->logits) {
+    cudaPointerAttributes pa{};
+    if (cudaPointerGetAttributes(&pa, batch->logits) == cudaSuccess && pa.type == cudaMemoryTypeHost)
+      dev_alias = pa.devicePointer;
+    cudaGetLastError();  // pageable memory reports an error on some drivers: not sticky
+  }
+  int32_t m = mode;
+  if (m == SC_HOST_AUTO) {
+    // zero copy pays where the gather kernel runs: whole 128-B lines of a row stay untouched
+    // (B200, cfg3 f32: 1.46x over copy-then-compute); dense contexts copy
+    const int dt = batch->dtype == SC_BF16 ? 1 : 0;
+    const int64_t lines_row = (static_cast<int64_t>(std::max(ctx->ncols, 1)) * elt + 127) / 128;
+    const double frac = static_cast<double>(ctx->touched_lines[dt]) / (static_cast<double>(lines_row) * ctx->n_apps);
+    const bool sparse = ctx->max_ent <= 1024 && ctx->order == SC_ORDER_API_OUTPUT && frac <= gather_threshold(ctx->n_apps);
+    m = (dev_alias && sparse) ? SC_HOST_ZERO_COPY : SC_HOST_COPY;
+  }
+  if (mode_used) *mode_used = m;
+  if (m == SC_HOST_ZERO_COPY) {
+    if (batch->rows > 0 && !dev_alias)
+      return fail(SC_ERR_INVALID_ARG, "SC_HOST_ZERO_COPY needs page-locked host logits");
+    sc_batch b = *batch;
+    b.logits = dev_alias;
+    return run_eval(ctx, &b, w, grad_scale, loss_sum, loss_row, grad_idx, grad_val, grad_dense, decision,
+                    n_incorrect, hist_pred, hist_gt, true, st);
+  }
+  if (!stg) return fail(SC_ERR_INVALID_ARG, "SC_HOST_COPY needs a stager");
+  if (batch->rows == 0) return run_eval(ctx, batch, w, grad_scale, loss_sum, loss_row, grad_idx, grad_val,
+                                        grad_dense, decision, n_incorrect, hist_pred, hist_gt, true, st);
+  if (!batch->logits) return fail(SC_ERR_INVALID_ARG, "logits is NULL");
+  const int64_t row_bytes = batch->ld * elt;
+  if (row_bytes <= 0 || row_bytes > stg->chunk_bytes)
+    return fail(SC_ERR_INVALID_ARG, "a row (%lld B) is wider than the stager's chunk (%lld B)",
+                (long long)row_bytes, (long long)stg->chunk_bytes);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev != stg->device) return fail(SC_ERR_INVALID_ARG, "the stager belongs to device %d", stg->device);
+  const int S = ctx->order == SC_ORDER_MULTI_SELECT ? 8 : 2;
+  const int64_t chunk_rows = stg->chunk_bytes / row_bytes;
+  // buffers are free once every earlier use on `stream` is done
+  for (int i = 0; i < 2; ++i)
+    if (cudaError_t e = cudaEventRecord(stg->free_[i], st)) return cuda_fail(e, "cudaEventRecord");
+  const uint8_t* host = static_cast<const uint8_t*>(batch->logits);
+  for (int64_t lo = 0, ci = 0; lo < batch->rows; lo += chunk_rows, ++ci) {
+    const int64_t nr = std::min<int64_t>(chunk_rows, batch->rows - lo);
+    const int k = static_cast<int>(ci & 1);
+    cudaError_t e = cudaStreamWaitEvent(stg->copy, stg->free_[k], 0);
+    if (!e) e = cudaMemcpyAsync(stg->buf[k], host + lo * row_bytes, static_cast<size_t>(nr * row_bytes),
+                                cudaMemcpyHostToDevice, stg->copy);
+    if (!e) e = cudaEventRecord(stg->ready[k], stg->copy);
+    if (!e) e = cudaStreamWaitEvent(st, stg->ready[k], 0);
+    if (e) return cuda_fail(e, "sc_loss_fwd_bwd_host: staging copy");
+    sc_batch b = *batch;
+    b.logits = stg->buf[k];
+    b.rows = nr;
+    b.gt_mask = batch->gt_mask ? batch->gt_mask + lo : nullptr;
+    b.gt_off = batch->gt_mask ? nullptr : (batch->gt_off ? batch->gt_off + lo : nullptr);
+    b.app = batch->app ? batch->app + lo : nullptr;
+    if (sc_status s = run_eval(ctx, &b, w, grad_scale, loss_sum, loss_row ? loss_row + lo : nullptr,
+                               grad_idx ? grad_idx + S * lo : nullptr, grad_val ? grad_val + S * lo : nullptr,
+                               grad_dense ? grad_dense + lo * batch->ld : nullptr, decision ? decision + lo : nullptr,
+                               n_incorrect, hist_pred, hist_gt, true, st))
+      return s;
+    if (cudaError_t e2 = cudaEventRecord(stg->free_[k], st)) return cuda_fail(e2, "cudaEventRecord");
+  }
   return SC_OK;
 }
 

@@ -48,6 +48,8 @@ constexpr int kBM = 128;           // rows per tile (UMMA M)
 constexpr int kBK = 64;            // bf16 elements per k-block = one 128-B swizzle row
 constexpr int kHeadThreads = 352;  // 11 warps: x / MMA / 4 epilogue / W / 4 epilogue (second tile)
 constexpr int kMaxCols = 512;      // TMEM columns
+constexpr int kPassCols = 256;     // columns per pass when a head has more than kMaxCols (one MMA, N <= 256)
+constexpr int kMaxHeadCols = 4096; // keys + bias tables in shared memory (32 KB)
 constexpr int kMaxLists = 8;
 
 struct HeadParams {
@@ -75,6 +77,10 @@ struct HeadParams {
   int32_t list_col0[kMaxLists];  // first column of list j (multiple of 16)
   int32_t list_nch[kMaxLists];   // 16-column groups of list j
   int32_t probe;            // experiment (SC_HEAD_PROBE): bit 0 skips the epilogue's reduction, bit 1 the MMAs
+  int32_t n_pass;           // column passes per row tile: 1 = every column in TMEM at once (n_cols <= 512);
+                            // > 1 = pass_w columns per pass, x re-streamed per pass (from L2)
+  int32_t pass_w;           // columns per pass (n_pass > 1; = chunk)
+  int32_t pat;              // 0: API-output order (split maxima); 1: per-list patterns (finish_lists_core)
 };
 
 // ------------------------------------------------------------------ tcgen05 / TMA / cluster PTX
@@ -120,6 +126,12 @@ __device__ __forceinline__ void tma_3d(void* dst, const CUtensorMap* map, int32_
 __device__ __forceinline__ uint64_t evict_last_policy() {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+__device__ __forceinline__ uint64_t evict_normal_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
   return pol;
 }
 
@@ -264,8 +276,10 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
   uint64_t* tempty = tfull + 2;               // [2]         (PAIR: the leader's counts both CTAs)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
-  // rows per unit: a CTA pair's two tiles, or p.tiles tiles of one CTA that share each W stage
-  const int kUnit = PAIR ? 2 * kBM : p.tiles * kBM;
+  // rows per unit: p.tiles row tiles sharing each W stage, of 128 rows (one CTA) or 256 rows
+  // (a CTA pair: rows [t*256, t*256 + 128) in CTA 0, the next 128 in CTA 1)
+  const int kTileRows = PAIR ? 2 * kBM : kBM;
+  const int kUnit = p.tiles * kTileRows;
 
   for (int i = tid; i < p.n_cols; i += blockDim.x) {
     s_keys[i] = __ldg(p.keys + i);
@@ -282,7 +296,7 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(tfull + b, 1);
-      mbar_init(tempty + b, PAIR ? 8 : 4 * p.tiles);  // one arrive per working epilogue warp (of both CTAs)
+      mbar_init(tempty + b, (PAIR ? 8 : 4) * p.tiles);  // one arrive per working epilogue warp (of both CTAs)
     }
     fence_mbar_init();
   }
@@ -317,28 +331,32 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- x producer: kbs k-blocks of this CTA's 128 rows per stage (from HBM)
-      const uint64_t pol_x = evict_first_policy();
+      const uint64_t pol_first = evict_first_policy();
+      const uint64_t pol_keep = evict_normal_policy();  // column passes: the tile is read again from L2
       const uint32_t tx = static_cast<uint32_t>(p.x_stage_bytes);
       int s = 0;
       uint32_t ph = 0;
       for (int64_t st = 0; st < n_steps; ++st) {
         // may be past the last row: TMA fills zeros, the epilogue skips those rows
         const int32_t row0 = static_cast<int32_t>((unit0 + st * n_grid_units) * kUnit + rank * kBM);
+        for (int ps = 0; ps < p.n_pass; ++ps) {
+        const uint64_t pol_x = ps + 1 < p.n_pass ? pol_keep : pol_first;
         for (int xb = 0; xb < p.n_xb; ++xb) {
           mbar_wait(xempty + s, ph ^ 1u);
           uint8_t* stg = sm + static_cast<size_t>(s) * p.x_stage_bytes;
           const uint32_t fb = xfull_l + 8u * s;
           if (rank == 0) mbar_arrive_expect_tx(xfull + s, tx);
           else mbar_arrive_expect_tx_cl(fb, tx);
-          for (int t = 0; t < (PAIR ? 1 : p.tiles); ++t) {  // tile t: kbs k-blocks at t * kbs * 16 KB
+          for (int t = 0; t < p.tiles; ++t) {  // tile t: kbs k-blocks at t * kbs * 16 KB
             uint8_t* dst = stg + static_cast<size_t>(t) * p.kbs * (kBM * kBK * 2);
-            if (p.x3d) tma_3d<PAIR>(dst, &map_x, 0, row0 + t * kBM, xb * p.kbs, fb, pol_x);
-            else tma_2d<PAIR>(dst, &map_x, xb * kBK, row0 + t * kBM, fb, pol_x);
+            if (p.x3d) tma_3d<PAIR>(dst, &map_x, 0, row0 + t * kTileRows, xb * p.kbs, fb, pol_x);
+            else tma_2d<PAIR>(dst, &map_x, xb * kBK, row0 + t * kTileRows, fb, pol_x);
           }
           if (++s == p.x_stages) {
             s = 0;
             ph ^= 1u;
           }
+        }
         }
       }
     }
@@ -351,6 +369,8 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
       int s = 0;
       uint32_t ph = 0;
       for (int64_t st = 0; st < n_steps; ++st) {
+        for (int ps = 0; ps < p.n_pass; ++ps) {
+        const int col0 = ps * p.pass_w;  // 0 when n_pass == 1
         for (int kb = 0; kb < p.n_kb; ++kb) {
           mbar_wait(wempty + s, ph ^ 1u);
           uint8_t* stg = sm + p.w_ring_off + static_cast<size_t>(s) * p.w_stage_bytes;
@@ -359,11 +379,12 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
           else mbar_arrive_expect_tx_cl(fb, tx);
           for (int c = 0; c < p.n_chunks; ++c)
             tma_2d<PAIR>(stg + c * rows_c * (kBK * 2), &map_w, 0,
-                         kb * p.n_cols + c * p.chunk + static_cast<int>(rank) * rows_c, fb, pol_w);
+                         kb * p.n_cols + col0 + c * p.chunk + static_cast<int>(rank) * rows_c, fb, pol_w);
           if (++s == p.w_stages) {
             s = 0;
             ph ^= 1u;
           }
+        }
         }
       }
     }
@@ -379,16 +400,19 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
       const uint64_t w_step = static_cast<uint32_t>(p.w_stage_bytes) >> 4;
       const uint64_t c_step = static_cast<uint32_t>((PAIR ? p.chunk / 2 : p.chunk) * kBK * 2) >> 4;
       const bool two = p.n_chunks == 2;
-      const bool tile2 = !PAIR && p.tiles == 2;                               // n_chunks == 1 then
+      const bool tile2 = p.tiles == 2;                                        // n_chunks == 1 then
       const uint64_t t_step = static_cast<uint32_t>(p.kbs * a_bytes) >> 4;  // tile 1 in an x stage
       const bool no_mma = (p.probe & 2) != 0;
       int xs = 0, ws = 0, b = 0;
       uint32_t xph = 0, wph = 0, tph[2] = {0, 0};
+      // accumulator buffer b at column b * acc_stride (a column pass holds pass_w columns)
+      const int acc_stride = p.n_pass > 1 ? p.pass_w : p.n_cols;
       for (int64_t st = 0; st < n_steps; ++st) {
+        for (int ps = 0; ps < p.n_pass; ++ps) {
         mbar_wait(tempty + b, tph[b] ^ 1u);  // the epilogue(s) drained this accumulator
         tph[b] ^= 1u;
         tc_fence_after();
-        const uint32_t acc = tmem_base + static_cast<uint32_t>(b * p.n_cols);
+        const uint32_t acc = tmem_base + static_cast<uint32_t>(b * acc_stride);
         for (int xb = 0; xb < p.n_xb; ++xb) {
           mbar_wait(xfull + xs, xph);
           tc_fence_after();
@@ -424,9 +448,10 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
         }
         umma_commit<PAIR>(tfull + b);  // accumulator complete (in both CTAs)
         if (p.acc_bufs == 2) b ^= 1;
+        }
       }
     }
-  } else if (warp <= 5 || (warp >= 7 && warp <= 10 && !PAIR && p.tiles == 2)) {
+  } else if (warp <= 5 || (warp >= 7 && warp <= 10 && p.tiles == 2)) {
     // ---------------- epilogue: one row per thread
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     const uint32_t lane_base = static_cast<uint32_t>(32 * q) << 16;
@@ -437,66 +462,65 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
     uint32_t tph[2] = {0, 0};
     RowBatch rb;
     rb.n = 0;
-    const int ntile = PAIR ? 1 : p.tiles;
-    // two tiles per unit: warps 2-5 drain tile 0, warps 7-10 tile 1 (lane quarters 3,0,1,2)
-    const int t_lo = ntile == 2 ? (warp >= 7 ? 1 : 0) : 0;
-    const int t_hi = ntile == 2 ? t_lo + 1 : 1;
+    const int ntile = p.tiles;
+    // two tiles per unit: warps 2-5 drain tile 0, warps 7-10 tile 1 (lane quarters 3,0,1,2);
+    // each warp drains one tile
+    const int t = ntile == 2 ? (warp >= 7 ? 1 : 0) : 0;
+    const int acc_stride = p.n_pass > 1 ? p.pass_w : p.n_cols;
     for (int64_t st = 0; st < n_steps; ++st) {
-      const int64_t first0 = (unit0 + st * n_grid_units) * kUnit + rank * kBM + 32 * q;
-      // G_i of each tile's row before waiting on the accumulator (overlaps the MMA)
-      uint32_t Gt[2] = {0u, 0u};
-#pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        const int64_t row = first0 + t * kBM + lane;
-        if (t >= t_lo && t < t_hi && row < p.rows) {
-          uint32_t G = 0;
-          if (ep.gt_mask) {
-            G = __ldg(ep.gt_mask + row);
-          } else if (ep.gt_off) {
-            const int64_t g0 = __ldg(ep.gt_off + row), g1 = __ldg(ep.gt_off + row + 1);
-            for (int64_t i = g0; i < g1; ++i) G |= label_lists(__ldg(cat + __ldg(ep.gt_lab + i)), kApiOutput);
-          }
-          Gt[t] = G;
+      const int64_t first = (unit0 + st * n_grid_units) * kUnit + t * kTileRows + rank * kBM + 32 * q;
+      const int64_t row = first + lane;
+      // G_i of the row before waiting on the accumulator (overlaps the MMA)
+      uint32_t G = 0;
+      if (row < p.rows) {
+        if (ep.gt_mask) {
+          G = __ldg(ep.gt_mask + row);
+        } else if (ep.gt_off) {
+          const int64_t g0 = __ldg(ep.gt_off + row), g1 = __ldg(ep.gt_off + row + 1);
+          for (int64_t i = g0; i < g1; ++i) G |= label_lists(__ldg(cat + __ldg(ep.gt_lab + i)), ep.ctx.order);
         }
       }
-      mbar_wait(tfull + b, tph[b]);
-      tph[b] ^= 1u;
-      tc_fence_after();
-      float zpt[2], zmt[2];
-      uint32_t kpt[2], kmt[2];
+      // per-list arg max over the list's 16-column groups, in column order (a list's columns
+      // hold its labels ascending, so strict > keeps the smaller label on ties); the state
+      // (list j, group g, running max) carries across column passes
+      float lz[kMaxLists];
+      int lc[kMaxLists];
 #pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        if (t < t_lo || t >= t_hi) continue;
-        const uint32_t acc = tmem_base + lane_base + static_cast<uint32_t>((b + t) * p.n_cols);
-        // per-list arg max over the list's 16-column groups; the next group's load is in
-        // flight while the current one is reduced
-        float lz[kMaxLists];
-        int lc[kMaxLists];
-#pragma unroll
-        for (int j = 0; j < kMaxLists; ++j) {
-          lz[j] = -CUDART_INF_F;
-          lc[j] = -1;
-        }
+      for (int jj = 0; jj < kMaxLists; ++jj) {
+        lz[jj] = -CUDART_INF_F;
+        lc[jj] = -1;
+      }
+      int j = 0, g = 0;  // list, group within the list
+      while (j < D && p.list_nch[j] == 0) ++j;
+      if (p.probe & 1) j = D;
+      float run_z = -CUDART_INF_F;
+      int run_c = -1;
+      for (int ps = 0; ps < p.n_pass; ++ps) {
+        const int c_lo = p.n_pass > 1 ? ps * p.pass_w : 0;
+        const int c_hi = p.n_pass > 1 ? c_lo + p.pass_w : p.n_cols;
+        mbar_wait(tfull + b, tph[b]);
+        tph[b] ^= 1u;
+        tc_fence_after();
+        // column c of this pass lives at acc + c - c_lo
+        const uint32_t acc = tmem_base + lane_base +
+                             static_cast<uint32_t>(p.n_pass > 1 ? b * acc_stride : (b + t) * p.n_cols) -
+                             static_cast<uint32_t>(c_lo);
         uint32_t v[16], vn[16];
-        int j = 0, g = 0;  // list, group within the list
-        while (j < D && p.list_nch[j] == 0) ++j;
-        if (p.probe & 1) j = D;
-        if (j < D) {
-          tmem_ld16(acc + p.list_col0[j], v);
+        if (j < D && p.list_col0[j] + 16 * g < c_hi) {
+          tmem_ld16(acc + p.list_col0[j] + 16 * g, v);
           tmem_wait_ld(v);
         }
-        float run_z = -CUDART_INF_F;
-        int run_c = -1;
-        while (j < D) {
+        while (j < D && p.list_col0[j] + 16 * g < c_hi) {
           const int col = p.list_col0[j] + 16 * g;
-          // next group (warp-uniform)
+          // next group (warp-uniform); its load is in flight while this one is reduced
           int jn = j, gn = g + 1;
           if (gn == p.list_nch[jn]) {
             gn = 0;
             ++jn;
             while (jn < D && p.list_nch[jn] == 0) ++jn;
           }
-          if (jn < D) tmem_ld16(acc + p.list_col0[jn] + 16 * gn, vn);
+          const bool more = jn < D && p.list_col0[jn] + 16 * gn < c_hi;
+          if (more) tmem_ld16(acc + p.list_col0[jn] + 16 * gn, vn);
           float z[16];
           const float4* b4 = reinterpret_cast<const float4*>(s_bias + col);
 #pragma unroll
@@ -526,12 +550,27 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
           }
           j = jn;
           g = gn;
-          if (j < D) {
+          if (more) {
             tmem_wait_ld(vn);
 #pragma unroll
             for (int i = 0; i < 16; ++i) v[i] = vn[i];
           }
         }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {  // the MMA may overwrite this accumulator
+          if (rank == 0) mbar_arrive(tempty + b);
+          else mbar_arrive_cl(tempty_l + 8u * b);
+        }
+        if (p.acc_bufs == 2) b ^= 1;
+      }
+      const int64_t nrow = p.rows - first;
+      if (nrow <= 0) continue;  // warp-uniform
+      rb.G = G;
+      rb.app = 0;
+      rb.row = row;
+      rb.n = nrow < 32 ? static_cast<int>(nrow) : 32;
+      if (p.pat == 0) {
         // split maxima over the list winners: P⁺ over lists in G_i, P⁻ over the rest (A8)
         float zp = -CUDART_INF_F, zm = -CUDART_INF_F;
         uint32_t kp = kNone, km = kNone;
@@ -539,33 +578,25 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
         for (int jj = 0; jj < kMaxLists; ++jj) {
           if (lc[jj] >= 0) {
             const uint32_t key = s_keys[lc[jj]];
-            if ((Gt[t] >> jj) & 1u) {
+            if ((G >> jj) & 1u) {
               if (beats(lz[jj], key, zp, kp)) { zp = lz[jj]; kp = key; }
             } else {
               if (beats(lz[jj], key, zm, km)) { zm = lz[jj]; km = key; }
             }
           }
         }
-        zpt[t] = zp; kpt[t] = kp; zmt[t] = zm; kmt[t] = km;
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {  // the MMA may overwrite this accumulator
-        if (rank == 0) mbar_arrive(tempty + b);
-        else mbar_arrive_cl(tempty_l + 8u * b);
-      }
-      if (p.acc_bufs == 2) b ^= 1;
+        rb.zp = zp; rb.kp = kp; rb.zm = zm; rb.km = km;
+        finish_batch(ep, rb, nullptr, lane);
+      } else {
+        // application-choice order / Multi-Select: the list maxima P_j themselves
+        float zj[8];
+        uint32_t kj[8];
 #pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        if (t < t_lo || t >= t_hi) continue;
-        const int64_t first = first0 + t * kBM;
-        const int64_t nrow = p.rows - first;
-        if (nrow > 0) {
-          rb.zp = zpt[t]; rb.kp = kpt[t]; rb.zm = zmt[t]; rb.km = kmt[t]; rb.G = Gt[t]; rb.app = 0;
-          rb.row = first + lane;
-          rb.n = nrow < 32 ? static_cast<int>(nrow) : 32;
-          finish_batch(ep, rb, nullptr, lane);
+        for (int jj = 0; jj < 8; ++jj) {
+          zj[jj] = lz[jj];
+          kj[jj] = lc[jj] >= 0 ? s_keys[lc[jj]] : kNone;
         }
+        finish_lists_core(ep, rb, zj, kj, nullptr, lane);
       }
     }
   }
@@ -608,6 +639,8 @@ struct sc_head_s {
   int64_t d = 0, d_pad = 0;
   int32_t n_mapped = 0, n_cols = 0, chunk = 0, n_chunks = 0;
   int32_t n_lists = 0;
+  int32_t n_pass = 1, pass_w = 0;  // column passes (n_cols > 512)
+  int32_t order = 0;
   int32_t list_col0[sc::kMaxLists] = {}, list_nch[sc::kMaxLists] = {};
   uint16_t* Wm = nullptr;  // [n_kb][n_cols][64]
   float* bias = nullptr;   // [n_cols]
@@ -729,8 +762,7 @@ sc_status sc_head_load(sc_context ctx, const uint16_t* weight, int64_t ldw, int6
   if (!ctx || !weight || !out) return sc::set_error(SC_ERR_INVALID_ARG, "sc_head_load: NULL argument");
   *out = nullptr;
   if (d < 1 || ldw < d) return sc::set_error(SC_ERR_INVALID_ARG, "sc_head_load: need d >= 1 and ldw >= d");
-  if (ctx->order != SC_ORDER_API_OUTPUT || ctx->n_apps != 1)
-    return sc::set_error(SC_ERR_UNSUPPORTED, "sc_head_load: API-output order and one application only");
+  if (ctx->n_apps != 1) return sc::set_error(SC_ERR_UNSUPPORTED, "sc_head_load: one application only");
   if (d > (int64_t(1) << 31) - sc::kBK) return sc::set_error(SC_ERR_INVALID_ARG, "sc_head_load: d too large");
   const int32_t nm = ctx->n_mapped[0];
   const int32_t D = ctx->nlists[0];
@@ -742,10 +774,12 @@ sc_status sc_head_load(sc_context ctx, const uint16_t* weight, int64_t ldw, int6
   std::vector<uint32_t> keys;
   sc_head h = new sc_head_s;
   h->n_lists = D;
+  h->order = ctx->order;
+  // list j's columns: its member labels ascending (Multi-Select: a label sits in every list holding it)
   for (int32_t j = 0; j < D; ++j) {
     h->list_col0[j] = static_cast<int32_t>(col_label.size());
     for (int32_t t = 0; t < nm; ++t)
-      if ((ent[t] & 0xFFu) == static_cast<uint32_t>(j)) {
+      if ((sc::label_lists(static_cast<uint8_t>(ent[t] & 0xFFu), ctx->order) >> j) & 1u) {
         col_label.push_back(ctx->compact ? ctx->cols[ent[t] >> 8] : static_cast<int32_t>(ent[t] >> 8));  // W row
         keys.push_back(ent[t]);
       }
@@ -759,18 +793,32 @@ sc_status sc_head_load(sc_context ctx, const uint16_t* weight, int64_t ldw, int6
     col_label.push_back(-1);
     keys.push_back(sc::kNone);
   }
+  if (col_label.size() > static_cast<size_t>(sc::kMaxCols)) {
+    // more columns than TMEM holds: equal column passes of <= 256 (a multiple of 32) each,
+    // double-buffered in TMEM; the epilogue carries per-list maxima across passes
+    const int32_t n0 = static_cast<int32_t>(col_label.size());
+    h->n_pass = (n0 + sc::kPassCols - 1) / sc::kPassCols;
+    h->pass_w = ((n0 + h->n_pass - 1) / h->n_pass + 31) / 32 * 32;
+    while (static_cast<int32_t>(col_label.size()) < h->n_pass * h->pass_w) {
+      col_label.push_back(-1);
+      keys.push_back(sc::kNone);
+    }
+  }
   const int32_t n = static_cast<int32_t>(col_label.size());
-  if (n > sc::kMaxCols) {
+  if (n > sc::kMaxHeadCols) {
     sc_head_free(h);
     return sc::set_error(SC_ERR_UNSUPPORTED,
                          "sc_head_load: |W| = %d mapped labels need %d head columns (lists padded to 16) > %d", nm, n,
-                         sc::kMaxCols);
+                         sc::kMaxHeadCols);
   }
   h->d = d;
   h->d_pad = (d + 7) / 8 * 8;
   h->n_mapped = nm;
   h->n_cols = n;
-  if (n <= 256) {
+  if (h->n_pass > 1) {  // one MMA of pass_w columns per pass
+    h->chunk = h->pass_w;
+    h->n_chunks = 1;
+  } else if (n <= 256) {
     h->chunk = n;
     h->n_chunks = 1;
   } else {  // two MMAs of n/2 <= 256 columns
@@ -829,8 +877,9 @@ sc_status sc_head_loss_fwd_bwd(sc_context ctx, sc_head head, const sc_head_batch
                                float* grad_val, uint8_t* decision, uint64_t* n_incorrect, uint64_t* hist_pred,
                                uint64_t* hist_gt, sc_stream stream) {
   if (!ctx || !head || !batch) return sc::set_error(SC_ERR_INVALID_ARG, "sc_head_loss_fwd_bwd: NULL argument");
-  if (ctx->order != SC_ORDER_API_OUTPUT || ctx->n_apps != 1)
-    return sc::set_error(SC_ERR_UNSUPPORTED, "sc_head_loss_fwd_bwd: API-output order and one application only");
+  if (ctx->n_apps != 1) return sc::set_error(SC_ERR_UNSUPPORTED, "sc_head_loss_fwd_bwd: one application only");
+  if (ctx->order != head->order)
+    return sc::set_error(SC_ERR_INVALID_ARG, "sc_head_loss_fwd_bwd: the head was compiled for another context");
   const sc_head_batch& b = *batch;
   if (b.rows < 0) return sc::set_error(SC_ERR_INVALID_ARG, "sc_head_loss_fwd_bwd: rows < 0");
   if (b.rows > (int64_t(1) << 31) - (int64_t(1) << 20))
@@ -885,11 +934,15 @@ sc_status sc_head_loss_fwd_bwd(sc_context ctx, sc_head head, const sc_head_batch
   p.n_cols = head->n_cols;
   p.chunk = head->chunk;
   p.n_chunks = head->n_chunks;
-  p.acc_bufs = 2 * head->n_cols <= sc::kMaxCols ? 2 : 1;
+  p.n_pass = head->n_pass;
+  p.pass_w = head->pass_w;
+  p.pat = ctx->order == SC_ORDER_API_OUTPUT ? 0 : 1;
+  p.acc_bufs = (p.n_pass > 1 || 2 * head->n_cols <= sc::kMaxCols) ? 2 : 1;
   // lone CTAs: two 128-row tiles per unit share every W stage (W_𝕎, re-read from L2 for each
   // unit, moves half the bytes per row) when both accumulators fit TMEM; then single-buffered
   const char* t2env = std::getenv("SC_HEAD_T2");
-  const bool t2_ok = head->n_chunks == 1 && 2 * head->n_cols <= sc::kMaxCols && !(t2env && std::atoi(t2env) == 0);
+  const bool t2_ok = head->n_pass == 1 && head->n_chunks == 1 && 2 * head->n_cols <= sc::kMaxCols &&
+                     !(t2env && std::atoi(t2env) == 0);
   p.n_lists = head->n_lists;
   for (int j = 0; j < sc::kMaxLists; ++j) {
     p.list_col0[j] = head->list_col0[j];
@@ -909,9 +962,15 @@ sc_status sc_head_loss_fwd_bwd(sc_context ctx, sc_head head, const sc_head_batch
   bool x3d = false;
   size_t smem = 0;
   for (int attempt = 0; attempt < 2; ++attempt) {
-    const bool want_pair = attempt == 0;
-    p.w_stage_bytes = (want_pair ? head->n_cols / 2 : head->n_cols) * sc::kBK * 2;
-    p.tiles = (!want_pair && t2_ok) ? 2 : 1;
+    const bool want_pair = attempt == 0 && head->n_pass == 1;
+    if (attempt == 0 && !want_pair) continue;
+    // one k-block of the W rows an MMA pass reads (all n_cols, or pass_w in column passes)
+    const int32_t pass_cols = head->chunk * head->n_chunks;
+    p.w_stage_bytes = (want_pair ? pass_cols / 2 : pass_cols) * sc::kBK * 2;
+    // two row tiles per unit share every W stage (lone CTAs by default; CTA pairs with
+    // SC_HEAD_PAIR_T2=1: 512 rows per pass over W)
+    const char* pt2 = std::getenv("SC_HEAD_PAIR_T2");
+    p.tiles = (t2_ok && (!want_pair || (pt2 && std::atoi(pt2) == 1))) ? 2 : 1;
     // x: 3-D boxes of kbs k-blocks (rows read kbs*128 B at a time) when d % 64 == 0; as many
     // x bytes in flight as fit next to >= 3 W stages (>= 2 for wide heads)
     x3d = head->d % sc::kBK == 0 && !(std::getenv("SC_HEAD_X2D"));
@@ -971,8 +1030,9 @@ sc_status sc_head_loss_fwd_bwd(sc_context ctx, sc_head head, const sc_head_batch
     pair = want_pair;
     break;
   }
-  if (!pair && p.tiles == 2) p.acc_bufs = 1;  // both accumulators of a unit in TMEM at once
-  p.n_units = pair ? (b.rows + 2 * sc::kBM - 1) / (2 * sc::kBM) : (n_tiles + p.tiles - 1) / p.tiles;
+  if (p.tiles == 2) p.acc_bufs = 1;  // both accumulators of a unit in TMEM at once
+  const int64_t unit_rows = static_cast<int64_t>(p.tiles) * (pair ? 2 : 1) * sc::kBM;
+  p.n_units = (b.rows + unit_rows - 1) / unit_rows;
   CUtensorMap map_x;
   p.x3d = x3d ? 1 : 0;
   if (x3d ? !make_map3(&map_x, b.x, head->d, b.rows, b.ldx, p.kbs)

@@ -225,9 +225,6 @@ __device__ __forceinline__ void scan_lists(const LaneEnt<EPL>& le, int D, const 
   }
 }
 
-__device__ __forceinline__ void finish_lists_core(const EvalParams& p, RowBatch& b, const float (&zj)[8],
-                                                  const uint32_t (&kj)[8], const float* wtab_smem, int lane);
-
 // Epilogue of the application-choice order (Eq. app_choice) and Multi-Select (Eq.
 // multi-select) for the batch's rows, one row per lane; counters as in finish_batch.
 __device__ __forceinline__ void finish_lists(const EvalParams& p, RowBatch& b, ListBatch lb, const float* wtab_smem,
@@ -317,155 +314,6 @@ __device__ __forceinline__ void finish_slots(const EvalParams& p, RowBatch& b, c
     }
   }
   finish_lists_core(p, b, zj, kj, wtab_smem, lane);
-}
-
-__device__ __forceinline__ void finish_lists_core(const EvalParams& p, RowBatch& b, const float (&zj)[8],
-                                                  const uint32_t (&kj)[8], const float* wtab_smem, int lane) {
-  const bool active = lane < b.n;
-  const unsigned act = __ballot_sync(kFull, active);
-  const float tau = p.ctx.tau, theta = p.ctx.theta, k = p.ctx.k;
-  const bool ms = p.ctx.order == kMultiSelect;
-  const int S = ms ? 8 : 2;
-  uint32_t dec = 0, correct = 1;
-  float L = 0.f;
-  int32_t gi[8];
-  float gv[8];
-#pragma unroll
-  for (int q = 0; q < 8; ++q) { gi[q] = -1; gv[q] = 0.f; }
-  if (active) {
-    const int D = __ldg(p.ctx.nlists + b.app);
-    const uint32_t G = b.G;
-    const bool y = G != 0;
-    const float wi = p.w ? (wtab_smem ? wtab_smem[G] : __ldg(p.w + b.app * 256u + G)) : 1.f;
-    if (!ms) {
-      // application-choice order: the first list (code order) holding an output label
-      dec = static_cast<uint32_t>(D);
-#pragma unroll
-      for (int j = 7; j >= 0; --j)
-        if (kj[j] != kNone && zj[j] > tau) dec = static_cast<uint32_t>(j);
-      const int kk = y ? __ffs(G) - 1 : D;  // the ground truth's decision
-      correct = dec == static_cast<uint32_t>(kk);
-      if (p.want_loss) {
-        // competitor: lists j < k when y = 1 (P_{k⁻}), every list when y = 0 (P)
-        float zc = -CUDART_INF_F;
-        uint32_t kc = kNone;
-        float zk = -CUDART_INF_F;
-        uint32_t kk_key = kNone;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          if (j == kk) { zk = zj[j]; kk_key = kj[j]; }
-          const bool compete = y ? (j < kk) : (j < D);
-          if (compete && kj[j] != kNone && beats(zj[j], kj[j], zc, kc)) { zc = zj[j]; kc = kj[j]; }
-        }
-        if (y && kk_key != kNone) {
-          const bool c_over = kc != kNone && zc > tau;
-          const float am = c_over ? sigmoid_f(zc) : theta;  // max(θ, P_{k⁻})
-          const float x = am - sigmoid_f(zk);
-          const float ds = k * dsigmoid_f(k * x);
-          L = wi * sigmoid_f(k * x);
-          gi[0] = static_cast<int32_t>(kk_key >> 8);
-          gv[0] = -wi * ds * dsigmoid_f(zk) * p.grad_scale;
-          if (c_over) {
-            gi[1] = static_cast<int32_t>(kc >> 8);
-            gv[1] = wi * ds * dsigmoid_f(zc) * p.grad_scale;
-          }
-        } else if (!y && kc != kNone) {
-          const float x = sigmoid_f(zc) - theta;  // P − θ
-          L = wi * sigmoid_f(k * x);
-          gi[1] = static_cast<int32_t>(kc >> 8);
-          gv[1] = wi * k * dsigmoid_f(k * x) * dsigmoid_f(zc) * p.grad_scale;
-        }
-      }
-    } else {
-      // Multi-Select: every list holding an output label; exact match with G
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (kj[j] != kNone && zj[j] > tau) dec |= 1u << j;
-      correct = dec == G;
-      if (p.want_loss) {
-        float ell = 0.f;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          if (kj[j] != kNone) {
-            const float pj = sigmoid_f(zj[j]);
-            const bool yj = (G >> j) & 1u;
-            const float x = yj ? theta - pj : pj - theta;
-            ell += sigmoid_f(k * x);
-            const float g = wi * k * dsigmoid_f(k * x) * dsigmoid_f(zj[j]) * p.grad_scale;
-            gi[j] = static_cast<int32_t>(kj[j] >> 8);
-            gv[j] = yj ? -g : g;
-          }
-        }
-        L = wi * ell;
-      }
-    }
-    if (p.decision) p.decision[b.row] = static_cast<uint8_t>(dec);
-    if (p.want_loss) {
-      if (p.loss_row) p.loss_row[b.row] = L;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        if (q < S) {
-          if (p.grad_idx) p.grad_idx[S * b.row + q] = out_label(p.ctx, gi[q]);  // gi: logit columns
-          if (p.grad_val) p.grad_val[S * b.row + q] = gv[q];
-        }
-      }
-    }
-  }
-  if (p.hist_pred && active) {
-    const uint32_t key = b.app * 256u + dec;
-    const unsigned peers = __match_any_sync(act, key);
-    if (lane == __ffs(peers) - 1) atomicAdd(p.hist_pred + key, static_cast<unsigned long long>(__popc(peers)));
-  }
-  if (p.has_gt) {
-    if (p.hist_gt && active) {
-      const uint32_t key = b.app * 256u + b.G;
-      const unsigned peers = __match_any_sync(act, key);
-      if (lane == __ffs(peers) - 1) atomicAdd(p.hist_gt + key, static_cast<unsigned long long>(__popc(peers)));
-    }
-    const unsigned inc = __ballot_sync(kFull, active && !correct);
-    if (p.n_incorrect && (inc >> lane & 1u)) {
-      const unsigned peers = __match_any_sync(inc, b.app);
-      if (lane == __ffs(peers) - 1) atomicAdd(p.n_incorrect + b.app, static_cast<unsigned long long>(__popc(peers)));
-    }
-    if (p.loss_sum && p.want_loss) {
-      double sl = active ? static_cast<double>(L) : 0.0;
-      const uint32_t app0 = __shfl_sync(kFull, b.app, 0);
-      if (__all_sync(kFull, !active || b.app == app0)) {
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) sl += __shfl_xor_sync(kFull, sl, off);
-        if (lane == 0) atomicAdd(p.loss_sum + app0, sl);
-      } else if (active) {
-        atomicAdd(p.loss_sum + b.app, sl);
-      }
-    }
-  }
-  if (p.grad_dense) {
-    for (int t = 0; t < b.n; ++t) {
-      const int64_t row = __shfl_sync(kFull, b.row, t);
-      int32_t ci[8];
-      float cv[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        ci[q] = __shfl_sync(kFull, gi[q], t);
-        cv[q] = __shfl_sync(kFull, gv[q], t);
-      }
-      float* out = p.grad_dense + row * p.ld;
-      const int64_t nv = p.ld >> 2;
-      for (int64_t v = lane; v < nv; v += 32) {
-        float e[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-        for (int q4 = 0; q4 < 4; ++q4) {
-          const int64_t c = 4 * v + q4;
-#pragma unroll
-          for (int q = 0; q < 8; ++q)
-            if (c == ci[q]) e[q4] += cv[q];  // Multi-Select: one label may lead several lists
-        }
-        st_cs_f4(out + 4 * v, make_float4(e[0], e[1], e[2], e[3]));
-      }
-    }
-  }
-  __syncwarp();
-  b.n = 0;
 }
 
 // ------------------------------------------------------------------ fused evaluation kernel

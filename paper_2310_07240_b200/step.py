@@ -16,7 +16,8 @@ from dataclasses import dataclass
 
 import torch
 
-from . import Batch, Context, sc_decision_hist, sc_decision_hist_weights, sc_loss_fwd_bwd, sc_weights_from_hist
+from . import (SC_HOST_AUTO, Batch, Context, Stager, sc_decision_hist, sc_decision_hist_weights, sc_loss_fwd_bwd,
+               sc_loss_fwd_bwd_host, sc_weights_from_hist)
 
 
 def shard_range(rows: int, rank: int, world: int):
@@ -154,29 +155,27 @@ class Evaluator:
                     loss_sum=torch.empty(na, dtype=torch.float64, **pin))
 
     def step_host(self, h_logits, h_gt_off, h_gt_lab, host_out, h_app=None, grad_scale=None,
-                  global_rows=None, chunk_rows: int = 1 << 16):
+                  global_rows=None, chunk_rows: int = 1 << 16, host_mode: int = SC_HOST_AUTO):
         """The same step with inputs and outputs in (pinned) host memory.
 
-        The small ground truth goes first (pre-pass + weights need all of it); the logits
-        then stream host->device in chunks on a copy stream, double-buffered, each chunk's
-        sc_loss_fwd_bwd overlapping the next chunk's copy; per-row results stream back."""
+        The small ground truth goes first (pre-pass + weights need all of it); the logits are
+        then evaluated from host memory by sc_loss_fwd_bwd_host (C ABI): chunked host->device
+        copies double-buffered against the pass inside libsc, or the kernels reading the
+        pinned rows in place (sparse contexts); per-row results and aggregates come back."""
         o, ctx, na = self.out, self.ctx, self.ctx.n_apps
         dev = o.decision.device
         rows, C = h_logits.shape
         if grad_scale is None:
             grad_scale = 1.0 / max(1, global_rows if global_rows is not None else rows)
-        if not hasattr(self, "_stage") or self._stage[0].shape[0] < chunk_rows or self._stage[0].shape[1] != C \
-                or self._stage[0].dtype != h_logits.dtype:
-            self._stage = [torch.empty((chunk_rows, C), dtype=h_logits.dtype, device=dev) for _ in range(2)]
-            self._copy_stream = torch.cuda.Stream(dev)
-            self._d_off = None
-        if self._d_off is None or self._d_off.numel() < rows + 1 or self._d_lab.numel() < h_gt_lab.numel():
+        row_bytes = h_logits.stride(0) * h_logits.element_size()
+        if getattr(self, "_stager", None) is None or self._stager.chunk_bytes < chunk_rows * row_bytes:
+            self._stager = Stager(chunk_rows * row_bytes)
+        if getattr(self, "_d_off", None) is None or self._d_off.numel() < rows + 1 or \
+                self._d_lab.numel() < h_gt_lab.numel():
             self._d_off = torch.empty(rows + 1, dtype=torch.int64, device=dev)
             self._d_lab = torch.empty(max(1, h_gt_lab.numel()), dtype=torch.int32, device=dev)
         if h_app is not None and (getattr(self, "_d_app", None) is None or self._d_app.numel() < rows):
             self._d_app = torch.empty(max(1, rows), dtype=torch.int16, device=dev)
-        comp = torch.cuda.current_stream(dev)
-        cp = self._copy_stream
         d_off = self._d_off[:rows + 1]
         d_off.copy_(h_gt_off, non_blocking=True)
         d_lab = self._d_lab[:h_gt_lab.numel()]
@@ -190,24 +189,11 @@ class Evaluator:
                          gt_mask_out=o.gt_mask)
         allreduce_(o.hist_gt, self.group)
         sc_weights_from_hist(ctx, o.hist_gt, o.w)
-        free = [torch.cuda.Event(), torch.cuda.Event()]
-        ready = [torch.cuda.Event(), torch.cuda.Event()]
-        for e in free:
-            e.record(comp)
-        for ci, lo in enumerate(range(0, rows, chunk_rows)):
-            hi = min(rows, lo + chunk_rows)
-            buf = self._stage[ci & 1]
-            with torch.cuda.stream(cp):
-                cp.wait_event(free[ci & 1])
-                buf[:hi - lo].copy_(h_logits[lo:hi], non_blocking=True)
-                ready[ci & 1].record(cp)
-            comp.wait_event(ready[ci & 1])
-            sc_loss_fwd_bwd(ctx, Batch(logits=buf[:hi - lo], gt_mask=o.gt_mask[lo:], app=None if d_app is None
-                                       else d_app[lo:hi]),
-                            w=o.w, grad_scale=grad_scale, loss_sum=o.loss_sum, grad_idx=o.grad_idx[self.S * lo:self.S * hi],
-                            grad_val=o.grad_val[self.S * lo:self.S * hi], decision=o.decision[lo:hi],
-                            n_incorrect=o.counts[:na], hist_pred=o.counts[na:])
-            free[ci & 1].record(comp)
+        self.host_mode_used = sc_loss_fwd_bwd_host(
+            ctx, self._stager, Batch(logits=h_logits, gt_mask=o.gt_mask[:rows], app=d_app), mode=host_mode, w=o.w,
+            grad_scale=grad_scale, loss_sum=o.loss_sum, grad_idx=o.grad_idx[:self.S * rows],
+            grad_val=o.grad_val[:self.S * rows], decision=o.decision[:rows], n_incorrect=o.counts[:na],
+            hist_pred=o.counts[na:])
         allreduce_many_([o.counts, o.loss_sum], self.group)
         host_out["decision"][:rows].copy_(o.decision[:rows], non_blocking=True)
         S = self.S
@@ -216,5 +202,5 @@ class Evaluator:
         host_out["counts"].copy_(o.counts, non_blocking=True)
         host_out["hist_gt"].copy_(o.hist_gt, non_blocking=True)
         host_out["loss_sum"].copy_(o.loss_sum, non_blocking=True)
-        comp.synchronize()
+        torch.cuda.current_stream(dev).synchronize()
         return host_out

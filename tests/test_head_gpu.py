@@ -41,9 +41,10 @@ def bits_to_dev(bits, ld=None):
     return torch.from_numpy(bits.view(np.int16)).cuda().view(torch.bfloat16)
 
 
-def run_head(spec, x, W, b, gt_off, gt_lab, w=None, mode="csr", ldx=None, grad_scale=1.0, outputs=None):
+def run_head(spec, x, W, b, gt_off, gt_lab, w=None, mode="csr", ldx=None, grad_scale=1.0, outputs=None, order=0):
     torch, sc, _, _ = _mods()
-    ctx = sc.Context(spec.C, spec.lists, spec.tau, spec.k, multi_app=True)
+    ctx = sc.Context(spec.C, spec.lists, spec.tau, spec.k, order=order, multi_app=True)
+    S = ctx.grad_slots
     head = sc.Head(ctx, bits_to_dev(W), torch.from_numpy(b).cuda() if b is not None else None)
     rows = x.shape[0]
     xd = bits_to_dev(x, ldx)
@@ -54,8 +55,8 @@ def run_head(spec, x, W, b, gt_off, gt_lab, w=None, mode="csr", ldx=None, grad_s
         hist_gt=torch.zeros(256, dtype=torch.int64, device="cuda"),
         loss_sum=torch.zeros(1, dtype=torch.float64, device="cuda"),
         loss_row=torch.full((rows,), -1.0, dtype=torch.float32, device="cuda"),
-        grad_idx=torch.full((2 * rows,), -7, dtype=torch.int32, device="cuda"),
-        grad_val=torch.full((2 * rows,), -7.0, dtype=torch.float32, device="cuda"),
+        grad_idx=torch.full((S * rows,), -7, dtype=torch.int32, device="cuda"),
+        grad_val=torch.full((S * rows,), -7.0, dtype=torch.float32, device="cuda"),
     )
     if outputs is not None:
         o = {k: v for k, v in o.items() if k in outputs}
@@ -74,18 +75,18 @@ def run_head(spec, x, W, b, gt_off, gt_lab, w=None, mode="csr", ldx=None, grad_s
     return res
 
 
-def oracle_eval(spec, x, W, b, gt_off, gt_lab, w=None, grad_scale=1.0):
+def oracle_eval(spec, x, W, b, gt_off, gt_lab, w=None, grad_scale=1.0, order=0):
     *_, oracle = _mods()
     z = oracle.head_logits(x, W, b)
     z32 = z.astype(np.float32)
-    orc = oracle.Oracle.from_spec(spec)
+    orc = oracle.Oracle.from_spec(spec, order)
     wo = None if w is None else np.asarray(w, dtype=np.float32).astype(np.float64)
     return orc.eval(z32, gt_off, gt_lab, w=wo, grad_scale=grad_scale), z, orc
 
 
-def weights(spec, gt_off, gt_lab):
+def weights(spec, gt_off, gt_lab, order=0):
     *_, oracle = _mods()
-    orc = oracle.Oracle.from_spec(spec)
+    orc = oracle.Oracle.from_spec(spec, order)
     rows = len(gt_off) - 1
     pre = orc.eval(np.zeros((rows, spec.C), np.float32), gt_off, gt_lab, want_loss=False)
     return oracle.Oracle.weights_by_mask(pre["hist_gt"]).astype(np.float32).reshape(-1)
@@ -214,26 +215,33 @@ def test_head_errors():
         sc.sc_head_loss_fwd_bwd(ctx, head, xb, decision=torch.zeros(10, dtype=torch.uint8, device="cuda"))
     # empty batch is a no-op
     sc.sc_head_loss_fwd_bwd(ctx, head, x[:0], decision=torch.zeros(1, dtype=torch.uint8, device="cuda"))
-    # unsupported: other orders, several applications, |W| > 512
+    # a head compiled for one order, used with a context of another
     ctx_ac = sc.Context(spec.C, spec.lists, spec.tau, spec.k, order=sc.SC_ORDER_APP_CHOICE, multi_app=True)
-    with pytest.raises(sc.ScError, match="UNSUPPORTED"):
-        sc.Head(ctx_ac, bits_to_dev(W), None)
+    with pytest.raises(sc.ScError, match="INVALID"):
+        sc.sc_head_loss_fwd_bwd(ctx_ac, head, x, decision=torch.zeros(10, dtype=torch.uint8, device="cuda"))
+    # unsupported: several applications, more than 4096 head columns
     spec4 = synth.config_context(4)
     ctx4 = sc.Context(spec4.C, spec4.lists, spec4.tau, spec4.k, multi_app=True)
     with pytest.raises(sc.ScError, match="UNSUPPORTED"):
         sc.Head(ctx4, bits_to_dev(W), None)
-    big = custom_spec(1000, (300, 250), 3)
+    big = custom_spec(5000, (2500, 1700), 3)
     ctxb = sc.Context(big.C, big.lists, big.tau, big.k, multi_app=True)
+    _, Wb, _ = synth.head_operands(big.C, 64, 1, seed=1, kind="int")
     with pytest.raises(sc.ScError, match="UNSUPPORTED"):
-        sc.Head(ctxb, bits_to_dev(W), None)
+        sc.Head(ctxb, bits_to_dev(Wb), None)
 
 
-@pytest.mark.parametrize("q", [1, 2])
-@pytest.mark.parametrize("name,rows", [("cfg2", 148 * 128 * 2 + 1000), ("w300", 5000), ("cfg1", 300), ("w512", 700)])
+@pytest.mark.parametrize("q", [1, 2, "2t2"])
+@pytest.mark.parametrize("name,rows", [("cfg2", 148 * 128 * 2 + 1000), ("w300", 5000), ("cfg1", 300), ("w512", 700),
+                                       ("cfg2", 148 * 512 + 777)])
 def test_head_single_and_pair(q, name, rows, monkeypatch):
     """Lone CTAs (cta_group::1, M = 128) and CTA pairs (cta_group::2, M = 256, W halves in the
-    two CTAs), SC_HEAD_CLUSTER; unit counts that leave some CTAs without rows in the last step,
-    odd tile counts (a pair's second CTA past the end)."""
+    two CTAs), SC_HEAD_CLUSTER; "2t2": pairs with two row tiles per unit (512 rows per pass over
+    W, SC_HEAD_PAIR_T2); unit counts that leave some CTAs without rows in the last step, odd tile
+    counts (a pair's second CTA past the end)."""
+    if q == "2t2":
+        monkeypatch.setenv("SC_HEAD_PAIR_T2", "1")
+        q = 2
     torch, sc, synth, _ = _mods()
     spec = SPECS[name](synth)
     d = 320
@@ -353,3 +361,40 @@ def test_head_fullsize_sampled():
     d_all = dec.cpu().numpy()
     np.testing.assert_array_equal(hp.cpu().numpy(), np.bincount(d_all, minlength=256))
     assert int(hg.sum()) == rows and int(hp.sum()) == rows
+
+
+# more columns than TMEM holds: equal column passes of <= 256 columns, per-list maxima carried
+# across passes (lists straddle pass boundaries)
+WIDE = {
+    "w560": lambda s: custom_spec(1000, (300, 250), 3),                    # 304+256 = 560 -> 3 passes x 192
+    "cfg3": lambda s: s.config_context(3),                                 # |W| = 1000 of C = 20000: 1056 -> 5 x 224
+    "w1100": lambda s: custom_spec(3000, (700, 10, 390), 4),               # 704+16+400 -> 5 passes x 224
+}
+
+
+@pytest.mark.parametrize("order", [0, 1, 2])
+@pytest.mark.parametrize("name,d,rows,mode", [
+    ("cfg2", 256, 700, "mask"),
+    ("cfg1", 64, 300, "csr"),
+    ("ovl", 192, 900, "mask"),      # overlapping lists: Multi-Select columns repeat a label per list
+    ("d8", 128, 1100, "csr"),
+    ("w560", 128, 600, "mask"),
+    ("cfg3", 192, 400, "mask"),
+    ("w1100", 64, 333, "csr"),
+])
+def test_head_patterns_and_passes(order, name, d, rows, mode):
+    """The head under every decision pattern (API-output order, application-choice order,
+    Multi-Select) and with column passes (|𝕎| up to the OpenImages-shaped
+    1000 mapped labels): exact integer logits, so the path's full bar."""
+    torch, sc, synth, _ = _mods()
+    spec = {**SPECS, **WIDE}[name](synth)
+    x, W, b = synth.head_operands(spec.C, d, rows, seed=rows + d + order, kind="int")
+    gt_off, gt_lab = gt_for(spec, rows, seed=5 + order)
+    w = weights(spec, gt_off, gt_lab, order)
+    gs = 1.0 / rows
+    g = run_head(spec, x, W, b, gt_off, gt_lab, w=w, mode=mode, grad_scale=gs, order=order)
+    o, z, _ = oracle_eval(spec, x, W, b, gt_off, gt_lab, w=w, grad_scale=gs, order=order)
+    assert np.all(z.astype(np.float32).astype(np.float64) == z)  # exact logits
+    if name in WIDE:
+        assert g["n_cols"] > 512
+    compare_exact(g, o)

@@ -38,9 +38,11 @@ def to_dev(b, dtype):
     return out
 
 
-def run_gpu(ctxspec, d, mode="mask", dense=False, with_app=False, order=0, compact=False):
+def run_gpu(ctxspec, d, mode="mask", dense=False, with_app=False, order=0, compact=False, host=None):
     """hist pre-pass -> weights -> fused loss pass; returns numpy dict.  compact: the logits
-    are column-compacted rows of a sc_context_load_compact context."""
+    are column-compacted rows of a sc_context_load_compact context.  host = (mode, stager
+    chunk bytes): the loss pass reads the logits from pinned host memory
+    (sc_loss_fwd_bwd_host); res["host_mode"] = the mode libsc took."""
     torch, sc, _, _ = _mods()
     ctx = sc.Context(ctxspec.C, ctxspec.lists, ctxspec.tau, ctxspec.k, order=order, multi_app=True, compact=compact)
     rows, na = d["logits"].shape[0], ctxspec.n_apps
@@ -70,9 +72,17 @@ def run_gpu(ctxspec, d, mode="mask", dense=False, with_app=False, order=0, compa
     else:
         batch = sc.Batch(logits=d["logits"], gt_off=d["gt_off"], gt_lab=d["gt_lab"], app=app)
     grad_scale = 1.0 / max(rows, 1)
-    sc.sc_loss_fwd_bwd(ctx, batch, w=w, grad_scale=grad_scale, **o)
+    used = None
+    if host is None:
+        sc.sc_loss_fwd_bwd(ctx, batch, w=w, grad_scale=grad_scale, **o)
+    else:
+        hmode, chunk = host
+        batch.logits = d["logits"].cpu().pin_memory()
+        stager = sc.Stager(chunk) if chunk else None
+        used = sc.sc_loss_fwd_bwd_host(ctx, stager, batch, mode=hmode, w=w, grad_scale=grad_scale, **o)
     torch.cuda.synchronize()
     res = {k: v.cpu().numpy() for k, v in o.items()}
+    res["host_mode"] = used
     res["hist_pre"] = hist.cpu().numpy()
     res["gt_mask"] = gmask[:rows].cpu().numpy()
     res["w"] = w.cpu().numpy()
@@ -426,3 +436,51 @@ def test_unaligned_side_bands(mask_off, app_off, kernel):
     np.testing.assert_array_equal(gi.cpu().numpy(), o["grad_idx"])
     assert_rel(gv.cpu().numpy(), o["grad_val"], err_msg="grad_val")
     np.testing.assert_allclose(ls.cpu().numpy(), o["loss_sum"], rtol=RTOL)
+
+
+@pytest.mark.parametrize("cfg,dtype,rows,mode,host_mode,chunk_rows,expect", [
+    (2, "f32", 5000, "mask", 0, 1234, 1),     # dense context: AUTO copies (ragged last chunk)
+    (2, "bf16", 3001, "csr", 1, 1000, 1),
+    (3, "f32", 700, "mask", 0, 300, 2),       # sparse context (cfg3): AUTO reads the pinned rows in place
+    (3, "bf16", 650, "csr", 1, 200, 1),
+    (1, "f32", 4096, "csr", 2, 0, 2),         # ZERO_COPY needs no stager
+    (4, "f32", 2000, "mask", 1, 512, 1),      # 256 applications, per-row app ids
+])
+def test_loss_fwd_bwd_host(cfg, dtype, rows, mode, host_mode, chunk_rows, expect):
+    """sc_loss_fwd_bwd_host (C ABI, logits in pinned host memory): chunked double-buffered
+    copies inside libsc, or zero copy, give exactly the oracle's outputs (same bar as the
+    device path; dense gradients written chunk by chunk)."""
+    torch, sc, synth, _ = _mods()
+    spec = synth.config_context(cfg)
+    wl = synth.Workload(spec, seed=cfg, dtype=dtype, layout=1)
+    b = wl.host_batch(17, rows)
+    multi = spec.n_apps > 1
+    elt = 4 if dtype == "f32" else 2
+    chunk = chunk_rows * synth.default_ld(spec.C, dtype) * elt
+    g = run_gpu(spec, to_dev(b, dtype), mode=mode, dense=(cfg in (1, 2)), with_app=multi, host=(host_mode, chunk))
+    assert g["host_mode"] == expect
+    o, w = run_oracle(spec, b, g["grad_scale"], with_app=multi)
+    compare(g, o, w, rows)
+
+
+def test_loss_fwd_bwd_host_errors():
+    torch, sc, synth, _ = _mods()
+    spec = synth.config_context(2)
+    ctx = sc.Context(spec.C, spec.lists, multi_app=True)
+    lg = torch.zeros((64, 1000), dtype=torch.float32)  # pageable
+    gm = torch.zeros(64, dtype=torch.uint8, device="cuda")
+    dec = torch.zeros(64, dtype=torch.uint8, device="cuda")
+    with pytest.raises(sc.ScError, match="page-locked"):
+        sc.sc_loss_fwd_bwd_host(ctx, None, sc.Batch(logits=lg, gt_mask=gm), mode=sc.SC_HOST_ZERO_COPY, decision=dec)
+    with pytest.raises(sc.ScError, match="stager"):
+        sc.sc_loss_fwd_bwd_host(ctx, None, sc.Batch(logits=lg.pin_memory(), gt_mask=gm), mode=sc.SC_HOST_COPY,
+                                decision=dec)
+    with pytest.raises(sc.ScError, match="wider"):
+        sc.sc_loss_fwd_bwd_host(ctx, sc.Stager(1024), sc.Batch(logits=lg.pin_memory(), gt_mask=gm),
+                                mode=sc.SC_HOST_COPY, decision=dec)
+    with pytest.raises(ValueError):  # device logits are not host logits
+        sc.sc_loss_fwd_bwd_host(ctx, sc.Stager(1 << 20), sc.Batch(logits=lg.cuda(), gt_mask=gm), decision=dec)
+    # pageable rows still work through the copy path (synchronous copies)
+    used = sc.sc_loss_fwd_bwd_host(ctx, sc.Stager(1 << 20), sc.Batch(logits=lg, gt_mask=gm), decision=dec)
+    torch.cuda.synchronize()
+    assert used == sc.SC_HOST_COPY
