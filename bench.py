@@ -509,11 +509,23 @@ def run_all_apps(args, sc, ctx, logits, gt_off, gt_lab, B, dev, stream, rank):
     e.record(stream)
     torch.cuda.synchronize(dev)
     ms = s.elapsed_time(e) / args.steps
+    # roofline: plain ALU work, at least one compare per (row, application, mapped label); the
+    # peak is the ALU pipe (IADD3/LOP3/FMNMX: 16 lanes/clk per SM sub-partition, 4 per SM,
+    # /opt/skills/guides/B300_MICROARCH.md "Pipe rates") x 148 SMs x the max SM clock
+    import synth
+    entries = int(synth.config_context(args.config).mapped().sum())
+    ops = B * entries
+    peak_ops = 148 * 64 * 1.965e9
+    hbm = B * (logits.stride(0) * logits.element_size() + 18) / (ms / 1e3) / 1e9
     if rank == 0:
         print(json.dumps({"metric": "row-application evaluations/s (one read, every application)",
                           "value": B * A / (ms / 1e3), "unit": "evaluations/s", "ms_per_step": ms, "rows": B,
                           "apps": A, "dtype": args.dtype, "config": {"workload": workload_name(args.config, args.dtype)},
-                          "reread_equivalent_ms": None}), flush=True)
+                          "roofline": {"bound": "alu", "achieved": ops / (ms / 1e3) / 1e12, "peak": peak_ops / 1e12,
+                                       "unit": "Tops/s (one compare per row x app x mapped label)",
+                                       "frac": ops / (ms / 1e3) / peak_ops, "entries_per_row": entries,
+                                       "hbm_gbs": hbm, "hbm_frac": hbm / _peak()},
+                          "gpu_launches_per_step": 1}), flush=True)
     return 0
 
 

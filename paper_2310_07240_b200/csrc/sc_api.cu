@@ -166,8 +166,16 @@ sc_status run_eval(const sc_context_s* ctx, const sc_batch* b, const float* w, f
   // (per-list patterns: <= 8 list-major slots per app, one per register slot)
   const bool lane_ok = whole_rows && ctx->max_ent <= 1024 && want_epl &&
                        (pat ? ctx->max_slots <= 8 : sc::eval_epl_for(ctx->max_ent) > 0);
+  // dense-mapped rows: every column of a row is a mapped label of the one application (column-
+  // compacted rows): 16-B vector loads per lane, winners tracked by slot index (pat 2)
+  const int dm_vec = elt == 4 ? 4 : 8;
+  const int dm_nv = static_cast<int>((static_cast<int64_t>(ctx->ncols) + 32 * dm_vec - 1) / (32 * dm_vec));
+  const char* dm_env = std::getenv("SC_DM");
+  const bool dm = pat == 0 && ctx->n_apps == 1 && whole_rows && ctx->ncols >= 1 && ctx->max_ent == ctx->ncols &&
+                  dm_nv * dm_vec <= 32 && !(dm_env && std::atoi(dm_env) == 0) &&
+                  !(std::getenv("SC_KERNEL") && std::string(std::getenv("SC_KERNEL")) == "gather");
   // ---- kernel choice: sector-sparse gather when the mapped labels leave enough row sectors untouched
-  {
+  if (!dm) {
     const char* kenv = std::getenv("SC_KERNEL");
     const int dt = b->dtype == SC_BF16 ? 1 : 0;
     // HBM is read in 128-B lines here (measured: sector-sparse loads still move whole lines),
@@ -221,6 +229,12 @@ sc_status run_eval(const sc_context_s* ctx, const sc_batch* b, const float* w, f
   // f32 cfg2 fastest (0.592 vs 0.625 ms, 7.09 TB/s), so they are the default wherever whole
   // rows fit a stage.  SC_EPL=0 forces the shared-list path.
   if (lane_ok) epl = pat ? std::max(1, ctx->max_slots) : sc::eval_epl_for(ctx->max_ent);
+  int launch_pat = pat;
+  if (dm) {
+    epl = dm_nv;
+    launch_pat = 2;
+    p.dm_full = 1;  // nv = ceil(n / (32 kVec)): every group but the last lies inside the row
+  }
   int64_t logits_region;
   p.ng = 1;
   if (epl > 0) {
@@ -266,7 +280,7 @@ sc_status run_eval(const sc_context_s* ctx, const sc_batch* b, const float* w, f
   int64_t pmtab_bytes = 0;
   if (epl > 0) {
     p.ent_mode = 3;  // lane registers
-    if (ctx->n_apps == 1 && !pat) {
+    if (ctx->n_apps == 1 && launch_pat != 1) {
       p.pmtab_bits = ctx->nlists[0];
       pmtab_bytes = (int64_t(1) << p.pmtab_bits) * 32 * 4;
     }
@@ -282,7 +296,9 @@ sc_status run_eval(const sc_context_s* ctx, const sc_batch* b, const float* w, f
   }
   const bool wtab = want_loss && w && ctx->n_apps == 1;
   const int64_t max_stages = epl > 0 ? 32 : 8;
-  const int64_t other = ent_bytes + pmtab_bytes + (wtab ? 1024 : 0) + 2 * 8 * max_stages + 256;
+  // dense-mapped rows read whole 512-B groups: up to 511 B past a row's last column
+  const int64_t dm_slack = launch_pat == 2 ? 512 : 0;
+  const int64_t other = ent_bytes + pmtab_bytes + (wtab ? 1024 : 0) + 2 * 8 * max_stages + 256 + dm_slack;
   int64_t S = (static_cast<int64_t>(kSmemMax) - other) / p.stage_bytes;
   if (S > max_stages) S = max_stages;
   S -= S % p.ng;  // stage s always belongs to group s % ng
@@ -298,7 +314,7 @@ sc_status run_eval(const sc_context_s* ctx, const sc_batch* b, const float* w, f
   p.wtab_off = wtab ? static_cast<int32_t>(off) : -1;
   off += wtab ? 1024 : 0;
   p.bar_off = static_cast<int32_t>(round_up(off, 8));
-  off = p.bar_off + 2 * 8 * S;
+  off = p.bar_off + 2 * 8 * S + dm_slack;
   const size_t smem = static_cast<size_t>(off);
 
   p.split_copy = std::getenv("SC_SPLIT_COPY") ? 1 : 0;
@@ -309,8 +325,10 @@ sc_status run_eval(const sc_context_s* ctx, const sc_batch* b, const float* w, f
   // bandwidth (bf16 2.90 ms vs 1.42 ms blocked, f32 3.56 vs 2.38 ms, B200).
   p.blocked = std::getenv("SC_BLOCKED") ? std::atoi(std::getenv("SC_BLOCKED")) : (b->app ? 1 : 0);
   const int grid = static_cast<int>(std::min<int64_t>(p.nunits, di.sms));
-  if (cudaError_t e = sc::launch_eval(p, epl, pat, grid, smem, st)) return cuda_fail(e, "eval kernel launch");
-  g_last_kernel = epl ? (pat ? "tma_ring_lists_epl" : "tma_ring_epl") + std::to_string(epl) : "tma_ring_list";
+  if (cudaError_t e = sc::launch_eval(p, epl, launch_pat, grid, smem, st)) return cuda_fail(e, "eval kernel launch");
+  g_last_kernel = epl ? (launch_pat == 2 ? "tma_ring_dense_nv" : launch_pat ? "tma_ring_lists_epl" : "tma_ring_epl") +
+                            std::to_string(epl)
+                      : "tma_ring_list";
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return SC_OK;
 }

@@ -96,6 +96,7 @@ struct EvalParams {
   int32_t no_evict_first;   // experiment: L2 evict_normal instead of evict_first for the stream
   int32_t blocked;          // units: one contiguous block per CTA (1) or round-robin over CTAs (0)
   int32_t ld_flavor;        // gather kernel global-load cache flavour (see ldg_stream_f32)
+  int32_t dm_full;          // dense-mapped rows (pat 2): groups 0..NV-2 fully inside the row's n columns
 };
 
 struct HistParams {
@@ -133,6 +134,7 @@ cudaError_t launch_all_apps(const AllAppsParams& p, int grid, size_t smem, cudaS
 
 // Launchers (sc_kernels.cu).  Return cudaError_t of the launch.
 // epl > 0: lane-resident entries (|W| <= 32*epl, whole rows per stage); 0: generic list path.
+// pat 0: split maxima; 1: per-list slots; 2: dense-mapped rows (epl = 16-B groups per lane, 1..8).
 cudaError_t launch_eval(const EvalParams& p, int epl, int pat, int grid, size_t smem, cudaStream_t st);
 // Sector-sparse variant: epl = entries per lane capacity (1,2,4,8,16,32 -> |W| <= 32*epl).
 // pat 0: split maxima (API-output order); pat 1: per-list maxima (application-choice, Multi-Select).

@@ -316,6 +316,128 @@ __device__ __forceinline__ void finish_slots(const EvalParams& p, RowBatch& b, c
   finish_lists_core(p, b, zj, kj, wtab_smem, lane);
 }
 
+// ------------------------------------------------------------------ dense-mapped rows (PAT 2)
+
+// Every column 0..n-1 of a row is a mapped label of the single application (column-compacted
+// rows; or a context that maps every label).  Lane l reads 16-B vectors at
+// byte 512 g + 16 l of the row: entry (g, q) = column g·32·kVec + l·kVec + q (kVec = 4 f32 /
+// 8 bf16), ascending within the lane, so the strict '>' keeps the smaller label on ties.  No
+// per-entry key or offset registers (the EPL = 32 path of a 1000-label row spilled at the
+// 96-register cap and was ALU-bound): a winner is tracked by its slot index (an immediate)
+// and its key rebuilt once per row.
+template <int NV, bool BF16>
+struct DmEnt {
+  static constexpr int kVec = BF16 ? 8 : 4;
+  static constexpr bool kOk = NV * kVec <= 32;  // slot bits fit one register
+  uint32_t catm[8];  // bit g*kVec+q set iff entry (g, q) belongs to list j
+  uint32_t valid;    // bit set iff the entry's column is < n
+};
+
+template <int NV, bool BF16>
+__device__ __forceinline__ void dm_ent_load(DmEnt<NV, BF16>& de, const uint32_t* ents, int n, int lane) {
+  constexpr int V = DmEnt<NV, BF16>::kVec;
+  de.valid = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) de.catm[j] = 0;
+#pragma unroll
+  for (int g = 0; g < NV; ++g)
+#pragma unroll
+    for (int q = 0; q < V; ++q) {
+      const int col = g * 32 * V + lane * V + q, bit = g * V + q;
+      if (bit < 32 && col < n) {
+        de.valid |= 1u << bit;
+        const uint32_t lists = label_lists(static_cast<uint8_t>(__ldg(ents + col) & 0xFFu), kApiOutput);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) de.catm[j] |= ((lists >> j) & 1u) << bit;
+      }
+    }
+}
+
+// One entry of the split-maxima scan with its slot index as an immediate.
+template <uint32_t IDX>
+__device__ __forceinline__ void dm_entry(float z, uint32_t pm, float& zp, uint32_t& ip, float& zm, uint32_t& im) {
+  asm("{\n\t"
+      ".reg .pred bp, gp, gm;\n\t"
+      ".reg .b32 t;\n\t"
+      "and.b32 t, %5, %6;\n\t"
+      "setp.ne.u32 bp, t, 0;\n\t"
+      "setp.gt.and.f32 gp, %4, %0, bp;\n\t"
+      "setp.gt.and.f32 gm, %4, %2, !bp;\n\t"
+      "@gp mov.f32 %0, %4;\n\t"
+      "@gp mov.b32 %1, %7;\n\t"
+      "@gm mov.f32 %2, %4;\n\t"
+      "@gm mov.b32 %3, %7;\n\t"
+      "}"
+      : "+f"(zp), "+r"(ip), "+f"(zm), "+r"(im)
+      : "f"(z), "r"(pm), "n"(1u << IDX), "n"(IDX));
+}
+
+// The same for a slot that may lie past column n (separate plus / minus validity masks).
+template <uint32_t IDX>
+__device__ __forceinline__ void dm_entry_masked(float z, uint32_t vp, uint32_t vm, float& zp, uint32_t& ip, float& zm,
+                                                uint32_t& im) {
+  asm("{\n\t"
+      ".reg .pred bp, bm, gp, gm;\n\t"
+      ".reg .b32 t, u;\n\t"
+      "and.b32 t, %5, %7;\n\t"
+      "and.b32 u, %6, %7;\n\t"
+      "setp.ne.u32 bp, t, 0;\n\t"
+      "setp.ne.u32 bm, u, 0;\n\t"
+      "setp.gt.and.f32 gp, %4, %0, bp;\n\t"
+      "setp.gt.and.f32 gm, %4, %2, bm;\n\t"
+      "@gp mov.f32 %0, %4;\n\t"
+      "@gp mov.b32 %1, %8;\n\t"
+      "@gm mov.f32 %2, %4;\n\t"
+      "@gm mov.b32 %3, %8;\n\t"
+      "}"
+      : "+f"(zp), "+r"(ip), "+f"(zm), "+r"(im)
+      : "f"(z), "r"(vp), "r"(vm), "n"(1u << IDX), "n"(IDX));
+}
+
+__device__ __forceinline__ void lds_v4(uint32_t a, uint32_t (&w)[4]) {
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]) : "r"(a));
+}
+
+// Element q of a 16-B vector: f32 word q, or bf16 half q (little-endian: even q in the low half).
+template <bool BF16, int Q>
+__device__ __forceinline__ float dm_elem(const uint32_t (&w)[4]) {
+  if constexpr (BF16) return __uint_as_float((Q & 1) ? (w[Q >> 1] & 0xFFFF0000u) : (w[Q >> 1] << 16));
+  else return __uint_as_float(w[Q]);
+}
+
+template <int NV, bool BF16, bool MASKED, int G, int Q = 0>
+__device__ __forceinline__ void dm_vec(const uint32_t (&w)[4], uint32_t pm, uint32_t vp, uint32_t vm, float& zp,
+                                       uint32_t& ip, float& zm, uint32_t& im) {
+  constexpr int V = BF16 ? 8 : 4;
+  const float z = dm_elem<BF16, Q>(w);
+  if constexpr (MASKED) dm_entry_masked<G * V + Q>(z, vp, vm, zp, ip, zm, im);
+  else dm_entry<G * V + Q>(z, pm, zp, ip, zm, im);
+  if constexpr (Q + 1 < V) dm_vec<NV, BF16, MASKED, G, Q + 1>(w, pm, vp, vm, zp, ip, zm, im);
+}
+
+// FULL: every slot of groups 0..NV-2 is valid in every lane (n > (NV-1)·32·kVec).
+template <int NV, bool BF16, bool FULL, int G = 0>
+__device__ __forceinline__ void dm_scan(const uint32_t (&w)[NV][4], uint32_t pm, uint32_t vp, uint32_t vm, float& zp,
+                                        uint32_t& ip, float& zm, uint32_t& im) {
+  if constexpr (FULL && G < NV - 1) dm_vec<NV, BF16, false, G>(w[G], pm, vp, vm, zp, ip, zm, im);
+  else dm_vec<NV, BF16, true, G>(w[G], pm, vp, vm, zp, ip, zm, im);
+  if constexpr (G + 1 < NV) dm_scan<NV, BF16, FULL, G + 1>(w, pm, vp, vm, zp, ip, zm, im);
+}
+
+// Ordering key (column << 8) of this lane's slot `idx`, kNone if none; the winner's list is
+// looked up once, after the warp reduction (dm_cat).
+template <bool BF16>
+__device__ __forceinline__ uint32_t dm_colkey(uint32_t idx, int lane) {
+  constexpr uint32_t LV = BF16 ? 3 : 2;  // log2 kVec
+  const uint32_t col = ((idx >> LV) << (5 + LV)) | (static_cast<uint32_t>(lane) << LV) | (idx & ((1u << LV) - 1));
+  return idx == kNone ? kNone : col << 8;
+}
+// Full key of a reduced winner: entry `column` of the application's sorted entry list IS the
+// column's key (every column is mapped, so entry e = column e).
+__device__ __forceinline__ uint32_t dm_cat(const EvalParams& p, uint32_t k) {
+  return k == kNone ? kNone : __ldg(p.ctx.ent + (k >> 8));
+}
+
 // ------------------------------------------------------------------ fused evaluation kernel
 
 // The CTA's units: round-robin (u = blockIdx + i*grid) or one contiguous block per CTA.
@@ -459,19 +581,33 @@ __global__ void __launch_bounds__(kThreads, 1) eval_kernel(const EvalParams p) {
     // CTA-local unit i lives in stage i % S and is consumed by group i % NG only, so a
     // stage is released as soon as its WG warps are done (no CTA-wide stage barrier).
     constexpr uint32_t kElt = BF16 ? 2u : 4u;
-    LaneEnt<PAT ? 1 : EPL> le;  // split maxima (PAT 0)
-    SlotEnt<PAT ? EPL : 1> se;  // list-major slots (PAT 1)
-    float sz[PAT ? EPL : 1];    // this lane's batch row: arg max of every slot (PAT 1)
-    uint32_t sk[PAT ? EPL : 1];
+    constexpr bool kSplit = PAT != 1;  // split-maxima epilogue (finish_batch): PAT 0 and 2
+    LaneEnt<PAT == 0 ? EPL : 1> le;    // split maxima (PAT 0)
+    SlotEnt<PAT == 1 ? EPL : 1> se;    // list-major slots (PAT 1)
+    DmEnt<PAT == 2 ? EPL : 1, BF16> de;  // dense-mapped rows (PAT 2)
+    float sz[PAT == 1 ? EPL : 1];      // this lane's batch row: arg max of every slot (PAT 1)
+    uint32_t sk[PAT == 1 ? EPL : 1];
     if constexpr (PAT == 0)
       lane_ent_load(le, p.ctx.ent + __ldg(p.ctx.ent_off), __ldg(p.ctx.ent_off + 1) - __ldg(p.ctx.ent_off), 0, lane,
                     kElt);
-    else
+    else if constexpr (PAT == 1)
       slot_ent_load(se, p.ctx, 0, lane, kElt);
+    else
+      dm_ent_load(de, p.ctx.ent, __ldg(p.ctx.ent_off + 1), lane);
     // single app: table of plus-masks per G value (one LDS per row instead of 8 selects)
     uint32_t* pmtab = p.pmtab_off >= 0 ? reinterpret_cast<uint32_t*>(smem + p.pmtab_off) : nullptr;
-    if (PAT == 0 && pmtab) {
-      for (int g = cw; g < (1 << p.pmtab_bits); g += kConsumerWarps) pmtab[g * 32 + lane] = plus_mask(le, g);
+    if (kSplit && pmtab) {
+      for (int g = cw; g < (1 << p.pmtab_bits); g += kConsumerWarps) {
+        uint32_t pmv;
+        if constexpr (PAT == 2) {
+          pmv = 0;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) pmv |= (g & (1 << j)) ? de.catm[j] : 0u;
+        } else {
+          pmv = plus_mask(le, g);
+        }
+        pmtab[g * 32 + lane] = pmv;
+      }
       asm volatile("bar.sync 1, %0;" ::"r"(kConsumerWarps * 32) : "memory");
     }
     const int ng = p.ng, wg = kConsumerWarps / p.ng;
@@ -501,8 +637,32 @@ __global__ void __launch_bounds__(kThreads, 1) eval_kernel(const EvalParams p) {
         if (p.gt_mask) G = static_cast<uint32_t>(j) - wm.head < wm.nb ? lds_u8(m_base + j) : static_cast<uint32_t>(__ldg(p.gt_mask + row));
         else if (p.has_gt) G = warp_gt_mask(p, row, a, lane);
         const uint32_t srow = sbase + st_off + static_cast<uint32_t>(j) * static_cast<uint32_t>(p.ld_bytes);
-        float zs[EPL];
-        if constexpr (PAT == 0) {
+        float zs[PAT == 2 ? 1 : EPL];
+        if constexpr (PAT == 2) {
+          if constexpr (DmEnt<EPL, BF16>::kOk) {
+            uint32_t w[EPL][4];
+            const uint32_t lrow = srow + 16u * static_cast<uint32_t>(lane);
+#pragma unroll
+            for (int g = 0; g < EPL; ++g) lds_v4(lrow + 512u * g, w[g]);
+            const uint32_t pm = pmtab ? lds_u32(sbase + p.pmtab_off + (G * 32 + lane) * 4) : 0u;
+            float zp = -CUDART_INF_F, zm = -CUDART_INF_F;
+            uint32_t ip = kNone, im = kNone;
+            if (p.dm_full)  // warp-uniform
+              dm_scan<EPL, BF16, true>(w, pm, de.valid & pm, de.valid & ~pm, zp, ip, zm, im);
+            else
+              dm_scan<EPL, BF16, false>(w, pm, de.valid & pm, de.valid & ~pm, zp, ip, zm, im);
+            uint32_t kp = dm_colkey<BF16>(ip, lane), km = dm_colkey<BF16>(im, lane);
+            warp_argmax(zp, kp);
+            warp_argmax(zm, km);
+            kp = dm_cat(p, kp);
+            km = dm_cat(p, km);
+            if (b.n == lim) {
+              finish_batch(p, b, wtab, lane);
+              lim = 32;
+            }
+            deposit(b, lane, zp, kp, zm, km, G, a, row);
+          }
+        } else if constexpr (PAT == 0) {
           if (static_cast<int32_t>(a) != le.app) {
             const int32_t e0 = __ldg(p.ctx.ent_off + a);
             lane_ent_load(le, p.ctx.ent + e0, __ldg(p.ctx.ent_off + a + 1) - e0, static_cast<int32_t>(a), lane, kElt);
@@ -535,7 +695,7 @@ __global__ void __launch_bounds__(kThreads, 1) eval_kernel(const EvalParams p) {
       // the batch epilogue runs after the stage is released, and the warps' batch boundaries
       // are staggered (lim) so they do not all hold the pipeline in the same stage
       if (b.n == lim) {
-        if constexpr (PAT == 0) finish_batch(p, b, wtab, lane);
+        if constexpr (kSplit) finish_batch(p, b, wtab, lane);
         else finish_slots<EPL>(p, b, sz, sk, wtab, lane);
         lim = 32;
       }
@@ -543,7 +703,7 @@ __global__ void __launch_bounds__(kThreads, 1) eval_kernel(const EvalParams p) {
       if (st_idx >= p.stages) { st_idx -= p.stages; ph ^= 1u; }
     }
     if (b.n > 0) {
-      if constexpr (PAT == 0) finish_batch(p, b, wtab, lane);
+      if constexpr (kSplit) finish_batch(p, b, wtab, lane);
       else finish_slots<EPL>(p, b, sz, sk, wtab, lane);
     }
     return;
@@ -996,6 +1156,7 @@ static cudaError_t set_limit_t(size_t smem) {
 
 #define SC_EVAL_EPLS(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(12) X(16) X(24) X(32)
 #define SC_EVAL_EPLS_PAT(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8)  // per-list patterns: slots (PAT = 1)
+#define SC_EVAL_NV_DM(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8)     // dense-mapped rows: 16-B groups (PAT = 2)
 
 cudaError_t set_eval_smem_limit(size_t smem) {
   cudaError_t e = set_limit_t<0>(smem);
@@ -1004,6 +1165,9 @@ cudaError_t set_eval_smem_limit(size_t smem) {
 #undef SC_SET
 #define SC_SET(N) if (!e) e = set_limit_t<N, 1>(smem);
   SC_EVAL_EPLS_PAT(SC_SET)
+#undef SC_SET
+#define SC_SET(N) if (!e) e = set_limit_t<N, 2>(smem);
+  SC_EVAL_NV_DM(SC_SET)
 #undef SC_SET
   return e;
 }
@@ -1022,6 +1186,15 @@ int eval_epl_for(int max_ent, int pat) {
 
 template <bool BF16>
 static void launch_eval_dt(const EvalParams& p, int epl, int pat, int grid, size_t smem, cudaStream_t st) {
+  if (pat == 2) {
+    switch (epl) {
+#define SC_CASE(N) case N: eval_kernel<N, BF16, 2><<<grid, kThreads, smem, st>>>(p); break;
+      SC_EVAL_NV_DM(SC_CASE)
+#undef SC_CASE
+      default: break;
+    }
+    return;
+  }
   if (pat) {
     switch (epl) {
 #define SC_CASE(N) case N: eval_kernel<N, BF16, 1><<<grid, kThreads, smem, st>>>(p); break;

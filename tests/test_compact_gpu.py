@@ -128,3 +128,32 @@ def test_compact_head_and_errors():
     torch.cuda.synchronize()
     ref, _, _ = oracle_eval(spec, x, W, bias, gt_off, gt_lab, w=wv, grad_scale=1.0 / rows)
     compare_exact({k: v.cpu().numpy() for k, v in o.items()}, ref)
+
+
+@pytest.mark.parametrize("C,dtype,rows", [(1, "f32", 100), (4, "f32", 333), (37, "f32", 1000), (128, "f32", 700),
+                                          (129, "f32", 513), (1000, "f32", 999), (1024, "f32", 300),
+                                          (8, "bf16", 257), (1000, "bf16", 640), (1024, "bf16", 300)])
+def test_dense_mapped_rows(C, dtype, rows):
+    """Rows whose every column is a mapped label of the one application (what a compacted
+    context produces, and any context that maps every label) take the dense-mapped kernel
+    (16-B vector loads per lane, winners tracked by slot index): tie-heavy values (integers,
+    exactly tau, -0.0), every label mapped, overlapping lists, ragged last groups."""
+    import paper_2310_07240_b200 as sc
+    import synth
+    from test_parity_gpu import tie_heavy_batch
+    rng = np.random.default_rng(C * 13 + rows)
+    for tau in (0.0, -1.0):
+        D = int(rng.integers(1, 9))
+        owner = rng.integers(0, D, size=C)
+        lists = [sorted(np.nonzero(owner == j)[0].tolist()) for j in range(D)]
+        for j in range(D):  # overlaps: a few labels repeated in a later list (first list wins, A5)
+            lists[j] = sorted(set(lists[j]) | set(rng.integers(0, C, size=3).tolist()))
+        spec = synth.ContextSpec(C, [lists], tau=tau, k=10.0)
+        ld = synth.default_ld(C, dtype)
+        b = tie_heavy_batch(rng, C, rows, ld, lists, tau)
+        if dtype == "bf16":
+            b["logits"] = synth.f32_to_bf16_bits(b["logits"])
+        g = run_gpu(spec, to_dev(b, dtype), mode="mask" if tau == 0 else "csr", dense=True)
+        assert sc.sc_last_kernel().startswith("tma_ring_dense_nv"), sc.sc_last_kernel()
+        o, w = run_oracle(spec, b, g["grad_scale"])
+        compare(g, o, w, rows)
