@@ -167,12 +167,17 @@ sc_status run_eval(const sc_context_s* ctx, const sc_batch* b, const float* w, f
   const bool lane_ok = whole_rows && ctx->max_ent <= 1024 && want_epl &&
                        (pat ? ctx->max_slots <= 8 : sc::eval_epl_for(ctx->max_ent) > 0);
   // dense-mapped rows: every column of a row is a mapped label of the one application (column-
-  // compacted rows): 16-B vector loads per lane, winners tracked by slot index (pat 2)
+  // compacted rows): 16-B vector loads per lane, winners tracked by slot index (pat 2).
   const int dm_vec = elt == 4 ? 4 : 8;
   const int dm_nv = static_cast<int>((static_cast<int64_t>(ctx->ncols) + 32 * dm_vec - 1) / (32 * dm_vec));
   const char* dm_env = std::getenv("SC_DM");
-  const bool dm = pat == 0 && ctx->n_apps == 1 && whole_rows && ctx->ncols >= 1 && ctx->max_ent == ctx->ncols &&
-                  dm_nv * dm_vec <= 32 && !(dm_env && std::atoi(dm_env) == 0) &&
+  // Taken above 256 entries (EPL > 8, where the lane-resident path stops caching offsets in
+  // registers): B200, cfg3 compacted (1000 columns) 0.392 vs 0.695 ms; cfg2 compacted (180
+  // columns) the lane-resident path is faster, 0.330 vs 0.386 ms.
+  // SC_DM=0 disables it, SC_DM=2 takes it at any width (tests)
+  const int dm_mode = dm_env ? std::atoi(dm_env) : 1;
+  const bool dm = pat == 0 && ctx->n_apps == 1 && whole_rows && (ctx->ncols > 256 || dm_mode == 2) &&
+                  ctx->ncols >= 1 && ctx->max_ent == ctx->ncols && dm_nv * dm_vec <= 32 && dm_mode != 0 &&
                   !(std::getenv("SC_KERNEL") && std::string(std::getenv("SC_KERNEL")) == "gather");
   // ---- kernel choice: sector-sparse gather when the mapped labels leave enough row sectors untouched
   if (!dm) {

@@ -131,9 +131,10 @@ def test_compact_head_and_errors():
 
 
 @pytest.mark.parametrize("C,dtype,rows", [(1, "f32", 100), (4, "f32", 333), (37, "f32", 1000), (128, "f32", 700),
-                                          (129, "f32", 513), (1000, "f32", 999), (1024, "f32", 300),
-                                          (8, "bf16", 257), (1000, "bf16", 640), (1024, "bf16", 300)])
-def test_dense_mapped_rows(C, dtype, rows):
+                                          (129, "f32", 513), (257, "f32", 600), (1000, "f32", 999), (1024, "f32", 300),
+                                          (8, "bf16", 257), (300, "bf16", 333), (1000, "bf16", 640),
+                                          (1024, "bf16", 300)])
+def test_dense_mapped_rows(C, dtype, rows, monkeypatch):
     """Rows whose every column is a mapped label of the one application (what a compacted
     context produces, and any context that maps every label) take the dense-mapped kernel
     (16-B vector loads per lane, winners tracked by slot index): tie-heavy values (integers,
@@ -142,6 +143,8 @@ def test_dense_mapped_rows(C, dtype, rows):
     import synth
     from test_parity_gpu import tie_heavy_batch
     rng = np.random.default_rng(C * 13 + rows)
+    if C <= 256:  # below the automatic threshold the lane-resident path runs: force the dense-mapped one
+        monkeypatch.setenv("SC_DM", "2")
     for tau in (0.0, -1.0):
         D = int(rng.integers(1, 9))
         owner = rng.integers(0, D, size=C)
