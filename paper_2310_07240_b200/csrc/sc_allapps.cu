@@ -219,7 +219,143 @@ __global__ void __launch_bounds__(kAAWarps * 32, 1) all_apps_kernel(const AllApp
       atomicAdd(p.hist_pred + (i >> 4) * 256 + (i & 15), static_cast<unsigned long long>(cnt_pred[i]));
 }
 
+// Lane per application (the default): the 32 lanes of a warp scan 32 different applications
+// of one row, each its own entries in ascending label order (strict '>' keeps the smaller
+// label on ties, A4), so no warp reduction is needed at all; decision, correctness and the
+// counters are per lane.  Applications are grouped 32 at a time by size (largest first) so a
+// warp's lanes run similar trip counts; work items (group, row of the unit) are dealt to the
+// warps in a snake order over the size-sorted items, pairing large groups with small ones.
+// Padding entries point at a -inf slot past the row's copied columns and at list 31, in no G.
+__global__ void __launch_bounds__(kAAWarps * 32, 1) all_apps_lane_kernel(const AllAppsParams p) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int A = p.ctx.n_apps, R = p.rows_per_unit, NG = p.n_groups;
+  uint8_t* rowbuf = sm;                                                     // [2][R][row_bytes_pad]
+  uint32_t* ents = reinterpret_cast<uint32_t*>(sm + 2 * R * p.row_bytes_pad);  // [aa_ent_total]
+  int32_t* goff = reinterpret_cast<int32_t*>(ents + p.aa_ent_total);        // [NG + 1]
+  uint16_t* perm = reinterpret_cast<uint16_t*>(goff + NG + 1);             // [NG * 32]
+  unsigned* cnt_inc = reinterpret_cast<unsigned*>(perm + NG * 32);          // [A]
+  unsigned* cnt_pred = cnt_inc + A;                                         // [A][16]
+  uint8_t* gs2 = reinterpret_cast<uint8_t*>(cnt_pred + A * 16);            // [2][R][A]
+  uint8_t* nl = gs2 + 2 * R * A;                                            // [A]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + p.bar_off);            // [2]
+  for (int i = tid; i < p.aa_ent_total; i += blockDim.x) ents[i] = __ldg(p.aa_ent + i);
+  for (int i = tid; i <= NG; i += blockDim.x) goff[i] = __ldg(p.aa_goff + i);
+  for (int i = tid; i < NG * 32; i += blockDim.x) perm[i] = __ldg(p.aa_perm + i);
+  for (int i = tid; i < A; i += blockDim.x) { cnt_inc[i] = 0; nl[i] = __ldg(p.ctx.nlists + i); }
+  for (int i = tid; i < A * 16; i += blockDim.x) cnt_pred[i] = 0;
+  // the -inf slot of every row buffer (column round_up(C, 8), past what the bulk copies write)
+  const uint32_t elt = p.bf16 ? 2u : 4u;
+  for (int i = tid; i < 2 * R; i += blockDim.x) {
+    uint8_t* slot = rowbuf + i * p.row_bytes_pad + (p.dummy_key >> 8) * elt;
+    if (p.bf16) *reinterpret_cast<uint16_t*>(slot) = 0xFF80u;
+    else *reinterpret_cast<uint32_t*>(slot) = 0xFF800000u;
+  }
+  if (tid == 0) { mbar_init1(bar); mbar_init1(bar + 1); }
+  __syncthreads();
+
+  const int64_t n_units = (p.rows + R - 1) / R;
+  const int64_t first = blockIdx.x, step = gridDim.x;
+  auto unit_rows = [&](int64_t u) {
+    const int64_t r0 = u * R;
+    return static_cast<int>(p.rows - r0 < R ? p.rows - r0 : R);
+  };
+  auto load_unit = [&](int64_t u, int b) {
+    const int nr = unit_rows(u);
+    mbar_expect(bar + b, p.copy_bytes * nr);
+    for (int r = 0; r < nr; ++r)
+      bulk_copy(rowbuf + (b * R + r) * p.row_bytes_pad, p.logits + (u * R + r) * p.ld_bytes, p.copy_bytes, bar + b);
+  };
+  auto build_g = [&](int64_t u, uint8_t* gs) {
+    if (u >= n_units) return;
+    const int nr = unit_rows(u);
+    for (int r = 0; r < nr; ++r) {
+      const int64_t row = u * R + r;
+      const int64_t g0 = __ldg(p.gt_off + row), g1 = __ldg(p.gt_off + row + 1);
+      for (int a = tid; a < A; a += blockDim.x) {
+        uint32_t G = 0;
+        for (int64_t t = g0; t < g1; ++t) {
+          const int32_t c = __ldg(p.gt_lab + t);
+          G |= label_lists(__ldg(p.catT + static_cast<int64_t>(c) * A + a), kApiOutput);
+        }
+        gs[r * A + a] = static_cast<uint8_t>(G);
+      }
+    }
+  };
+  if (tid == 0 && first < n_units) load_unit(first, 0);
+  build_g(first, gs2);
+  __syncthreads();
+  uint32_t phase[2] = {0, 0};
+  int buf = 0;
+  const int n_items = NG * R;
+  for (int64_t u = first; u < n_units; u += step, buf ^= 1) {
+    const int64_t nxt = u + step;
+    if (tid == 0 && nxt < n_units) load_unit(nxt, buf ^ 1);
+    build_g(nxt, gs2 + (buf ^ 1) * R * A);
+    mbar_wait_parity(bar + buf, phase[buf]);
+    phase[buf] ^= 1u;
+    const int nr = unit_rows(u);
+    const uint8_t* gs = gs2 + buf * R * A;
+    // items i = g * R + r in descending cost; warp w takes w, 2*32-1-w, 2*32+w, 4*32-1-w, ...
+    for (int k = 0;; ++k) {
+      const int blk = k >> 1;
+      const int i = blk * 2 * kAAWarps + ((k & 1) ? 2 * kAAWarps - 1 - warp : warp);
+      if (i >= n_items) {
+        if (k & 1) continue;  // the mirrored item of this round is past the end; the next may not be
+        break;
+      }
+      const int g = i / R, r = i - g * R;
+      if (r >= nr) continue;
+      const int slot = 32 * g + lane;
+      const uint32_t a = perm[slot];
+      const bool live = a != 0xFFFFu;
+      const uint32_t G = live ? gs[r * A + a] : 0u;
+      const uint8_t* rb = rowbuf + (buf * R + r) * p.row_bytes_pad;
+      float zp = -CUDART_INF_F, zm = -CUDART_INF_F;
+      uint32_t kp = kNone, km = kNone;
+      const uint32_t* e = ents + goff[g] + lane;
+      const int n = (goff[g + 1] - goff[g]) >> 5;
+      for (int t = 0; t < n; ++t) {
+        const uint32_t key = e[32 * t];
+        const uint32_t col = key >> 8;
+        const float z = p.bf16 ? __uint_as_float(static_cast<uint32_t>(*reinterpret_cast<const uint16_t*>(rb + 2u * col)) << 16)
+                               : *reinterpret_cast<const float*>(rb + 4u * col);
+        // padding entries carry list 31 (bit 31 of an 8-bit G is 0: the minus side) and point
+        // at z = -inf, which never beats the running maximum
+        const bool plus = (G >> (key & 0x1Fu)) & 1u;
+        if (plus) {
+          if (z > zp) { zp = z; kp = key; }
+        } else {
+          if (z > zm) { zm = z; km = key; }
+        }
+      }
+      if (live) {
+        uint32_t dec;
+        bool ok;
+        aa_decide(Split{zp, zm, kp, km}, G, nl[a], p.ctx.tau, dec, ok);
+        if (!ok) atomicAdd(cnt_inc + a, 1u);
+        atomicAdd(cnt_pred + a * 16 + dec, 1u);
+        if (p.decision) p.decision[(u * R + r) * A + a] = static_cast<uint8_t>(dec);
+      }
+    }
+    __syncthreads();  // row buffers, gs and the next unit's G are reused / complete
+  }
+  for (int i = tid; i < A; i += blockDim.x)
+    if (cnt_inc[i] && p.n_incorrect) atomicAdd(p.n_incorrect + i, static_cast<unsigned long long>(cnt_inc[i]));
+  for (int i = tid; i < A * 16; i += blockDim.x)
+    if (cnt_pred[i] && p.hist_pred)
+      atomicAdd(p.hist_pred + (i >> 4) * 256 + (i & 15), static_cast<unsigned long long>(cnt_pred[i]));
+}
+
 }  // namespace
+
+cudaError_t launch_all_apps_lane(const AllAppsParams& p, int grid, size_t smem, cudaStream_t st) {
+  cudaError_t e = cudaFuncSetAttribute(all_apps_lane_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e) return e;
+  all_apps_lane_kernel<<<grid, kAAWarps * 32, smem, st>>>(p);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_all_apps(const AllAppsParams& p, int grid, size_t smem, cudaStream_t st) {
   cudaError_t e = cudaFuncSetAttribute(all_apps_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

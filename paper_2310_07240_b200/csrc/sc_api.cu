@@ -517,6 +517,39 @@ static sc_status load_context(int32_t C, int32_t n_apps, const int32_t* n_lists,
   if (!e) e = cudaMalloc(&ctx->d_catT, catT.size());
   if (!e) e = cudaMemcpy(ctx->d_catT, catT.data(), catT.size(), cudaMemcpyHostToDevice);
   if (!e) e = cudaMemset(ctx->d_done, 0, sizeof(unsigned int) * sc_context_s::kDonePool);
+  {  // all-apps, lane per application: applications by |W_a| descending, 32 per group,
+     // each group's entries transposed and padded to its largest application
+    std::vector<int32_t> perm(n_apps);
+    for (int32_t a = 0; a < n_apps; ++a) perm[a] = a;
+    std::stable_sort(perm.begin(), perm.end(), [&](int32_t x, int32_t y) {
+      return ent_off[x + 1] - ent_off[x] > ent_off[y + 1] - ent_off[y];
+    });
+    const int32_t ng = (n_apps + 31) / 32;
+    std::vector<int32_t> goff(ng + 1, 0);
+    std::vector<uint16_t> aperm(static_cast<size_t>(ng) * 32, 0xFFFF);
+    for (int32_t g = 0; g < ng; ++g) {
+      const int32_t a0 = perm[32 * g];
+      goff[g + 1] = goff[g] + 32 * (ent_off[a0 + 1] - ent_off[a0]);
+      for (int l = 0; l < 32 && 32 * g + l < n_apps; ++l) aperm[32 * g + l] = static_cast<uint16_t>(perm[32 * g + l]);
+    }
+    // padding entries: a key whose column is the row buffer's -inf slot (column round_up(C, 8),
+    // past the bytes a row copy writes for f32 and bf16) and whose list 31 is in no G
+    const uint32_t dummy = (static_cast<uint32_t>((C + 7) / 8 * 8) << 8) | 31u;
+    std::vector<uint32_t> aent(std::max<int32_t>(goff[ng], 1), dummy);
+    for (int32_t g = 0; g < ng; ++g)
+      for (int l = 0; l < 32 && 32 * g + l < n_apps; ++l) {
+        const int32_t a = perm[32 * g + l];
+        for (int32_t t = ent_off[a]; t < ent_off[a + 1]; ++t) aent[goff[g] + 32 * (t - ent_off[a]) + l] = ent[t];
+      }
+    ctx->aa_groups = ng;
+    ctx->aa_ent_total = goff[ng];
+    if (!e) e = cudaMalloc(&ctx->d_aa_ent, aent.size() * 4);
+    if (!e) e = cudaMalloc(&ctx->d_aa_goff, goff.size() * 4);
+    if (!e) e = cudaMalloc(&ctx->d_aa_perm, aperm.size() * 2);
+    if (!e) e = cudaMemcpy(ctx->d_aa_ent, aent.data(), aent.size() * 4, cudaMemcpyHostToDevice);
+    if (!e) e = cudaMemcpy(ctx->d_aa_goff, goff.data(), goff.size() * 4, cudaMemcpyHostToDevice);
+    if (!e) e = cudaMemcpy(ctx->d_aa_perm, aperm.data(), aperm.size() * 2, cudaMemcpyHostToDevice);
+  }
   if (!e) e = cudaMemcpy(ctx->d_cat, cat.data(), cat.size(), cudaMemcpyHostToDevice);
   if (!e) e = cudaMemcpy(ctx->d_ent, ent.data(), ent.size() * 4, cudaMemcpyHostToDevice);
   if (!e) e = cudaMemcpy(ctx->d_ent_off, ent_off.data(), ent_off.size() * 4, cudaMemcpyHostToDevice);
@@ -544,6 +577,9 @@ sc_status sc_context_free(sc_context ctx) {
   cudaFree(ctx->d_nlists);
   cudaFree(ctx->d_done);
   cudaFree(ctx->d_catT);
+  cudaFree(ctx->d_aa_ent);
+  cudaFree(ctx->d_aa_goff);
+  cudaFree(ctx->d_aa_perm);
   cudaFree(ctx->d_col_label);
   delete ctx;
   return SC_OK;
@@ -699,6 +735,37 @@ sc_status sc_decide_all_apps(sc_context ctx, const sc_batch* b, uint64_t* n_inco
   p.hist_pred = reinterpret_cast<unsigned long long*>(hist_pred);
   p.decision = decision;
   const int64_t A = ctx->n_apps;
+  const char* aa_env = std::getenv("SC_ALLAPPS");
+  if (!(aa_env && std::string(aa_env) == "warp")) {
+    // lane per application: [2 units x R] row buffers (each with a -inf slot at column C),
+    // transposed entries, group offsets, perm, counters, G [2][R][A], D'
+    p.aa_ent = ctx->d_aa_ent;
+    p.aa_goff = ctx->d_aa_goff;
+    p.aa_perm = ctx->d_aa_perm;
+    p.n_groups = ctx->aa_groups;
+    p.aa_ent_total = ctx->aa_ent_total;
+    p.dummy_key = (static_cast<uint32_t>((ctx->C + 7) / 8 * 8) << 8) | 31u;
+    p.row_bytes_pad = static_cast<int32_t>(round_up(static_cast<int64_t>((ctx->C + 7) / 8 * 8 + 1) * elt, 128));
+    const int64_t ng = ctx->aa_groups;
+    for (int R = 8; R >= 1; R /= 2) {
+      int64_t o = 2 * R * static_cast<int64_t>(p.row_bytes_pad) + 4 * static_cast<int64_t>(p.aa_ent_total) +
+                  4 * (ng + 1) + 64 * ng + 4 * A + 64 * A + 2 * R * A + A;
+      o = round_up(o, 8);
+      const size_t sm = static_cast<size_t>(o + 16);
+      if (sm <= kSmemMax) {
+        p.rows_per_unit = R;
+        p.bar_off = static_cast<int32_t>(o);
+        const int grid = static_cast<int>(std::min<int64_t>((b->rows + R - 1) / R, di.sms));
+        if (cudaError_t e = sc::launch_all_apps_lane(p, grid, sm, static_cast<cudaStream_t>(stream)))
+          return cuda_fail(e, "all-apps kernel launch");
+        g_last_kernel = "all_apps_lane";
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        return SC_OK;
+      }
+    }
+    // contexts too large for the lane layout: the warp-per-application kernel below
+  }
+  p.row_bytes_pad = static_cast<int32_t>(round_up(p.copy_bytes, 128));
   // [2 units x kAARows] row buffers, entries, offsets, counters, G [2 units x kAARows][A], D'
   const int64_t ur = sc::kAllAppsRows;
   int64_t off = 2 * ur * static_cast<int64_t>(p.row_bytes_pad) + 4 * p.n_ent_total + 4 * (A + 1) + 4 * A + 64 * A +
@@ -709,6 +776,7 @@ sc_status sc_decide_all_apps(sc_context ctx, const sc_batch* b, uint64_t* n_inco
   const int grid = static_cast<int>(std::min<int64_t>((b->rows + ur - 1) / ur, di.sms));  // kAARows-row units
   if (cudaError_t e = sc::launch_all_apps(p, grid, smem, static_cast<cudaStream_t>(stream)))
     return cuda_fail(e, "all-apps kernel launch");
+  g_last_kernel = "all_apps_warp";
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return SC_OK;
 }

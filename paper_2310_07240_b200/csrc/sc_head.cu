@@ -36,6 +36,7 @@
 #include <algorithm>
 #include <array>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 #include <string>
@@ -76,12 +77,32 @@ struct HeadParams {
   int32_t n_lists;          // D'
   int32_t list_col0[kMaxLists];  // first column of list j (multiple of 16)
   int32_t list_nch[kMaxLists];   // 16-column groups of list j
-  int32_t probe;            // experiment (SC_HEAD_PROBE): bit 0 skips the epilogue's reduction, bit 1 the MMAs
+  int32_t probe;            // experiment (SC_HEAD_PROBE): bit 0 skips the epilogue's reduction, bit 1 the MMAs,
+                            // bit 2 the x loads, bit 3 the W loads (lone CTAs; results are garbage)
   int32_t n_pass;           // column passes per row tile: 1 = every column in TMEM at once (n_cols <= 512);
                             // > 1 = pass_w columns per pass, x re-streamed per pass (from L2)
   int32_t pass_w;           // columns per pass (n_pass > 1; = chunk)
   int32_t pat;              // 0: API-output order (split maxima); 1: per-list patterns (finish_lists_core)
+  int32_t n_groups;         // 16-column groups holding list columns (the lists back to back)
+  unsigned long long* trace;  // experiment (SC_HEAD_TRACE=file): per-unit timeline of CTAs < kTraceCtas, or NULL
 };
+
+// Timeline probe (SC_HEAD_TRACE): globaltimer stamps (ns) and wait sums per (CTA, unit) for
+// the first kTraceCtas CTAs and kTraceUnits units; slots: 0/1 MMA waits the accumulator
+// (start / acquired), 2/3 MMA's summed waits on x / W stages, 4 MMA's last commit of the unit,
+// 5/6 epilogue warp 2 waits the accumulator (start / acquired), 7 its drain done, 8 its finish
+// done, 9/10 x / W producers' summed waits for free stages, 11/12 epilogue warp 7 acquired /
+// drained.
+constexpr int kTraceCtas = 8, kTraceUnits = 32, kTraceSlots = 16;
+__device__ __forceinline__ unsigned long long tnow() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned long long* trace_slot(const HeadParams& p, int64_t st) {
+  if (p.trace == nullptr || blockIdx.x >= kTraceCtas || st >= kTraceUnits) return nullptr;
+  return p.trace + (static_cast<int64_t>(blockIdx.x) * kTraceUnits + st) * kTraceSlots;
+}
 
 // ------------------------------------------------------------------ tcgen05 / TMA / cluster PTX
 
@@ -177,36 +198,62 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int m, int n) {
 // D (TMEM) (+)= A (smem) · Bᵀ (smem).  CG2: M = 256 over the CTA pair — each CTA holds its
 // 128 rows of A and half of B's columns at the same shared-memory offsets, and receives its
 // 128 rows x N of D in its own TMEM; issued by the pair's leader only.
+// Called by the whole (converged) MMA warp with warp-uniform operands, which then stay in
+// uniform registers; one elected lane issues.  (Issued from a lane-0-only branch, every MMA
+// was wrapped in an ELECT / R2UR.BROADCAST loop: ~200 cycles per MMA, measured, against a
+// ~96-cycle tensor floor for M = 128, N = 192.)
 template <bool CG2>
 __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                           uint32_t accumulate) {
   if constexpr (CG2)
     asm volatile(
-        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
         : "memory");
   else
     asm volatile(
-        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
 
+// One k-block (4 K = 16 steps) of MMAs: NCH column chunks x NTL row tiles, each its own
+// accumulator at acc + t*tc_step + c*cc_step; A of tile t at ad + t*t_step, B of chunk c at
+// bd + c*c_step (descriptor units).
+template <bool CG2, int NCH, int NTL>
+__device__ __forceinline__ void mma_kblock(uint32_t acc, uint64_t ad, uint64_t bd, uint64_t t_step, uint64_t c_step,
+                                           uint32_t tc_step, uint32_t cc_step, uint32_t idesc, bool first) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const uint32_t accum = (first && k == 0) ? 0u : 1u;
+#pragma unroll
+    for (int c = 0; c < NCH; ++c)
+#pragma unroll
+      for (int t = 0; t < NTL; ++t)
+        umma_bf16<CG2>(acc + t * tc_step + c * cc_step, ad + t * t_step + 2 * k, bd + c * c_step + 2 * k, idesc,
+                       accum);
+  }
+}
+
 // Arrive once on `bar` (CG2: at `bar`'s offset in both CTAs of the pair) when every
 // tcgen05.mma issued so far by this thread has completed.
+// Elected like umma_bf16 (called by the whole MMA warp).
 template <bool CG2>
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   if constexpr (CG2)
     asm volatile(
-        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-            smem_addr(bar)),
+        "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n}\n" ::
+            "r"(smem_addr(bar)),
         "h"(static_cast<uint16_t>(3))
         : "memory");
   else
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_addr(bar))
-                 : "memory");
+    asm volatile(
+        "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(smem_addr(bar))
+        : "memory");
 }
 
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -220,6 +267,28 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
         "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
       : "r"(taddr));
 }
+// 32 lanes x 32 bits, 32 consecutive columns -> 32 registers per thread.
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+        "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+        "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld32(uint32_t (&v)[32]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7]),
+                 "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]), "+r"(v[14]),
+                 "+r"(v[15]), "+r"(v[16]), "+r"(v[17]), "+r"(v[18]), "+r"(v[19]), "+r"(v[20]), "+r"(v[21]),
+                 "+r"(v[22]), "+r"(v[23]), "+r"(v[24]), "+r"(v[25]), "+r"(v[26]), "+r"(v[27]), "+r"(v[28]),
+                 "+r"(v[29]), "+r"(v[30]), "+r"(v[31])
+               :
+               : "memory");
+}
+
 // Wait for the outstanding tcgen05.ld; `v` passes through so no use of it is hoisted above.
 __device__ __forceinline__ void tmem_wait_ld(uint32_t (&v)[16]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;"
@@ -342,9 +411,23 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
         for (int ps = 0; ps < p.n_pass; ++ps) {
         const uint64_t pol_x = ps + 1 < p.n_pass ? pol_keep : pol_first;
         for (int xb = 0; xb < p.n_xb; ++xb) {
-          mbar_wait(xempty + s, ph ^ 1u);
+          if (unsigned long long* tr = trace_slot(p, st)) {
+            const unsigned long long t0 = tnow();
+            mbar_wait(xempty + s, ph ^ 1u);
+            tr[9] += tnow() - t0;
+          } else {
+            mbar_wait(xempty + s, ph ^ 1u);
+          }
           uint8_t* stg = sm + static_cast<size_t>(s) * p.x_stage_bytes;
           const uint32_t fb = xfull_l + 8u * s;
+          if (!PAIR && (p.probe & 4)) {  // probe: no x traffic, the MMAs run on stale stages
+            mbar_arrive(xfull + s);
+            if (++s == p.x_stages) {
+              s = 0;
+              ph ^= 1u;
+            }
+            continue;
+          }
           if (rank == 0) mbar_arrive_expect_tx(xfull + s, tx);
           else mbar_arrive_expect_tx_cl(fb, tx);
           for (int t = 0; t < p.tiles; ++t) {  // tile t: kbs k-blocks at t * kbs * 16 KB
@@ -372,9 +455,23 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
         for (int ps = 0; ps < p.n_pass; ++ps) {
         const int col0 = ps * p.pass_w;  // 0 when n_pass == 1
         for (int kb = 0; kb < p.n_kb; ++kb) {
-          mbar_wait(wempty + s, ph ^ 1u);
+          if (unsigned long long* tr = trace_slot(p, st)) {
+            const unsigned long long t0 = tnow();
+            mbar_wait(wempty + s, ph ^ 1u);
+            tr[10] += tnow() - t0;
+          } else {
+            mbar_wait(wempty + s, ph ^ 1u);
+          }
           uint8_t* stg = sm + p.w_ring_off + static_cast<size_t>(s) * p.w_stage_bytes;
           const uint32_t fb = wfull_l + 8u * s;
+          if (!PAIR && (p.probe & 8)) {  // probe: no W traffic
+            mbar_arrive(wfull + s);
+            if (++s == p.w_stages) {
+              s = 0;
+              ph ^= 1u;
+            }
+            continue;
+          }
           if (rank == 0) mbar_arrive_expect_tx(wfull + s, tx);
           else mbar_arrive_expect_tx_cl(fb, tx);
           for (int c = 0; c < p.n_chunks; ++c)
@@ -389,8 +486,9 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && rank == 0) {
-      // ---------------- MMA issuer (the pair's leader)
+    if (rank == 0) {
+      // ---------------- MMA issuer (the pair's leader): the whole warp runs the loop (operands
+      // warp-uniform, so they live in uniform registers); one elected lane issues
       const uint32_t idesc = idesc_bf16(PAIR ? 2 * kBM : kBM, p.chunk);
       // descriptors advance by address >> 4 in their low bits: x stage, k-block in the
       // stage (16 KB), 32 B per K=16 step; W stage; second MMA's columns
@@ -399,8 +497,7 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
       const uint64_t x_step = static_cast<uint32_t>(p.x_stage_bytes) >> 4;
       const uint64_t w_step = static_cast<uint32_t>(p.w_stage_bytes) >> 4;
       const uint64_t c_step = static_cast<uint32_t>((PAIR ? p.chunk / 2 : p.chunk) * kBK * 2) >> 4;
-      const bool two = p.n_chunks == 2;
-      const bool tile2 = p.tiles == 2;                                        // n_chunks == 1 then
+      const int nch = p.n_chunks, ntl = p.tiles;
       const uint64_t t_step = static_cast<uint32_t>(p.kbs * a_bytes) >> 4;  // tile 1 in an x stage
       const bool no_mma = (p.probe & 2) != 0;
       int xs = 0, ws = 0, b = 0;
@@ -409,29 +506,50 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
       const int acc_stride = p.n_pass > 1 ? p.pass_w : p.n_cols;
       for (int64_t st = 0; st < n_steps; ++st) {
         for (int ps = 0; ps < p.n_pass; ++ps) {
+        unsigned long long* tr = (ps == 0 && lane == 0) ? trace_slot(p, st) : nullptr;
+        if (tr) tr[0] = tnow();
         mbar_wait(tempty + b, tph[b] ^ 1u);  // the epilogue(s) drained this accumulator
+        if (tr) tr[1] = tnow();
         tph[b] ^= 1u;
         tc_fence_after();
         const uint32_t acc = tmem_base + static_cast<uint32_t>(b * acc_stride);
         for (int xb = 0; xb < p.n_xb; ++xb) {
-          mbar_wait(xfull + xs, xph);
+          if (tr) {
+            const unsigned long long t0 = tnow();
+            mbar_wait(xfull + xs, xph);
+            tr[2] += tnow() - t0;
+          } else {
+            mbar_wait(xfull + xs, xph);
+          }
           tc_fence_after();
           const uint64_t ax = a_desc0 + static_cast<uint64_t>(xs) * x_step;
           const int nk = min(p.kbs, p.n_kb - xb * p.kbs);
           for (int kx = 0; kx < nk; ++kx) {
-            mbar_wait(wfull + ws, wph);
+            if (tr) {
+              const unsigned long long t0 = tnow();
+              mbar_wait(wfull + ws, wph);
+              tr[3] += tnow() - t0;
+            } else {
+              mbar_wait(wfull + ws, wph);
+            }
             tc_fence_after();
             const uint64_t ad = ax + static_cast<uint64_t>(kx) * (a_bytes >> 4);
             const uint64_t bd = b_desc0 + static_cast<uint64_t>(ws) * w_step;
             if (!no_mma) {
               const bool first = (xb | kx) == 0;
-#pragma unroll
-              for (int k = 0; k < kBK / 16; ++k) {
-                const uint32_t accum = (first && k == 0) ? 0u : 1u;
-                umma_bf16<PAIR>(acc, ad + 2 * k, bd + 2 * k, idesc, accum);
-                if (two) umma_bf16<PAIR>(acc + p.chunk, ad + 2 * k, bd + c_step + 2 * k, idesc, accum);
-                if (tile2)  // the second row tile: same W stage, its own accumulator
-                  umma_bf16<PAIR>(acc + p.n_cols, ad + t_step + 2 * k, bd + 2 * k, idesc, accum);
+              // column chunk c of row tile t: its own accumulator (t * n_cols + c * chunk), so
+              // the nch * ntl MMAs of a k-step are independent chains the tensor pipe overlaps
+              // (measured: back-to-back MMAs into one accumulator serialise at ~195 ns each).
+              // One straight-line instance per (nch, ntl): a predicated-off tcgen05.mma is not
+              // free (measured: 8 guarded MMAs per k-step ran at half the rate).
+              const uint32_t tc_step = static_cast<uint32_t>(p.n_cols), cc_step = static_cast<uint32_t>(p.chunk);
+              switch (nch * 2 + ntl - 1) {
+                case 2: mma_kblock<PAIR, 1, 1>(acc, ad, bd, t_step, c_step, tc_step, cc_step, idesc, first); break;
+                case 3: mma_kblock<PAIR, 1, 2>(acc, ad, bd, t_step, c_step, tc_step, cc_step, idesc, first); break;
+                case 4: mma_kblock<PAIR, 2, 1>(acc, ad, bd, t_step, c_step, tc_step, cc_step, idesc, first); break;
+                case 5: mma_kblock<PAIR, 2, 2>(acc, ad, bd, t_step, c_step, tc_step, cc_step, idesc, first); break;
+                case 8: mma_kblock<PAIR, 4, 1>(acc, ad, bd, t_step, c_step, tc_step, cc_step, idesc, first); break;
+                default: mma_kblock<PAIR, 4, 2>(acc, ad, bd, t_step, c_step, tc_step, cc_step, idesc, first); break;
               }
             }
             umma_commit<PAIR>(wempty + ws);  // W stage free (in both CTAs) once read
@@ -447,6 +565,7 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
           }
         }
         umma_commit<PAIR>(tfull + b);  // accumulator complete (in both CTAs)
+        if (tr) tr[4] = tnow();
         if (p.acc_bufs == 2) b ^= 1;
         }
       }
@@ -467,6 +586,7 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
     // each warp drains one tile
     const int t = ntile == 2 ? (warp >= 7 ? 1 : 0) : 0;
     const int acc_stride = p.n_pass > 1 ? p.pass_w : p.n_cols;
+    const uint32_t s_bias_addr = smem_addr(s_bias);
     for (int64_t st = 0; st < n_steps; ++st) {
       const int64_t first = (unit0 + st * n_grid_units) * kUnit + t * kTileRows + rank * kBM + 32 * q;
       const int64_t row = first + lane;
@@ -490,74 +610,100 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
         lz[jj] = -CUDART_INF_F;
         lc[jj] = -1;
       }
-      int j = 0, g = 0;  // list, group within the list
+      // 16-column groups k = 0 .. n_groups-1 run over the lists back to back (each list padded
+      // to 16 columns); j = list of the current group, jend = its first group past the list
+      int k = 0, j = 0;
       while (j < D && p.list_nch[j] == 0) ++j;
-      if (p.probe & 1) j = D;
+      int jend = j < D ? (p.list_col0[j] >> 4) + p.list_nch[j] : 0;
+      const int n_groups = (p.probe & 1) ? 0 : p.n_groups;
       float run_z = -CUDART_INF_F;
       int run_c = -1;
       for (int ps = 0; ps < p.n_pass; ++ps) {
         const int c_lo = p.n_pass > 1 ? ps * p.pass_w : 0;
         const int c_hi = p.n_pass > 1 ? c_lo + p.pass_w : p.n_cols;
+        unsigned long long* tr = (ps == 0 && lane == 0 && (warp == 2 || warp == 7)) ? trace_slot(p, st) : nullptr;
+        if (tr && warp == 2) tr[5] = tnow();
         mbar_wait(tfull + b, tph[b]);
+        if (tr) tr[warp == 2 ? 6 : 11] = tnow();
         tph[b] ^= 1u;
         tc_fence_after();
         // column c of this pass lives at acc + c - c_lo
         const uint32_t acc = tmem_base + lane_base +
                              static_cast<uint32_t>(p.n_pass > 1 ? b * acc_stride : (b + t) * p.n_cols) -
                              static_cast<uint32_t>(c_lo);
-        uint32_t v[16], vn[16];
-        if (j < D && p.list_col0[j] + 16 * g < c_hi) {
-          tmem_ld16(acc + p.list_col0[j] + 16 * g, v);
-          tmem_wait_ld(v);
+        const int khi = min(c_hi >> 4, n_groups);
+        // rounds of two groups (one 32-column TMEM load); the next round's load is in flight
+        // while this one is reduced (tcgen05.wait::ld waits for every outstanding load)
+        uint32_t v[32], vn[32];
+        if (k < khi) {
+          if (k + 1 < khi) tmem_ld32(acc + 16 * k, v);
+          else tmem_ld16(acc + 16 * k, *reinterpret_cast<uint32_t(*)[16]>(v));
+          tmem_wait_ld32(v);
         }
-        while (j < D && p.list_col0[j] + 16 * g < c_hi) {
-          const int col = p.list_col0[j] + 16 * g;
-          // next group (warp-uniform); its load is in flight while this one is reduced
-          int jn = j, gn = g + 1;
-          if (gn == p.list_nch[jn]) {
-            gn = 0;
-            ++jn;
-            while (jn < D && p.list_nch[jn] == 0) ++jn;
+        while (k < khi) {
+          const int kn = k + 2;
+          if (kn < khi) {
+            if (kn + 1 < khi) tmem_ld32(acc + 16 * kn, vn);
+            else tmem_ld16(acc + 16 * kn, *reinterpret_cast<uint32_t(*)[16]>(vn));
           }
-          const bool more = jn < D && p.list_col0[jn] + 16 * gn < c_hi;
-          if (more) tmem_ld16(acc + p.list_col0[jn] + 16 * gn, vn);
-          float z[16];
-          const float4* b4 = reinterpret_cast<const float4*>(s_bias + col);
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const float4 bb = b4[i];
-            z[4 * i + 0] = __uint_as_float(v[4 * i + 0]) + bb.x;
-            z[4 * i + 1] = __uint_as_float(v[4 * i + 1]) + bb.y;
-            z[4 * i + 2] = __uint_as_float(v[4 * i + 2]) + bb.z;
-            z[4 * i + 3] = __uint_as_float(v[4 * i + 3]) + bb.w;
-          }
-          float zc;
-          int ic;
-          argmax16(z, zc, ic);
-          if (zc > run_z) {  // strict: an earlier group (smaller labels) keeps ties
-            run_z = zc;
-            run_c = col + ic;
-          }
-          if (jn != j) {  // list j done
+          for (int h = 0; h < 2; ++h) {
+            const int kg = k + h;
+            if (kg < khi) {  // warp-uniform
+              while (kg >= jend) {  // list j done (lists past it may be empty)
 #pragma unroll
-            for (int jj = 0; jj < kMaxLists; ++jj)
-              if (jj == j) {
-                lz[jj] = run_z;
-                lc[jj] = run_c;
+                for (int jj = 0; jj < kMaxLists; ++jj)
+                  if (jj == j) {
+                    lz[jj] = run_z;
+                    lc[jj] = run_c;
+                  }
+                run_z = -CUDART_INF_F;
+                run_c = -1;
+                ++j;
+                jend = j < D ? (p.list_col0[j] >> 4) + p.list_nch[j] : 0x7FFFFFFF;
               }
-            run_z = -CUDART_INF_F;
-            run_c = -1;
-          }
-          j = jn;
-          g = gn;
-          if (more) {
-            tmem_wait_ld(vn);
+              const int col = 16 * kg;
+              float z[16];
+              // bias: shared-space 16-B loads (a generic pointer compiled to LD.E.128)
+              const uint32_t b_addr = s_bias_addr + 4u * static_cast<uint32_t>(col);
 #pragma unroll
-            for (int i = 0; i < 16; ++i) v[i] = vn[i];
+              for (int i = 0; i < 4; ++i) {
+                float bb[4];
+                asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                             : "=f"(bb[0]), "=f"(bb[1]), "=f"(bb[2]), "=f"(bb[3])
+                             : "r"(b_addr + 16u * i));
+                z[4 * i + 0] = __uint_as_float(v[16 * h + 4 * i + 0]) + bb[0];
+                z[4 * i + 1] = __uint_as_float(v[16 * h + 4 * i + 1]) + bb[1];
+                z[4 * i + 2] = __uint_as_float(v[16 * h + 4 * i + 2]) + bb[2];
+                z[4 * i + 3] = __uint_as_float(v[16 * h + 4 * i + 3]) + bb[3];
+              }
+              float zc;
+              int ic;
+              argmax16(z, zc, ic);
+              if (zc > run_z) {  // strict: an earlier group (smaller labels) keeps ties
+                run_z = zc;
+                run_c = col + ic;
+              }
+            }
           }
+          k = min(kn, khi);
+          if (k < khi) {
+            tmem_wait_ld32(vn);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = vn[i];
+          }
+        }
+        if (ps + 1 == p.n_pass && j < D) {  // the last list
+#pragma unroll
+          for (int jj = 0; jj < kMaxLists; ++jj)
+            if (jj == j) {
+              lz[jj] = run_z;
+              lc[jj] = run_c;
+            }
         }
         tc_fence_before();
         __syncwarp();
+        if (tr) tr[warp == 2 ? 7 : 12] = tnow();
         if (lane == 0) {  // the MMA may overwrite this accumulator
           if (rank == 0) mbar_arrive(tempty + b);
           else mbar_arrive_cl(tempty_l + 8u * b);
@@ -587,6 +733,8 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
         }
         rb.zp = zp; rb.kp = kp; rb.zm = zm; rb.km = km;
         finish_batch(ep, rb, nullptr, lane);
+        if (warp == 2 && lane == 0)
+          if (unsigned long long* tr = trace_slot(p, st)) tr[8] = tnow();
       } else {
         // application-choice order / Multi-Select: the list maxima P_j themselves
         float zj[8];
@@ -932,16 +1080,26 @@ sc_status sc_head_loss_fwd_bwd(sc_context ctx, sc_head head, const sc_head_batch
   p.rows = b.rows;
   p.n_kb = static_cast<int32_t>((head->d + sc::kBK - 1) / sc::kBK);
   p.n_cols = head->n_cols;
-  p.chunk = head->chunk;
-  p.n_chunks = head->n_chunks;
+  // MMA column chunks: each its own accumulator chain (SC_HEAD_NCHUNK = 1, 2 or 4 overrides)
+  {
+    const int32_t cols = head->n_pass > 1 ? head->pass_w : head->n_cols;
+    int nch = head->n_chunks;
+    if (const char* e = std::getenv("SC_HEAD_NCHUNK")) nch = std::atoi(e);
+    if (nch != 1 && nch != 2 && nch != 4) nch = head->n_chunks;
+    while (nch > 1 && (cols % (nch * 16) != 0 || cols / nch > 256)) nch /= 2;
+    if (cols / nch > 256) nch = 2;
+    p.n_chunks = nch;
+    p.chunk = cols / nch;
+  }
   p.n_pass = head->n_pass;
   p.pass_w = head->pass_w;
+  p.n_groups = head->n_lists > 0 ? (head->list_col0[head->n_lists - 1] >> 4) + head->list_nch[head->n_lists - 1] : 0;
   p.pat = ctx->order == SC_ORDER_API_OUTPUT ? 0 : 1;
   p.acc_bufs = (p.n_pass > 1 || 2 * head->n_cols <= sc::kMaxCols) ? 2 : 1;
   // lone CTAs: two 128-row tiles per unit share every W stage (W_𝕎, re-read from L2 for each
   // unit, moves half the bytes per row) when both accumulators fit TMEM; then single-buffered
   const char* t2env = std::getenv("SC_HEAD_T2");
-  const bool t2_ok = head->n_pass == 1 && head->n_chunks == 1 && 2 * head->n_cols <= sc::kMaxCols &&
+  const bool t2_ok = head->n_pass == 1 && 2 * head->n_cols <= sc::kMaxCols &&
                      !(t2env && std::atoi(t2env) == 0);
   p.n_lists = head->n_lists;
   for (int j = 0; j < sc::kMaxLists; ++j) {
@@ -949,6 +1107,13 @@ sc_status sc_head_loss_fwd_bwd(sc_context ctx, sc_head head, const sc_head_batch
     p.list_nch[j] = head->list_nch[j];
   }
   p.probe = std::getenv("SC_HEAD_PROBE") ? std::atoi(std::getenv("SC_HEAD_PROBE")) : 0;
+  const char* trace_file = std::getenv("SC_HEAD_TRACE");  // experiment: per-unit timeline, see trace_slot
+  const size_t trace_n = static_cast<size_t>(sc::kTraceCtas) * sc::kTraceUnits * sc::kTraceSlots;
+  if (trace_file) {
+    if (cudaMalloc(&p.trace, trace_n * 8) != cudaSuccess ||
+        cudaMemsetAsync(p.trace, 0, trace_n * 8, static_cast<cudaStream_t>(stream)) != cudaSuccess)
+      return sc::set_error(SC_ERR_CUDA, "sc_head_loss_fwd_bwd: trace buffer");
+  }
   const int a_bytes = sc::kBM * sc::kBK * 2;
   const int tab_bytes = head->n_cols * 8;
   const int bar_bytes = 8 * (2 * 32 + 4) + 16;
@@ -965,7 +1130,7 @@ sc_status sc_head_loss_fwd_bwd(sc_context ctx, sc_head head, const sc_head_batch
     const bool want_pair = attempt == 0 && head->n_pass == 1;
     if (attempt == 0 && !want_pair) continue;
     // one k-block of the W rows an MMA pass reads (all n_cols, or pass_w in column passes)
-    const int32_t pass_cols = head->chunk * head->n_chunks;
+    const int32_t pass_cols = p.chunk * p.n_chunks;
     p.w_stage_bytes = (want_pair ? pass_cols / 2 : pass_cols) * sc::kBK * 2;
     // two row tiles per unit share every W stage (lone CTAs by default; CTA pairs with
     // SC_HEAD_PAIR_T2=1: 512 rows per pass over W)
@@ -1038,6 +1203,11 @@ sc_status sc_head_loss_fwd_bwd(sc_context ctx, sc_head head, const sc_head_batch
   if (x3d ? !make_map3(&map_x, b.x, head->d, b.rows, b.ldx, p.kbs)
           : !make_map(&map_x, b.x, head->d, b.rows, b.ldx, sc::kBM))
     return sc::set_error(SC_ERR_CUDA, "sc_head_loss_fwd_bwd: cuTensorMapEncodeTiled failed");
+  // W boxes: the rows of one MMA chunk (half of them per CTA of a pair)
+  CUtensorMap map_w;
+  if (!make_map(&map_w, head->Wm, sc::kBK, static_cast<int64_t>(p.n_kb) * head->n_cols, sc::kBK,
+                pair ? p.chunk / 2 : p.chunk))
+    return sc::set_error(SC_ERR_CUDA, "sc_head_loss_fwd_bwd: cuTensorMapEncodeTiled failed");
   const int64_t units = std::max<int64_t>(1, std::min<int64_t>(pair ? hl.units : sms, p.n_units));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaError_t le = cudaSuccess;
@@ -1054,15 +1224,25 @@ sc_status sc_head_loss_fwd_bwd(sc_context ctx, sc_head head, const sc_head_batch
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    le = cudaLaunchKernelEx(&cfg, sc::head_kernel<true>, map_x, head->map_w[1], p);
+    le = cudaLaunchKernelEx(&cfg, sc::head_kernel<true>, map_x, map_w, p);
     sc::note_launch("head_tcgen05_pair");
   } else {
-    sc::head_kernel<false><<<static_cast<unsigned>(units), sc::kHeadThreads, smem, st>>>(map_x, head->map_w[0], p);
+    sc::head_kernel<false><<<static_cast<unsigned>(units), sc::kHeadThreads, smem, st>>>(map_x, map_w, p);
     sc::note_launch("head_tcgen05");
   }
   if (le) return sc::set_error(SC_ERR_CUDA, "sc_head_loss_fwd_bwd: %s", cudaGetErrorString(le));
   if (cudaError_t e2 = cudaGetLastError())
     return sc::set_error(SC_ERR_CUDA, "sc_head_loss_fwd_bwd: %s", cudaGetErrorString(e2));
+  if (trace_file) {  // experiment only: synchronous, appends one binary record per launch
+    std::vector<unsigned long long> h(trace_n);
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h.data(), p.trace, trace_n * 8, cudaMemcpyDeviceToHost);
+    cudaFree(p.trace);
+    if (FILE* f = std::fopen(trace_file, "ab")) {
+      std::fwrite(h.data(), 8, trace_n, f);
+      std::fclose(f);
+    }
+  }
   return SC_OK;
 }
 

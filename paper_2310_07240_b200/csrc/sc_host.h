@@ -37,6 +37,11 @@ struct sc_context_s {
   uint32_t* d_lent = nullptr;
   int32_t* d_lent_off = nullptr;
   uint32_t* d_lslot = nullptr;
+  // all-apps pass, lane per application (see AllAppsParams)
+  uint32_t* d_aa_ent = nullptr;
+  int32_t* d_aa_goff = nullptr;
+  uint16_t* d_aa_perm = nullptr;
+  int32_t aa_groups = 0, aa_ent_total = 0;
 };
 
 namespace sc {

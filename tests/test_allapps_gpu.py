@@ -9,14 +9,35 @@ from conftest import gpu_available
 pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device")]
 
 
-@pytest.mark.parametrize("dtype,rows", [("f32", 600), ("bf16", 301), ("f32", 603)])  # 4-row units, ragged tails
-def test_all_apps_parity(dtype, rows):
+def random_apps_spec(A, C, seed):
+    """A applications with 0..8 overlapping lists of 0..60 labels (some with no mapped label)."""
+    import synth
+    rng = np.random.default_rng(seed)
+    apps = []
+    for _ in range(A):
+        D = int(rng.integers(0, 9))
+        apps.append([sorted(set(rng.integers(0, C, size=int(rng.integers(0, 61))).tolist())) for _ in range(D)])
+    return synth.ContextSpec(C, apps, 0.0, 10.0)
+
+
+@pytest.mark.parametrize("impl", ["lane", "warp"])
+@pytest.mark.parametrize("cfg,dtype,rows", [(4, "f32", 600), (4, "bf16", 301), (4, "f32", 603),  # ragged unit tails
+                                            ("r300", "f32", 257), ("r300", "bf16", 130), ("r33", "f32", 999)])
+def test_all_apps_parity(impl, cfg, dtype, rows, monkeypatch):
+    """Both kernels: lane per application (default; applications grouped 32 at a time by size,
+    a partial last group with cfg "r300" / "r33", applications with no mapped label) and warp
+    per application (SC_ALLAPPS=warp)."""
     import torch
     import paper_2310_07240_b200 as sc
     import synth
     from oracle import Oracle
     from test_parity_gpu import to_dev
-    spec = synth.config_context(4)
+    if impl == "warp":
+        monkeypatch.setenv("SC_ALLAPPS", "warp")
+    if cfg == 4:
+        spec = synth.config_context(4)
+    else:
+        spec = random_apps_spec(int(cfg[1:]), 997, seed=rows)
     wl = synth.Workload(spec, seed=4, dtype=dtype, layout=1)
     b = wl.host_batch(1234, rows)
     d = to_dev(b, dtype)
@@ -28,6 +49,7 @@ def test_all_apps_parity(dtype, rows):
     sc.sc_decide_all_apps(ctx, sc.Batch(logits=d["logits"], gt_off=d["gt_off"], gt_lab=d["gt_lab"]),
                           n_incorrect=ni, hist_pred=hp, decision=dec)
     torch.cuda.synchronize()
+    assert sc.sc_last_kernel() == ("all_apps_warp" if impl == "warp" else "all_apps_lane")
     dec = dec.cpu().numpy().reshape(rows, A)
     orc = Oracle.from_spec(spec)
     ni_ref = np.zeros(A, np.uint64)

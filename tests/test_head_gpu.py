@@ -398,3 +398,36 @@ def test_head_patterns_and_passes(order, name, d, rows, mode):
     if name in WIDE:
         assert g["n_cols"] > 512
     compare_exact(g, o)
+
+
+@pytest.mark.parametrize("nchunk", [1, 2, 4])
+@pytest.mark.parametrize("name,rows,q", [("cfg2", 5000, 1), ("w300", 3000, 1), ("w512", 700, 1), ("cfg2", 3000, 2),
+                                         ("cfg1", 300, 1)])
+def test_head_mma_chunks(nchunk, name, rows, q, monkeypatch):
+    """The head's columns split into 1, 2 or 4 MMA chunks (SC_HEAD_NCHUNK), each its own
+    accumulator chain: the same exact results (integer operands)."""
+    torch, sc, synth, _ = _mods()
+    spec = SPECS[name](synth)
+    d = 192
+    x, W, b = synth.head_operands(spec.C, d, rows, seed=nchunk + rows, kind="int")
+    gt_off, gt_lab = gt_for(spec, rows, seed=nchunk)
+    w = weights(spec, gt_off, gt_lab)
+    monkeypatch.setenv("SC_HEAD_NCHUNK", str(nchunk))
+    monkeypatch.setenv("SC_HEAD_CLUSTER", str(q))
+    g = run_head(spec, x, W, b, gt_off, gt_lab, w=w, mode="mask", grad_scale=1.0 / rows)
+    o, _, _ = oracle_eval(spec, x, W, b, gt_off, gt_lab, w=w, grad_scale=1.0 / rows)
+    compare_exact(g, o)
+
+
+@pytest.mark.parametrize("nchunk", [1, 2])
+def test_head_mma_chunks_passes(nchunk, monkeypatch):
+    torch, sc, synth, _ = _mods()
+    spec = synth.config_context(3)
+    rows, d = 300, 128
+    x, W, b = synth.head_operands(spec.C, d, rows, seed=3 + nchunk, kind="int")
+    gt_off, gt_lab = gt_for(spec, rows, seed=3)
+    w = weights(spec, gt_off, gt_lab)
+    monkeypatch.setenv("SC_HEAD_NCHUNK", str(nchunk))
+    g = run_head(spec, x, W, b, gt_off, gt_lab, w=w, mode="mask", grad_scale=1.0 / rows)
+    o, _, _ = oracle_eval(spec, x, W, b, gt_off, gt_lab, w=w, grad_scale=1.0 / rows)
+    compare_exact(g, o)
