@@ -445,7 +445,7 @@ def run_ours(args):
         line["e2e"] = run_e2e(args, ev, data, global_rows, dev, barrier, world)
     del data, logits
     torch.cuda.empty_cache()
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:  # the oracle baseline: rank 0 at N = 1 only
         rate, rows, dt, threads, smp = cpu_oracle_rate(args.cpu_seconds)
         rate1, rows1, dt1, _, smp1 = cpu_oracle_rate(min(4.0, args.cpu_seconds / 3), threads=1)
         line["cpu_baseline"] = {"value": rate, "unit": "samples/s", "cores": threads, "kind": "oracle",

@@ -311,7 +311,9 @@ const char* sc_ranges_last_error(void);
  *   u          device [2n] double uniforms in [0,1), interleaved (u1, u2) per draw
  *   out        device [n] int64 row indices (-1 for every draw if all weights are 0)
  *   workspace  device scratch of at least sc_sample_workspace_bytes(rows) bytes
- * Four launches, stream-ordered; no allocation. */
+ *   rows       1 .. 2^31 - 1 (SC_ERR_INVALID_ARG otherwise)
+ * Five launches (mask counts per 1024-row chunk, per-mask scans, bucket starts + CDF, a stable
+ * scatter, the draws), stream-ordered; no allocation. */
 size_t sc_sample_workspace_bytes(int64_t rows);
 sc_status sc_rebalance_sample(const uint8_t* gt_mask, int64_t rows, const float* w, const double* u, int64_t n,
                               int64_t* out, void* workspace, size_t workspace_bytes, sc_stream stream);

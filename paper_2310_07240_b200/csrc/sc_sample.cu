@@ -9,9 +9,10 @@
 // min(count_m − 1, floor(u2·count_m)) of the bucket.
 //
 // Five launches: per-chunk mask counts; per-mask scans over the chunks (one CTA per mask);
-// bucket starts and the CDF in the oracle's summation order (one CTA); a stable scatter
-// (one warp per 1024-row chunk, rows in order); the draws (one thread per draw, CDF in
-// shared memory).
+// bucket starts and the CDF in the oracle's summation order (one CTA); a stable scatter (one
+// 1024-thread CTA per 1024-row chunk: per-warp ranks from __match_any_sync, a per-mask
+// prefix over the chunk's 32 warps in shared memory); the draws (one thread per draw, CDF in
+// shared memory).  Row ids are int32 in the bucket order (rows < 2^31).
 #include "sc.h"
 
 #include <cuda_runtime.h>
@@ -22,7 +23,6 @@ namespace {
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
 constexpr int64_t kChunk = 1024;  // rows per chunk of the counting sort (one scatter warp each)
-constexpr int kScatterWarps = 8;  // chunks per scatter CTA
 
 thread_local std::string g_serr;
 
@@ -37,7 +37,7 @@ struct Workspace {  // carved from the caller's buffer
   int64_t* count;        // [256]
   int64_t* start;        // [256]
   double* cum;           // [256]
-  int64_t* order;        // [rows] row ids in bucket order
+  int32_t* order;        // [rows] row ids in bucket order
   int* status;           // [1]  0 ok, 1 all weights zero
 };
 
@@ -62,8 +62,8 @@ size_t layout(int64_t rows, Workspace* ws, uint8_t* base) {
   if (ws) ws->start = reinterpret_cast<int64_t*>(p);
   p = take(sizeof(double) * 256);
   if (ws) ws->cum = reinterpret_cast<double*>(p);
-  p = take(sizeof(int64_t) * (rows > 0 ? rows : 1));
-  if (ws) ws->order = reinterpret_cast<int64_t*>(p);
+  p = take(sizeof(int32_t) * (rows > 0 ? rows : 1));
+  if (ws) ws->order = reinterpret_cast<int32_t*>(p);
   p = take(sizeof(int));
   if (ws) ws->status = reinterpret_cast<int*>(p);
   return off;
@@ -109,50 +109,74 @@ __global__ void __launch_bounds__(256) chunk_scan_kernel(const unsigned* chunk_c
   if (threadIdx.x == 0) ws.count[m] = carry_s;
 }
 
-// One CTA: bucket starts and the CDF, sequential in ascending m (the oracle's summation order).
+// One CTA: bucket starts (an exclusive scan of the counts) and the CDF.  The products
+// count_m·w[m] are formed in parallel; their running sum is taken by one thread in ascending m
+// from shared memory (the oracle's summation order, so both compare identical doubles).
 __global__ void __launch_bounds__(256) starts_kernel(const float* w, Workspace ws) {
   __shared__ int64_t cnt[256];
-  cnt[threadIdx.x] = ws.count[threadIdx.x];
+  __shared__ double prod[256];
+  __shared__ int64_t wsum[8];
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const int64_t c = ws.count[t];
+  cnt[t] = c;
+  prod[t] = static_cast<double>(c) * static_cast<double>(w[t]);
+  int64_t x = c;  // inclusive warp scan of the counts
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int64_t y = __shfl_up_sync(kFull, x, off);
+    if (lane >= off) x += y;
+  }
+  if (lane == 31) wsum[wid] = x;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int64_t s = 0;
+  int64_t before = 0;
+  for (int q = 0; q < wid; ++q) before += wsum[q];
+  ws.start[t] = before + x - c;
+  if (t == 0) {
     double tot = 0.0;
     for (int q = 0; q < 256; ++q) {
-      ws.start[q] = s;
-      s += cnt[q];
-      tot += static_cast<double>(cnt[q]) * static_cast<double>(w[q]);
-      ws.cum[q] = tot;
+      tot += prod[q];
+      prod[q] = tot;
     }
     *ws.status = tot > 0.0 ? 0 : 1;
   }
+  __syncthreads();
+  ws.cum[t] = prod[t];
 }
 
-// One warp per chunk walks its rows in order: stable rank among equal masks.
-__global__ void __launch_bounds__(32 * kScatterWarps) scatter_kernel(const uint8_t* gt_mask, int64_t rows,
-                                                                    int64_t nch, Workspace ws) {
-  __shared__ int64_t next_s[kScatterWarps][256];
+// One CTA per chunk (32 warps x 32 rows): a row's slot in its mask's bucket = bucket start +
+// rows of that mask in earlier chunks (chunk_off) + in earlier warps of this chunk (prefix of
+// the per-warp counts) + earlier lanes of its warp with the same mask (__match_any_sync), so
+// equal masks keep row order (stable).
+__global__ void __launch_bounds__(kChunk) scatter_kernel(const uint8_t* gt_mask, int64_t rows, Workspace ws) {
+  __shared__ uint16_t cnt[32][256];  // per warp and mask: count, then exclusive prefix over the warps
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int64_t chunk = static_cast<int64_t>(blockIdx.x) * kScatterWarps + wid;
-  if (chunk >= nch) return;  // whole warps only: no CTA-wide barrier below
-  int64_t* next = next_s[wid];
-  for (int m = lane; m < 256; m += 32) next[m] = ws.start[m] + ws.chunk_off[chunk * 256 + m];
-  __syncwarp();
-  const int64_t lo = chunk * kChunk;
-  const int64_t hi = lo + kChunk < rows ? lo + kChunk : rows;
-  for (int64_t i0 = lo; i0 < hi; i0 += 32) {
-    const int64_t i = i0 + lane;
-    const bool act = i < hi;
-    const unsigned am = __ballot_sync(kFull, act);
-    if (act) {
-      const unsigned key = gt_mask[i];
-      const unsigned peers = __match_any_sync(am, key);
-      const int rank = __popc(peers & ((1u << lane) - 1u));
-      const int64_t slot = next[key] + rank;
-      ws.order[slot] = i;
-      __syncwarp(am);
-      if (lane == __ffs(peers) - 1) next[key] += __popc(peers);
+  const int64_t chunk = blockIdx.x;
+  for (int i = threadIdx.x; i < 32 * 256; i += blockDim.x) (&cnt[0][0])[i] = 0;
+  __syncthreads();
+  const int64_t i = chunk * kChunk + threadIdx.x;
+  const bool act = i < rows;
+  const unsigned am = __ballot_sync(kFull, act);
+  unsigned key = 0, rank = 0;
+  if (act) {
+    key = gt_mask[i];
+    const unsigned peers = __match_any_sync(am, key);
+    rank = __popc(peers & ((1u << lane) - 1u));
+    if (lane == __ffs(peers) - 1) cnt[wid][key] = static_cast<uint16_t>(__popc(peers));
+  }
+  __syncthreads();
+  if (threadIdx.x < 256) {
+    unsigned run = 0;
+#pragma unroll 8
+    for (int w = 0; w < 32; ++w) {
+      const unsigned v = cnt[w][threadIdx.x];
+      cnt[w][threadIdx.x] = static_cast<uint16_t>(run);
+      run += v;
     }
-    __syncwarp();
+  }
+  __syncthreads();
+  if (act) {
+    const int64_t slot = ws.start[key] + ws.chunk_off[chunk * 256 + key] + cnt[wid][key] + rank;
+    ws.order[slot] = static_cast<int32_t>(i);
   }
 }
 
@@ -190,6 +214,7 @@ size_t sc_sample_workspace_bytes(int64_t rows) { return layout(rows < 0 ? 0 : ro
 sc_status sc_rebalance_sample(const uint8_t* gt_mask, int64_t rows, const float* w, const double* u, int64_t n,
                               int64_t* out, void* workspace, size_t workspace_bytes, sc_stream stream) {
   if (rows <= 0) return sfail(SC_ERR_INVALID_ARG, "rows must be > 0");
+  if (rows > INT32_MAX) return sfail(SC_ERR_INVALID_ARG, "rows must be < 2^31");
   if (n < 0) return sfail(SC_ERR_INVALID_ARG, "n < 0");
   if (!gt_mask || !w || !workspace || (n > 0 && (!u || !out))) return sfail(SC_ERR_INVALID_ARG, "NULL argument");
   if (workspace_bytes < sc_sample_workspace_bytes(rows)) return sfail(SC_ERR_INVALID_ARG, "workspace too small");
@@ -201,8 +226,7 @@ sc_status sc_rebalance_sample(const uint8_t* gt_mask, int64_t rows, const float*
   chunk_count_kernel<<<static_cast<unsigned>(nch), 256, 0, st>>>(gt_mask, rows, ws.chunk_cnt);
   chunk_scan_kernel<<<256, 256, 0, st>>>(ws.chunk_cnt, nch, ws);
   starts_kernel<<<1, 256, 0, st>>>(w, ws);
-  scatter_kernel<<<static_cast<unsigned>((nch + kScatterWarps - 1) / kScatterWarps), 32 * kScatterWarps, 0, st>>>(
-      gt_mask, rows, nch, ws);
+  scatter_kernel<<<static_cast<unsigned>(nch), kChunk, 0, st>>>(gt_mask, rows, ws);
   if (n > 0) {
     int64_t g = (n + 255) / 256;
     if (g > 148 * 16) g = 148 * 16;
