@@ -727,7 +727,6 @@ sc_status sc_decide_all_apps(sc_context ctx, const sc_batch* b, uint64_t* n_inco
   p.ld_bytes = b->ld * elt;
   p.bf16 = b->dtype == SC_BF16;
   p.copy_bytes = static_cast<uint32_t>(round_up(static_cast<int64_t>(ctx->C) * elt, 16));
-  p.row_bytes_pad = static_cast<int32_t>(round_up(p.copy_bytes, 128));
   p.n_ent_total = ctx->n_ent_total;
   p.gt_off = b->gt_off;
   p.gt_lab = b->gt_lab;

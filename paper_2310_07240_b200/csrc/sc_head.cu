@@ -794,8 +794,7 @@ struct sc_head_s {
   float* bias = nullptr;   // [n_cols]
   uint32_t* keys = nullptr;
   int32_t* col_label = nullptr;
-  CUtensorMap map_w[2];    // [0]: box rows = chunk (one CTA), [1]: chunk / 2 (CTA pair)
-  bool map_ok[2] = {false, false};
+  bool pair_ok = false;    // CTA pairs possible: half a chunk per CTA is a whole number of 8-row swizzle atoms
 };
 
 namespace {
@@ -993,9 +992,9 @@ sc_status sc_head_load(sc_context ctx, const uint16_t* weight, int64_t ldw, int6
     return sc::set_error(e == cudaErrorMemoryAllocation ? SC_ERR_OOM : SC_ERR_CUDA, "sc_head_load: %s",
                          cudaGetErrorString(e));
   }
-  h->map_ok[0] = make_map(&h->map_w[0], h->Wm, sc::kBK, static_cast<int64_t>(n_kb) * n, sc::kBK, h->chunk);
-  h->map_ok[1] = make_map(&h->map_w[1], h->Wm, sc::kBK, static_cast<int64_t>(n_kb) * n, sc::kBK, h->chunk / 2);
-  if (!h->map_ok[0]) {
+  CUtensorMap probe_map;  // the W maps are encoded per launch (their box is the launch's MMA chunk)
+  h->pair_ok = (h->chunk / 2) % 8 == 0;
+  if (!make_map(&probe_map, h->Wm, sc::kBK, static_cast<int64_t>(n_kb) * n, sc::kBK, h->chunk)) {
     sc_head_free(h);
     return sc::set_error(SC_ERR_CUDA, "sc_head_load: cuTensorMapEncodeTiled failed");
   }
@@ -1191,7 +1190,7 @@ sc_status sc_head_loss_fwd_bwd(sc_context ctx, sc_head head, const sc_head_batch
     });
     if (attr_err) return sc::set_error(SC_ERR_CUDA, "sc_head_loss_fwd_bwd: %s", cudaGetErrorString(attr_err));
     hl = pick_launch(smem, sms, n_tiles);
-    if (want_pair && !(hl.pair && head->map_ok[1])) continue;  // re-plan the ring for a lone CTA
+    if (want_pair && !(hl.pair && head->pair_ok && (p.chunk / 2) % 8 == 0)) continue;  // re-plan for a lone CTA
     pair = want_pair;
     break;
   }

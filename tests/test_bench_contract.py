@@ -1,0 +1,53 @@
+"""Host-side checks of bench.py's launch contract (CPU, no GPU): `--gpus N` never reports a
+world size other than N, and the reference arm prints the contract's JSON line."""
+import importlib.util
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def load_bench():
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    m = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(m)
+    return m
+
+
+class Args:
+    def __init__(self, gpus, impl="ours"):
+        self.gpus, self.impl = gpus, impl
+
+
+def test_gpus_must_match_world_size(monkeypatch):
+    b = load_bench()
+    monkeypatch.setenv("WORLD_SIZE", "4")
+    assert b.launch_ranks(Args(8)) == 2          # --gpus 8 under a 4-rank launch: refused
+    a = Args(None)
+    assert b.launch_ranks(a) is None and a.gpus == 4  # the launcher's world size is taken
+    a = Args(4)
+    assert b.launch_ranks(a) is None and a.gpus == 4
+
+
+def test_single_process_defaults(monkeypatch):
+    b = load_bench()
+    monkeypatch.delenv("WORLD_SIZE", raising=False)
+    a = Args(None)
+    assert b.launch_ranks(a) is None and a.gpus == 1
+    a = Args(8, impl="reference")                # the reference arm runs on rank 0 only
+    assert b.launch_ranks(a) is None and a.gpus == 8
+
+
+def test_reference_arm_line():
+    """--impl reference: the oracle on this host's cores, one bounded sample per step."""
+    env = dict(os.environ)
+    env.pop("WORLD_SIZE", None)
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
+                          "--warmup", "0"], capture_output=True, text=True, env=env, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["unit"] == "samples/s" and line["value"] > 0
+    assert line["cpu_baseline"]["kind"] == "oracle" and line["cpu_baseline"]["cores"] >= 1
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["higher_is_better"] is True
