@@ -219,13 +219,43 @@ __global__ void __launch_bounds__(kAAWarps * 32, 1) all_apps_kernel(const AllApp
       atomicAdd(p.hist_pred + (i >> 4) * 256 + (i & 15), static_cast<unsigned long long>(cnt_pred[i]));
 }
 
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds16(uint32_t a) {
+  unsigned short v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+  return v;
+}
+
+// One entry of a lane's split maxima: plus side iff the entry's list bit is in G.
+__device__ __forceinline__ void aa_entry(float z, uint32_t key, uint32_t G, float& zp, uint32_t& kp, float& zm,
+                                         uint32_t& km) {
+  asm("{\n\t"
+      ".reg .pred bp, gp, gm;\n\t"
+      ".reg .b32 t;\n\t"
+      "and.b32 t, %5, %6;\n\t"  // G < 256: only the list bits survive
+      "setp.ne.u32 bp, t, 0;\n\t"
+      "setp.gt.and.f32 gp, %4, %0, bp;\n\t"
+      "setp.gt.and.f32 gm, %4, %2, !bp;\n\t"
+      "@gp mov.f32 %0, %4;\n\t"
+      "@gp mov.b32 %1, %5;\n\t"
+      "@gm mov.f32 %2, %4;\n\t"
+      "@gm mov.b32 %3, %5;\n\t"
+      "}"
+      : "+f"(zp), "+r"(kp), "+f"(zm), "+r"(km)
+      : "f"(z), "r"(key), "r"(G));
+}
+
 // Lane per application (the default): the 32 lanes of a warp scan 32 different applications
 // of one row, each its own entries in ascending label order (strict '>' keeps the smaller
 // label on ties, A4), so no warp reduction is needed at all; decision, correctness and the
 // counters are per lane.  Applications are grouped 32 at a time by size (largest first) so a
 // warp's lanes run similar trip counts; work items (group, row of the unit) are dealt to the
 // warps in a snake order over the size-sorted items, pairing large groups with small ones.
-// Padding entries point at a -inf slot past the row's copied columns and at list 31, in no G.
+// Padding entries point at a -inf slot past the row's copied columns and carry no list bit.
 __global__ void __launch_bounds__(kAAWarps * 32, 1) all_apps_lane_kernel(const AllAppsParams p) {
   extern __shared__ __align__(128) uint8_t sm[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -310,25 +340,29 @@ __global__ void __launch_bounds__(kAAWarps * 32, 1) all_apps_lane_kernel(const A
       const uint32_t a = perm[slot];
       const bool live = a != 0xFFFFu;
       const uint32_t G = live ? gs[r * A + a] : 0u;
-      const uint8_t* rb = rowbuf + (buf * R + r) * p.row_bytes_pad;
+      const uint32_t rb = smem_u32(rowbuf + (buf * R + r) * p.row_bytes_pad);
       float zp = -CUDART_INF_F, zm = -CUDART_INF_F;
       uint32_t kp = kNone, km = kNone;
-      const uint32_t* e = ents + goff[g] + lane;
+      const uint32_t e0 = smem_u32(ents + goff[g] + lane);
       const int n = (goff[g + 1] - goff[g]) >> 5;
-      for (int t = 0; t < n; ++t) {
-        const uint32_t key = e[32 * t];
-        const uint32_t col = key >> 8;
-        const float z = p.bf16 ? __uint_as_float(static_cast<uint32_t>(*reinterpret_cast<const uint16_t*>(rb + 2u * col)) << 16)
-                               : *reinterpret_cast<const float*>(rb + 4u * col);
-        // padding entries carry list 31 (bit 31 of an 8-bit G is 0: the minus side) and point
-        // at z = -inf, which never beats the running maximum
-        const bool plus = (G >> (key & 0x1Fu)) & 1u;
-        if (plus) {
-          if (z > zp) { zp = z; kp = key; }
-        } else {
-          if (z > zm) { zm = z; km = key; }
+      // keys here are column << 8 | (1 << list): the class test is one AND with G; padding
+      // entries carry no list bit (the minus side) and point at z = -inf, which never wins
+      if (p.bf16) {
+        for (int t = 0; t < n; ++t) {
+          const uint32_t key = lds32(e0 + 128u * t);
+          const float z = __uint_as_float(lds16(rb + 2u * (key >> 8)) << 16);
+          aa_entry(z, key, G, zp, kp, zm, km);
+        }
+      } else {
+        for (int t = 0; t < n; ++t) {
+          const uint32_t key = lds32(e0 + 128u * t);
+          const float z = __uint_as_float(lds32(rb + 4u * (key >> 8)));
+          aa_entry(z, key, G, zp, kp, zm, km);
         }
       }
+      // back to column << 8 | list for the decision
+      if (kp != kNone) kp = (kp & ~0xFFu) | static_cast<uint32_t>(__ffs(kp & 0xFFu) - 1);
+      if (km != kNone) km = (km & ~0xFFu) | static_cast<uint32_t>(__ffs(km & 0xFFu) - 1);
       if (live) {
         uint32_t dec;
         bool ok;

@@ -532,14 +532,16 @@ static sc_status load_context(int32_t C, int32_t n_apps, const int32_t* n_lists,
       goff[g + 1] = goff[g] + 32 * (ent_off[a0 + 1] - ent_off[a0]);
       for (int l = 0; l < 32 && 32 * g + l < n_apps; ++l) aperm[32 * g + l] = static_cast<uint16_t>(perm[32 * g + l]);
     }
-    // padding entries: a key whose column is the row buffer's -inf slot (column round_up(C, 8),
-    // past the bytes a row copy writes for f32 and bf16) and whose list 31 is in no G
-    const uint32_t dummy = (static_cast<uint32_t>((C + 7) / 8 * 8) << 8) | 31u;
+    // keys column << 8 | (1 << list) (the kernel's class test is one AND with G); padding
+    // entries: the row buffer's -inf slot (column round_up(C, 8), past the bytes a row copy
+    // writes for f32 and bf16) and no list bit
+    const uint32_t dummy = static_cast<uint32_t>((C + 7) / 8 * 8) << 8;
     std::vector<uint32_t> aent(std::max<int32_t>(goff[ng], 1), dummy);
     for (int32_t g = 0; g < ng; ++g)
       for (int l = 0; l < 32 && 32 * g + l < n_apps; ++l) {
         const int32_t a = perm[32 * g + l];
-        for (int32_t t = ent_off[a]; t < ent_off[a + 1]; ++t) aent[goff[g] + 32 * (t - ent_off[a]) + l] = ent[t];
+        for (int32_t t = ent_off[a]; t < ent_off[a + 1]; ++t)
+          aent[goff[g] + 32 * (t - ent_off[a]) + l] = (ent[t] & ~0xFFu) | (1u << (ent[t] & 0xFFu));
       }
     ctx->aa_groups = ng;
     ctx->aa_ent_total = goff[ng];
@@ -743,7 +745,7 @@ sc_status sc_decide_all_apps(sc_context ctx, const sc_batch* b, uint64_t* n_inco
     p.aa_perm = ctx->d_aa_perm;
     p.n_groups = ctx->aa_groups;
     p.aa_ent_total = ctx->aa_ent_total;
-    p.dummy_key = (static_cast<uint32_t>((ctx->C + 7) / 8 * 8) << 8) | 31u;
+    p.dummy_key = static_cast<uint32_t>((ctx->C + 7) / 8 * 8) << 8;
     p.row_bytes_pad = static_cast<int32_t>(round_up(static_cast<int64_t>((ctx->C + 7) / 8 * 8 + 1) * elt, 128));
     const int64_t ng = ctx->aa_groups;
     for (int R = 8; R >= 1; R /= 2) {

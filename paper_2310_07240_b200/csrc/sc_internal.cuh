@@ -130,14 +130,15 @@ struct AllAppsParams {
   uint8_t* decision;        // [rows][n_apps] or NULL
   // lane-per-application layout (all_apps_lane_kernel): applications sorted by |𝕎_a| in
   // groups of 32 (lane l of group g = application perm[32 g + l]); group g's entries
-  // transposed, entry e of lane l at aa_ent[aa_goff[g] + 32 e + l] (a dummy key past the
-  // application's own entries), so a lane scans its application with no cross-lane reduction
+  // transposed, entry e of lane l at aa_ent[aa_goff[g] + 32 e + l] as column << 8 | (1 << list)
+  // (a dummy key past the application's own entries), so a lane scans its application with no
+  // cross-lane reduction
   const uint32_t* aa_ent;
   const int32_t* aa_goff;   // [n_groups + 1]
   const uint16_t* aa_perm;  // [n_groups * 32], 0xFFFF = no application
   int32_t n_groups, aa_ent_total;
   int32_t rows_per_unit;    // R
-  uint32_t dummy_key;       // key of a padding entry: column = the row buffer's -inf slot, list 31
+  uint32_t dummy_key;       // key of a padding entry: column = the row buffer's -inf slot, no list bit
 };
 constexpr int kAllAppsRows = 4;  // rows per barrier interval of the warp-per-application kernel
 cudaError_t launch_all_apps_lane(const AllAppsParams& p, int grid, size_t smem, cudaStream_t st);

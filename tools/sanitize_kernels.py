@@ -7,8 +7,10 @@ Covers: the eval kernel on the TMA ring (split maxima and list-major slots, EPL 
 chunked paths), the sector gather kernel, both GT pre-pass kernels with and without the fused
 weights, the weights kernel, the all-apps kernel, the value-ranges kernels (packed / ballot /
 match counters, fast and far S arguments, unaligned arrays), the sampler, and the fused
-classifier head.  Side bands at unaligned offsets and ragged row counts exercise the clamped
-TMA windows.  Outputs are checked against each other only lightly (the parity tests do the
+classifier head.  Round 2 adds: the dense-mapped eval path (column-compacted rows, f32 /
+bf16), the host-buffer entry (copy and zero copy), the lane-per-application all-apps kernel,
+the head under every pattern and with column passes (CTA pairs with two row tiles too).
+Side bands at unaligned offsets and ragged row counts exercise the clamped TMA windows.  Outputs are checked against each other only lightly (the parity tests do the
 real checking); the point is a clean sanitizer report.
 """
 import os
@@ -36,8 +38,8 @@ def dev_batch(b, dtype="f32"):
     return out
 
 
-def step(spec, d, rows, order=0, app=False, mask_off=0, app_off=0):
-    ctx = sc.Context(spec.C, spec.lists, spec.tau, spec.k, order=order, multi_app=True)
+def step(spec, d, rows, order=0, app=False, mask_off=0, app_off=0, compact=False, host=None):
+    ctx = sc.Context(spec.C, spec.lists, spec.tau, spec.k, order=order, multi_app=True, compact=compact)
     na, S = spec.n_apps, ctx.grad_slots
     ap = None
     if app:
@@ -64,7 +66,14 @@ def step(spec, d, rows, order=0, app=False, mask_off=0, app_off=0):
     ld = d["logits"].stride(0)
     if spec.C <= 1000:
         o["grad_dense"] = torch.empty(rows * ld, dtype=torch.float32, device="cuda")
-    sc.sc_loss_fwd_bwd(ctx, sc.Batch(logits=d["logits"][:rows], gt_mask=gm, app=ap), w=w, grad_scale=1.0 / rows, **o)
+    if host is None:
+        sc.sc_loss_fwd_bwd(ctx, sc.Batch(logits=d["logits"][:rows], gt_mask=gm, app=ap), w=w, grad_scale=1.0 / rows, **o)
+    else:  # (mode, stager chunk rows): logits from pinned host memory
+        hmode, crows = host
+        hl = d["logits"][:rows].cpu().pin_memory()
+        stg = sc.Stager(crows * hl.stride(0) * hl.element_size()) if crows else None
+        sc.sc_loss_fwd_bwd_host(ctx, stg, sc.Batch(logits=hl, gt_mask=gm, app=ap), mode=hmode, w=w,
+                                grad_scale=1.0 / rows, **o)
     sc.sc_decide(ctx, sc.Batch(logits=d["logits"][:rows], gt_off=d["gt_off"][:rows + 1], gt_lab=d["gt_lab"], app=ap),
                  decision=o["decision"], n_incorrect=o["n_incorrect"], hist_pred=o["hist_pred"], hist_gt=o["hist_gt"])
     torch.cuda.synchronize()
@@ -100,6 +109,23 @@ def main():
     seen.append(("auto", "hist_warp", "f32", 0, step(spec, dev_batch(b), 999, mask_off=9)))
     os.environ.pop("SC_HIST")
 
+    # column-compacted rows: the dense-mapped path (> 256 mapped columns), f32 and bf16
+    for cfg, dtype, rows in ((3, "f32", 45), (3, "bf16", 70)):
+        spec = synth.config_context(cfg)
+        b = synth.Workload(spec, seed=cfg, dtype=dtype).host_batch(5, rows)
+        cols = np.nonzero(spec.mapped().any(axis=0))[0]
+        ldc = synth.default_ld(len(cols), dtype)
+        lg = np.zeros((rows, ldc), dtype=b["logits"].dtype)
+        lg[:, :len(cols)] = b["logits"][:, cols]
+        bc = dict(b)
+        bc["logits"] = lg
+        seen.append(("compact", cfg, dtype, step(spec, dev_batch(bc, dtype), rows, compact=True)))
+    # host-buffer entry: chunked copies (ragged last chunk) and zero copy
+    spec = synth.config_context(2)
+    b = synth.Workload(spec, seed=2).host_batch(3, 700)
+    seen.append(("host_copy", step(spec, dev_batch(b), 700, host=(1, 256))))
+    seen.append(("host_zero_copy", step(spec, dev_batch(b), 700, host=(2, 0))))
+
     # one read, every application
     spec = synth.config_context(4)
     b = synth.Workload(spec, seed=4, layout=1).host_batch(0, 77)
@@ -108,10 +134,14 @@ def main():
     ni = torch.zeros(256, dtype=torch.int64, device="cuda")
     hp = torch.zeros(256 * 256, dtype=torch.int64, device="cuda")
     dec = torch.empty(77 * 256, dtype=torch.uint8, device="cuda")
-    sc.sc_decide_all_apps(ctx, sc.Batch(logits=d["logits"], gt_off=d["gt_off"], gt_lab=d["gt_lab"]), n_incorrect=ni,
-                          hist_pred=hp, decision=dec)
-    torch.cuda.synchronize()
-    seen.append(("all_apps", sc.sc_last_kernel()))
+    for impl in ("lane", "warp"):
+        if impl == "warp":
+            os.environ["SC_ALLAPPS"] = "warp"
+        sc.sc_decide_all_apps(ctx, sc.Batch(logits=d["logits"], gt_off=d["gt_off"], gt_lab=d["gt_lab"]),
+                              n_incorrect=ni, hist_pred=hp, decision=dec)
+        torch.cuda.synchronize()
+        seen.append(("all_apps", sc.sc_last_kernel()))
+    os.environ.pop("SC_ALLAPPS")
 
     # value ranges: 2-8 bins packed, 21 ballot, 41 match; far S arguments; unaligned arrays
     for m, off, scale in ((7, 0, 1.0), (7, 1, 12.0), (20, 0, 1.0), (40, 3, 12.0)):
@@ -146,11 +176,16 @@ def main():
     assert int(out.min()) >= 0 and int(out.max()) < 5000
     seen.append(("sampler",))
 
-    # fused head: two tiles per unit (cfg2), one tile (w300), ragged rows
-    for sizes, d_, rows in (((90, 30, 60), 256, 300), ((120, 100, 80), 128, 129)):
+    # fused head: two tiles per unit (cfg2), one tile (w300), column passes (w560), the
+    # per-list patterns, CTA pairs with two row tiles; ragged rows
+    for sizes, d_, rows, order, env in (((90, 30, 60), 256, 300, 0, {}), ((120, 100, 80), 128, 129, 0, {}),
+                                        ((300, 250), 64, 200, 1, {}), ((90, 30, 60), 128, 600, 2, {}),
+                                        ((90, 30, 60), 128, 1100, 0, {"SC_HEAD_CLUSTER": "2", "SC_HEAD_PAIR_T2": "1"})):
+        os.environ.update(env)
         spec = synth.ContextSpec(1000, [synth.placed_context(1000, sizes, 9)], 0.0, 10.0)
         x, W, bias = synth.head_operands(1000, d_, rows, seed=3, kind="int")
-        ctx = sc.Context(spec.C, spec.lists, multi_app=True)
+        ctx = sc.Context(spec.C, spec.lists, order=order, multi_app=True)
+        S = ctx.grad_slots
         Wd = torch.from_numpy(W.view(np.int16)).cuda().view(torch.bfloat16)
         head = sc.Head(ctx, Wd, torch.from_numpy(bias).cuda())
         xd = torch.from_numpy(x.view(np.int16)).cuda().view(torch.bfloat16)
@@ -158,8 +193,8 @@ def main():
         go, gl = torch.from_numpy(hb["gt_off"]).cuda(), torch.from_numpy(hb["gt_lab"]).cuda()
         o = dict(decision=torch.empty(rows, dtype=torch.uint8, device="cuda"),
                  loss_row=torch.empty(rows, dtype=torch.float32, device="cuda"),
-                 grad_idx=torch.empty(2 * rows, dtype=torch.int32, device="cuda"),
-                 grad_val=torch.empty(2 * rows, dtype=torch.float32, device="cuda"),
+                 grad_idx=torch.empty(S * rows, dtype=torch.int32, device="cuda"),
+                 grad_val=torch.empty(S * rows, dtype=torch.float32, device="cuda"),
                  loss_sum=torch.zeros(1, dtype=torch.float64, device="cuda"),
                  n_incorrect=torch.zeros(1, dtype=torch.int64, device="cuda"),
                  hist_pred=torch.zeros(256, dtype=torch.int64, device="cuda"),
@@ -167,7 +202,9 @@ def main():
         sc.sc_head_loss_fwd_bwd(ctx, head, xd, gt_off=go, gt_lab=gl, grad_scale=1.0 / rows, **o)
         torch.cuda.synchronize()
         assert int(o["hist_pred"].sum()) == rows
-        seen.append(("head", sc.sc_last_kernel(), head.info()))
+        seen.append(("head", order, sc.sc_last_kernel(), head.info()))
+        for k in env:
+            os.environ.pop(k)
     for s in seen:
         print(*s)
     print(f"sanitize_kernels: {sc.sc_launch_count()} libsc launches ok")
