@@ -179,8 +179,15 @@ sc_status run_eval(const sc_context_s* ctx, const sc_batch* b, const float* w, f
   const bool dm = pat == 0 && ctx->n_apps == 1 && whole_rows && (ctx->ncols > 256 || dm_mode == 2) &&
                   ctx->ncols >= 1 && ctx->max_ent == ctx->ncols && dm_nv * dm_vec <= 32 && dm_mode != 0 &&
                   !(std::getenv("SC_KERNEL") && std::string(std::getenv("SC_KERNEL")) == "gather");
+  // application-choice order with <= 256 mapped labels: two arg maxima per row (list k and the
+  // lists before it) plus a warp OR of the output lists, on lane-resident entries (pat 3),
+  // instead of one arg max per 32-label slot (SC_AC2=0 keeps the slots)
+  const char* ac2_env = std::getenv("SC_AC2");
+  const bool ac2 = ctx->order == SC_ORDER_APP_CHOICE && whole_rows && ctx->max_ent <= 256 && want_epl &&
+                   !(ac2_env && std::atoi(ac2_env) == 0) &&
+                   !(std::getenv("SC_KERNEL") && std::string(std::getenv("SC_KERNEL")) == "gather");
   // ---- kernel choice: sector-sparse gather when the mapped labels leave enough row sectors untouched
-  if (!dm) {
+  if (!dm && !ac2) {
     const char* kenv = std::getenv("SC_KERNEL");
     const int dt = b->dtype == SC_BF16 ? 1 : 0;
     // HBM is read in 128-B lines here (measured: sector-sparse loads still move whole lines),
@@ -235,6 +242,10 @@ sc_status run_eval(const sc_context_s* ctx, const sc_batch* b, const float* w, f
   // rows fit a stage.  SC_EPL=0 forces the shared-list path.
   if (lane_ok) epl = pat ? std::max(1, ctx->max_slots) : sc::eval_epl_for(ctx->max_ent);
   int launch_pat = pat;
+  if (ac2) {
+    epl = sc::eval_epl_for(ctx->max_ent);
+    launch_pat = 3;
+  }
   if (dm) {
     epl = dm_nv;
     launch_pat = 2;
@@ -287,7 +298,9 @@ sc_status run_eval(const sc_context_s* ctx, const sc_batch* b, const float* w, f
     p.ent_mode = 3;  // lane registers
     if (ctx->n_apps == 1 && launch_pat != 1) {
       p.pmtab_bits = ctx->nlists[0];
-      pmtab_bytes = (int64_t(1) << p.pmtab_bits) * 32 * 4;
+      // pat 3: two masks per k = 0..D' (list k, lists before k); else one per G value
+      pmtab_bytes = launch_pat == 3 ? static_cast<int64_t>(p.pmtab_bits + 1) * 2 * 32 * 4
+                                    : (int64_t(1) << p.pmtab_bits) * 32 * 4;
     }
   } else if (ctx->n_apps == 1 && static_cast<int64_t>(ctx->max_ent) * 4 <= 64 * 1024) {
     p.ent_mode = 0;
@@ -331,7 +344,10 @@ sc_status run_eval(const sc_context_s* ctx, const sc_batch* b, const float* w, f
   p.blocked = std::getenv("SC_BLOCKED") ? std::atoi(std::getenv("SC_BLOCKED")) : (b->app ? 1 : 0);
   const int grid = static_cast<int>(std::min<int64_t>(p.nunits, di.sms));
   if (cudaError_t e = sc::launch_eval(p, epl, launch_pat, grid, smem, st)) return cuda_fail(e, "eval kernel launch");
-  g_last_kernel = epl ? (launch_pat == 2 ? "tma_ring_dense_nv" : launch_pat ? "tma_ring_lists_epl" : "tma_ring_epl") +
+  g_last_kernel = epl ? (launch_pat == 3   ? "tma_ring_appchoice_epl"
+                         : launch_pat == 2 ? "tma_ring_dense_nv"
+                         : launch_pat      ? "tma_ring_lists_epl"
+                                           : "tma_ring_epl") +
                             std::to_string(epl)
                       : "tma_ring_list";
   g_launches.fetch_add(1, std::memory_order_relaxed);

@@ -127,6 +127,7 @@ struct RowBatch {
   float zp, zm;      // max logit over 𝒲_i (P⁺ side) and over 𝕎∖𝒲_i (P⁻ side)
   uint32_t kp, km;   // their keys (label << 8 | cat), kNone if the set is empty
   uint32_t G, app;
+  uint32_t lo = 0;   // application-choice order: the lists holding an output label (z > tau)
   int64_t row;
   int n;             // rows held (warp-uniform)
 };
@@ -395,11 +396,114 @@ __device__ __forceinline__ void finish_lists_core(const EvalParams& p, RowBatch&
 }
 
 __device__ __forceinline__ void deposit(RowBatch& b, int lane, float zp, uint32_t kp, float zm, uint32_t km,
-                                        uint32_t G, uint32_t a, int64_t row) {
+                                        uint32_t G, uint32_t a, int64_t row, uint32_t lo = 0) {
   if (lane == b.n) {
-    b.zp = zp; b.kp = kp; b.zm = zm; b.km = km; b.G = G; b.app = a; b.row = row;
+    b.zp = zp; b.kp = kp; b.zm = zm; b.km = km; b.G = G; b.app = a; b.row = row; b.lo = lo;
   }
   ++b.n;
+}
+
+// The application-choice order (Eq. app_choice, reading A21) from two
+// arg maxima per row instead of one per list: with k = the lowest list of G_i, (zp, kp) is
+// the arg max over list k (P_k) and (zm, km) the arg max over lists j < k (P_{k⁻}); for
+// G_i = ∅ (zm, km) is over all of 𝕎 (P).  The decision is the first list holding an output
+// label (b.lo: lists with some z > tau).  Same formulas, in the same order, as the per-list
+// epilogue (finish_lists_core), so both give identical values.
+__device__ __forceinline__ void finish_app_choice(const EvalParams& p, RowBatch& b, const float* wtab_smem, int lane) {
+  const bool active = lane < b.n;
+  const unsigned act = __ballot_sync(kFull, active);
+  const float tau = p.ctx.tau, theta = p.ctx.theta, k = p.ctx.k;
+  uint32_t dec = 0, correct = 1;
+  float L = 0.f, g0 = 0.f, g1 = 0.f;
+  int32_t i0 = -1, i1 = -1;
+  if (active) {
+    const uint32_t D = __ldg(p.ctx.nlists + b.app);
+    const uint32_t G = b.G;
+    const bool y = G != 0;
+    dec = b.lo ? static_cast<uint32_t>(__ffs(b.lo) - 1) : D;
+    const uint32_t kk = y ? static_cast<uint32_t>(__ffs(G) - 1) : D;
+    correct = dec == kk;
+    if (p.decision) p.decision[b.row] = static_cast<uint8_t>(dec);
+    if (p.want_loss) {
+      const float wi = p.w ? (wtab_smem ? wtab_smem[G] : __ldg(p.w + b.app * 256u + G)) : 1.f;
+      if (y && b.kp != kNone) {
+        const bool c_over = b.km != kNone && b.zm > tau;
+        const float am = c_over ? sigmoid_f(b.zm) : theta;  // max(θ, P_{k⁻})
+        const float x = am - sigmoid_f(b.zp);
+        const float ds = k * dsigmoid_f(k * x);
+        L = wi * sigmoid_f(k * x);
+        i0 = static_cast<int32_t>(b.kp >> 8);
+        g0 = -wi * ds * dsigmoid_f(b.zp) * p.grad_scale;
+        if (c_over) {
+          i1 = static_cast<int32_t>(b.km >> 8);
+          g1 = wi * ds * dsigmoid_f(b.zm) * p.grad_scale;
+        }
+      } else if (!y && b.km != kNone) {
+        const float x = sigmoid_f(b.zm) - theta;  // P − θ
+        L = wi * sigmoid_f(k * x);
+        i1 = static_cast<int32_t>(b.km >> 8);
+        g1 = wi * k * dsigmoid_f(k * x) * dsigmoid_f(b.zm) * p.grad_scale;
+      }
+      if (p.loss_row) p.loss_row[b.row] = L;
+      if (p.grad_idx) {
+        p.grad_idx[2 * b.row] = out_label(p.ctx, i0);
+        p.grad_idx[2 * b.row + 1] = out_label(p.ctx, i1);
+      }
+      if (p.grad_val) {
+        p.grad_val[2 * b.row] = g0;
+        p.grad_val[2 * b.row + 1] = g1;
+      }
+    }
+  }
+  if (p.hist_pred && active) {
+    const uint32_t key = b.app * 256u + dec;
+    const unsigned peers = __match_any_sync(act, key);
+    if (lane == __ffs(peers) - 1) atomicAdd(p.hist_pred + key, static_cast<unsigned long long>(__popc(peers)));
+  }
+  if (p.has_gt) {
+    if (p.hist_gt && active) {
+      const uint32_t key = b.app * 256u + b.G;
+      const unsigned peers = __match_any_sync(act, key);
+      if (lane == __ffs(peers) - 1) atomicAdd(p.hist_gt + key, static_cast<unsigned long long>(__popc(peers)));
+    }
+    const unsigned inc = __ballot_sync(kFull, active && !correct);
+    if (p.n_incorrect && (inc >> lane & 1u)) {
+      const unsigned peers = __match_any_sync(inc, b.app);
+      if (lane == __ffs(peers) - 1) atomicAdd(p.n_incorrect + b.app, static_cast<unsigned long long>(__popc(peers)));
+    }
+    if (p.loss_sum && p.want_loss) {
+      double sl = active ? static_cast<double>(L) : 0.0;
+      const uint32_t app0 = __shfl_sync(kFull, b.app, 0);
+      if (__all_sync(kFull, !active || b.app == app0)) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) sl += __shfl_xor_sync(kFull, sl, off);
+        if (lane == 0) atomicAdd(p.loss_sum + app0, sl);
+      } else if (active) {
+        atomicAdd(p.loss_sum + b.app, sl);
+      }
+    }
+  }
+  if (p.grad_dense) {
+    for (int t = 0; t < b.n; ++t) {
+      const int64_t row = __shfl_sync(kFull, b.row, t);
+      const int32_t c0 = __shfl_sync(kFull, i0, t), c1 = __shfl_sync(kFull, i1, t);
+      const float v0 = __shfl_sync(kFull, g0, t), v1 = __shfl_sync(kFull, g1, t);
+      float* out = p.grad_dense + row * p.ld;
+      const int64_t nv = p.ld >> 2;
+      for (int64_t v = lane; v < nv; v += 32) {
+        float e[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int64_t c = 4 * v + q;
+          if (c == c0) e[q] = v0;
+          if (c == c1) e[q] = v1;
+        }
+        st_cs_f4(out + 4 * v, make_float4(e[0], e[1], e[2], e[3]));
+      }
+    }
+  }
+  __syncwarp();
+  b.n = 0;
 }
 
 // Shared-memory loads by 32-bit shared address (no generic-to-shared conversion per load).

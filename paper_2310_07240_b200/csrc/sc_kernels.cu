@@ -250,6 +250,7 @@ struct SlotEnt {
   uint32_t key[EPL];  // c << 8 | cat[c], kNone for padding
   uint32_t off[EPL];  // byte offset of the label in a row (0 for padding)
   int ns;             // slots of the application (warp-uniform)
+  uint32_t lists;     // list of slot s in bits 4s..4s+3 (DevContext::lslot)
   int32_t app;
 };
 
@@ -258,6 +259,7 @@ __device__ __forceinline__ void slot_ent_load(SlotEnt<EPL>& se, const DevContext
                                               uint32_t elt) {
   const int32_t e0 = __ldg(c.lent_off + app), e1 = __ldg(c.lent_off + app + 1);
   se.ns = (e1 - e0) >> 5;
+  se.lists = __ldg(c.lslot + app);
   se.app = app;
 #pragma unroll
   for (int t = 0; t < EPL; ++t) {
@@ -581,22 +583,36 @@ __global__ void __launch_bounds__(kThreads, 1) eval_kernel(const EvalParams p) {
     // CTA-local unit i lives in stage i % S and is consumed by group i % NG only, so a
     // stage is released as soon as its WG warps are done (no CTA-wide stage barrier).
     constexpr uint32_t kElt = BF16 ? 2u : 4u;
-    constexpr bool kSplit = PAT != 1;  // split-maxima epilogue (finish_batch): PAT 0 and 2
-    LaneEnt<PAT == 0 ? EPL : 1> le;    // split maxima (PAT 0)
+    constexpr bool kSplit = PAT != 1;  // two arg maxima per row: PAT 0, 2 (finish_batch), 3 (finish_app_choice)
+    LaneEnt<(PAT == 0 || PAT == 3) ? EPL : 1> le;  // lane-resident entries (PAT 0, 3)
     SlotEnt<PAT == 1 ? EPL : 1> se;    // list-major slots (PAT 1)
     DmEnt<PAT == 2 ? EPL : 1, BF16> de;  // dense-mapped rows (PAT 2)
     float sz[PAT == 1 ? EPL : 1];      // this lane's batch row: arg max of every slot (PAT 1)
     uint32_t sk[PAT == 1 ? EPL : 1];
-    if constexpr (PAT == 0)
+    if constexpr (PAT == 0 || PAT == 3)
       lane_ent_load(le, p.ctx.ent + __ldg(p.ctx.ent_off), __ldg(p.ctx.ent_off + 1) - __ldg(p.ctx.ent_off), 0, lane,
-                    kElt);
+                    kElt, PAT == 3 ? kAppChoice : kApiOutput);
     else if constexpr (PAT == 1)
       slot_ent_load(se, p.ctx, 0, lane, kElt);
     else
       dm_ent_load(de, p.ctx.ent, __ldg(p.ctx.ent_off + 1), lane);
     // single app: table of plus-masks per G value (one LDS per row instead of 8 selects)
     uint32_t* pmtab = p.pmtab_off >= 0 ? reinterpret_cast<uint32_t*>(smem + p.pmtab_off) : nullptr;
-    if (kSplit && pmtab) {
+    if (PAT == 3 && pmtab) {
+      // application-choice order, single app: per k (the lowest list of G; k = D' for G = ∅)
+      // the lane's entries of list k (P_k side) and of lists j < k (P_{k⁻}; all of 𝕎 for k = D')
+      for (int kq = cw; kq <= p.pmtab_bits; kq += kConsumerWarps) {
+        uint32_t vp = 0, vm = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (j == kq) vp = le.catm[j];
+          if (j < kq) vm |= le.catm[j];
+        }
+        pmtab[(2 * kq) * 32 + lane] = vp & le.valid;
+        pmtab[(2 * kq + 1) * 32 + lane] = vm & le.valid;
+      }
+      asm volatile("bar.sync 1, %0;" ::"r"(kConsumerWarps * 32) : "memory");
+    } else if (kSplit && pmtab) {
       for (int g = cw; g < (1 << p.pmtab_bits); g += kConsumerWarps) {
         uint32_t pmv;
         if constexpr (PAT == 2) {
@@ -662,6 +678,52 @@ __global__ void __launch_bounds__(kThreads, 1) eval_kernel(const EvalParams p) {
             }
             deposit(b, lane, zp, kp, zm, km, G, a, row);
           }
+        } else if constexpr (PAT == 3) {
+          // application-choice order by two arg maxima (finish_app_choice) + the lists holding
+          // an output label (one warp OR)
+          if (static_cast<int32_t>(a) != le.app) {
+            const int32_t e0 = __ldg(p.ctx.ent_off + a);
+            lane_ent_load(le, p.ctx.ent + e0, __ldg(p.ctx.ent_off + a + 1) - e0, static_cast<int32_t>(a), lane, kElt,
+                          kAppChoice);
+          }
+#pragma unroll
+          for (int t = 0; t < EPL; ++t) zs[t] = lds_z<BF16>(srow + le.off(t, kElt));
+          const uint32_t D = pmtab ? static_cast<uint32_t>(p.pmtab_bits) : __ldg(p.ctx.nlists + a);
+          const uint32_t kq = G ? static_cast<uint32_t>(__ffs(G) - 1) : D;
+          uint32_t vp, vm;
+          if (pmtab) {
+            vp = lds_u32(sbase + p.pmtab_off + ((2 * kq) * 32 + lane) * 4);
+            vm = lds_u32(sbase + p.pmtab_off + ((2 * kq + 1) * 32 + lane) * 4);
+          } else {
+            vp = 0;
+            vm = 0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              if (q == static_cast<int>(kq)) vp = le.catm[q];
+              if (q < static_cast<int>(kq)) vm |= le.catm[q];
+            }
+            vp &= le.valid;
+            vm &= le.valid;
+          }
+          float zp = -CUDART_INF_F, zm = -CUDART_INF_F;
+          uint32_t kp = kNone, km = kNone;
+          scan_all<EPL, false>(le, 0u, vp, vm, zs, zp, kp, zm, km);
+          // output lists: entries above tau, folded by list
+          uint32_t ob = 0;
+#pragma unroll
+          for (int t = 0; t < EPL; ++t) ob |= (zs[t] > p.ctx.tau ? 1u : 0u) << t;
+          ob &= le.valid;
+          uint32_t lo = 0;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) lo |= (ob & le.catm[q]) ? (1u << q) : 0u;
+          lo = __reduce_or_sync(kFull, lo);
+          warp_argmax(zp, kp);
+          warp_argmax(zm, km);
+          if (b.n == lim) {
+            finish_app_choice(p, b, wtab, lane);
+            lim = 32;
+          }
+          deposit(b, lane, zp, kp, zm, km, G, a, row, lo);
         } else if constexpr (PAT == 0) {
           if (static_cast<int32_t>(a) != le.app) {
             const int32_t e0 = __ldg(p.ctx.ent_off + a);
@@ -695,7 +757,8 @@ __global__ void __launch_bounds__(kThreads, 1) eval_kernel(const EvalParams p) {
       // the batch epilogue runs after the stage is released, and the warps' batch boundaries
       // are staggered (lim) so they do not all hold the pipeline in the same stage
       if (b.n == lim) {
-        if constexpr (kSplit) finish_batch(p, b, wtab, lane);
+        if constexpr (PAT == 3) finish_app_choice(p, b, wtab, lane);
+        else if constexpr (kSplit) finish_batch(p, b, wtab, lane);
         else finish_slots<EPL>(p, b, sz, sk, wtab, lane);
         lim = 32;
       }
@@ -703,7 +766,8 @@ __global__ void __launch_bounds__(kThreads, 1) eval_kernel(const EvalParams p) {
       if (st_idx >= p.stages) { st_idx -= p.stages; ph ^= 1u; }
     }
     if (b.n > 0) {
-      if constexpr (kSplit) finish_batch(p, b, wtab, lane);
+      if constexpr (PAT == 3) finish_app_choice(p, b, wtab, lane);
+      else if constexpr (kSplit) finish_batch(p, b, wtab, lane);
       else finish_slots<EPL>(p, b, sz, sk, wtab, lane);
     }
     return;
@@ -1157,6 +1221,7 @@ static cudaError_t set_limit_t(size_t smem) {
 #define SC_EVAL_EPLS(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(12) X(16) X(24) X(32)
 #define SC_EVAL_EPLS_PAT(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8)  // per-list patterns: slots (PAT = 1)
 #define SC_EVAL_NV_DM(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8)     // dense-mapped rows: 16-B groups (PAT = 2)
+#define SC_EVAL_EPLS_AC(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8)   // application-choice, two maxima (PAT = 3)
 
 cudaError_t set_eval_smem_limit(size_t smem) {
   cudaError_t e = set_limit_t<0>(smem);
@@ -1168,6 +1233,9 @@ cudaError_t set_eval_smem_limit(size_t smem) {
 #undef SC_SET
 #define SC_SET(N) if (!e) e = set_limit_t<N, 2>(smem);
   SC_EVAL_NV_DM(SC_SET)
+#undef SC_SET
+#define SC_SET(N) if (!e) e = set_limit_t<N, 3>(smem);
+  SC_EVAL_EPLS_AC(SC_SET)
 #undef SC_SET
   return e;
 }
@@ -1186,6 +1254,15 @@ int eval_epl_for(int max_ent, int pat) {
 
 template <bool BF16>
 static void launch_eval_dt(const EvalParams& p, int epl, int pat, int grid, size_t smem, cudaStream_t st) {
+  if (pat == 3) {
+    switch (epl) {
+#define SC_CASE(N) case N: eval_kernel<N, BF16, 3><<<grid, kThreads, smem, st>>>(p); break;
+      SC_EVAL_EPLS_AC(SC_CASE)
+#undef SC_CASE
+      default: break;
+    }
+    return;
+  }
   if (pat == 2) {
     switch (epl) {
 #define SC_CASE(N) case N: eval_kernel<N, BF16, 2><<<grid, kThreads, smem, st>>>(p); break;
