@@ -269,19 +269,37 @@ __device__ __forceinline__ void slot_ent_load(SlotEnt<EPL>& se, const DevContext
   }
 }
 
-// a3 for one row: the arg max of every slot; lane `slot` keeps them (sz, sk).
+// a3 for one row: the arg max of every list; lane `slot` keeps them (sz, sk), at the
+// position of the list's last slot (the list's other slots hold kNone).  A list's slots are
+// consecutive and a lane's entries in them ascend, so each lane first folds its slots of one
+// list with a strict '>' (the smaller label keeps ties), then one warp arg max per list —
+// not one per 32-label slot.
 template <int EPL>
 __device__ __forceinline__ void scan_slots(const SlotEnt<EPL>& se, const float (&zs)[EPL], float (&sz)[EPL],
                                            uint32_t (&sk)[EPL], int slot, int lane) {
+  float fz = -CUDART_INF_F;
+  uint32_t fk = kNone;
 #pragma unroll
   for (int t = 0; t < EPL; ++t) {
     if (t < se.ns) {  // warp-uniform
-      float z = zs[t];
-      uint32_t k = se.key[t];
-      warp_argmax(z, k);
-      if (lane == slot) {
-        sz[t] = z;
-        sk[t] = k;
+      const uint32_t k = se.key[t];
+      if (k != kNone && (fk == kNone || zs[t] > fz)) {
+        fz = zs[t];
+        fk = k;
+      }
+      const bool last = t + 1 == se.ns || ((se.lists >> (4 * t)) & 15u) != ((se.lists >> (4 * t + 4)) & 15u);
+      if (last) {  // warp-uniform: list of slot t ends here
+        float z = fz;
+        uint32_t kk = fk;
+        warp_argmax(z, kk);
+        if (lane == slot) {
+          sz[t] = z;
+          sk[t] = kk;
+        }
+        fz = -CUDART_INF_F;
+        fk = kNone;
+      } else if (lane == slot) {
+        sk[t] = kNone;
       }
     }
   }
