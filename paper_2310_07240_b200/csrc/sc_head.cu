@@ -78,7 +78,8 @@ struct HeadParams {
   int32_t list_col0[kMaxLists];  // first column of list j (multiple of 16)
   int32_t list_nch[kMaxLists];   // 16-column groups of list j
   int32_t probe;            // experiment (SC_HEAD_PROBE): bit 0 skips the epilogue's reduction, bit 1 the MMAs,
-                            // bit 2 the x loads, bit 3 the W loads (lone CTAs; results are garbage)
+                            // bit 2 the x loads, bit 3 the W loads (lone CTAs; results are garbage),
+                            // bit 4 the drain's reduction (loads kept), bit 5 the drain's TMEM loads
   int32_t n_pass;           // column passes per row tile: 1 = every column in TMEM at once (n_cols <= 512);
                             // > 1 = pass_w columns per pass, x re-streamed per pass (from L2)
   int32_t pass_w;           // columns per pass (n_pass > 1; = chunk)
@@ -217,6 +218,22 @@ __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint6
         "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
         : "memory");
+}
+
+// mbarrier wait for a whole converged warp whose loop exit is provably warp-uniform (a vote):
+// after it the compiler keeps warp-uniform values (the MMA descriptors) in uniform registers.
+// (An asm spin loop with a per-thread branch makes everything after it look divergent.)
+__device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_addr(bar);
+  for (;;) {
+    uint32_t ok;
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (__all_sync(0xFFFFFFFFu, ok)) break;
+  }
 }
 
 // One k-block (4 K = 16 steps) of MMAs: NCH column chunks x NTL row tiles, each its own
@@ -506,20 +523,21 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
       const int acc_stride = p.n_pass > 1 ? p.pass_w : p.n_cols;
       for (int64_t st = 0; st < n_steps; ++st) {
         for (int ps = 0; ps < p.n_pass; ++ps) {
-        unsigned long long* tr = (ps == 0 && lane == 0) ? trace_slot(p, st) : nullptr;
-        if (tr) tr[0] = tnow();
-        mbar_wait(tempty + b, tph[b] ^ 1u);  // the epilogue(s) drained this accumulator
-        if (tr) tr[1] = tnow();
+        // probe stamps: every lane takes the same path (the waits below vote), lane 0 writes
+        unsigned long long* tr = ps == 0 ? trace_slot(p, st) : nullptr;
+        if (tr && lane == 0) tr[0] = tnow();
+        mbar_wait_warp(tempty + b, tph[b] ^ 1u);  // the epilogue(s) drained this accumulator
+        if (tr && lane == 0) tr[1] = tnow();
         tph[b] ^= 1u;
         tc_fence_after();
         const uint32_t acc = tmem_base + static_cast<uint32_t>(b * acc_stride);
         for (int xb = 0; xb < p.n_xb; ++xb) {
           if (tr) {
             const unsigned long long t0 = tnow();
-            mbar_wait(xfull + xs, xph);
-            tr[2] += tnow() - t0;
+            mbar_wait_warp(xfull + xs, xph);
+            if (lane == 0) tr[2] += tnow() - t0;
           } else {
-            mbar_wait(xfull + xs, xph);
+            mbar_wait_warp(xfull + xs, xph);
           }
           tc_fence_after();
           const uint64_t ax = a_desc0 + static_cast<uint64_t>(xs) * x_step;
@@ -527,10 +545,10 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
           for (int kx = 0; kx < nk; ++kx) {
             if (tr) {
               const unsigned long long t0 = tnow();
-              mbar_wait(wfull + ws, wph);
-              tr[3] += tnow() - t0;
+              mbar_wait_warp(wfull + ws, wph);
+              if (lane == 0) tr[3] += tnow() - t0;
             } else {
-              mbar_wait(wfull + ws, wph);
+              mbar_wait_warp(wfull + ws, wph);
             }
             tc_fence_after();
             const uint64_t ad = ax + static_cast<uint64_t>(kx) * (a_bytes >> 4);
@@ -565,7 +583,7 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
           }
         }
         umma_commit<PAIR>(tfull + b);  // accumulator complete (in both CTAs)
-        if (tr) tr[4] = tnow();
+        if (tr && lane == 0) tr[4] = tnow();
         if (p.acc_bufs == 2) b ^= 1;
         }
       }
@@ -635,14 +653,19 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
         // rounds of two groups (one 32-column TMEM load); the next round's load is in flight
         // while this one is reduced (tcgen05.wait::ld waits for every outstanding load)
         uint32_t v[32], vn[32];
-        if (k < khi) {
+        const bool no_ld = (p.probe & 32) != 0, no_red = (p.probe & 16) != 0;  // drain probes
+        if (no_ld) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = vn[i] = 0u;
+        }
+        if (k < khi && !no_ld) {
           if (k + 1 < khi) tmem_ld32(acc + 16 * k, v);
           else tmem_ld16(acc + 16 * k, *reinterpret_cast<uint32_t(*)[16]>(v));
           tmem_wait_ld32(v);
         }
         while (k < khi) {
           const int kn = k + 2;
-          if (kn < khi) {
+          if (kn < khi && !no_ld) {
             if (kn + 1 < khi) tmem_ld32(acc + 16 * kn, vn);
             else tmem_ld16(acc + 16 * kn, *reinterpret_cast<uint32_t(*)[16]>(vn));
           }
@@ -663,6 +686,10 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
                 jend = j < D ? (p.list_col0[j] >> 4) + p.list_nch[j] : 0x7FFFFFFF;
               }
               const int col = 16 * kg;
+              if (no_red) {  // probe: keep only a dependency on the loaded values
+                run_z = fmaxf(run_z, __uint_as_float(v[16 * h]));
+                continue;
+              }
               float z[16];
               // bias: shared-space 16-B loads (a generic pointer compiled to LD.E.128)
               const uint32_t b_addr = s_bias_addr + 4u * static_cast<uint32_t>(col);
@@ -687,7 +714,7 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
             }
           }
           k = min(kn, khi);
-          if (k < khi) {
+          if (k < khi && !no_ld) {
             tmem_wait_ld32(vn);
 #pragma unroll
             for (int i = 0; i < 32; ++i) v[i] = vn[i];
