@@ -32,6 +32,15 @@ for c in range(CTAS):
         epi7_drain=(r[u, 12] - r[u, 11]).mean(),
         acc_ready_to_drain_start=(r[u, 6] - r[u, 4]).mean(),
         xprod_wait=r[u, 9].mean(), wprod_wait=r[u, 10].mean()))
+# CTAs without an MMA issuer (a pair's second CTA): their producers' and epilogue's numbers
+for c in range(CTAS):
+    r = rec[c]
+    if (r[:, 1] > 0).any() or not (r[:, 6] > 0).any():
+        continue
+    u = np.arange(2, UNITS - 1)
+    print(f"CTA {c} (pair peer): epi_wait {(r[u, 6] - r[u, 5]).mean() / 1e3:.2f}  epi_drain "
+          f"{(r[u, 7] - r[u, 6]).mean() / 1e3:.2f}  epi_finish {(r[u, 8] - r[u, 7]).mean() / 1e3:.2f}  "
+          f"xprod_wait {r[u, 9].mean() / 1e3:.2f}  wprod_wait {r[u, 10].mean() / 1e3:.2f} (us)")
 keys = list(rows[0].keys())
 print("CTA  " + "  ".join(f"{k:>12s}" for k in keys))
 for c, d in enumerate(rows):
