@@ -174,10 +174,6 @@ __device__ __forceinline__ uint32_t mapa(uint32_t saddr, uint32_t rank) {
   return r;
 }
 
-__device__ __forceinline__ void mbar_arrive_expect_tx_cl(uint32_t bar_cl, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(bar_cl), "r"(bytes)
-               : "memory");
-}
 
 __device__ __forceinline__ void mbar_arrive_cl(uint32_t bar_cl) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cl) : "memory");
@@ -306,14 +302,6 @@ __device__ __forceinline__ void tmem_wait_ld32(uint32_t (&v)[32]) {
                : "memory");
 }
 
-// Wait for the outstanding tcgen05.ld; `v` passes through so no use of it is hoisted above.
-__device__ __forceinline__ void tmem_wait_ld(uint32_t (&v)[16]) {
-  asm volatile("tcgen05.wait::ld.sync.aligned;"
-               : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7]),
-                 "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]), "+r"(v[12]), "+r"(v[13]), "+r"(v[14]), "+r"(v[15])
-               :
-               : "memory");
-}
 
 // Arg max of 16 columns (z, index); strict > keeps the lower index on ties (reading A4:
 // the lower column of a list is the smaller label id).
@@ -373,11 +361,11 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
   }
   if (tid == 0) {
     for (int s = 0; s < p.x_stages; ++s) {
-      mbar_init(xfull + s, PAIR ? 2 : 1);
+      mbar_init(xfull + s, 1);  // PAIR: the leader's one arrival expects both CTAs' bytes
       mbar_init(xempty + s, 1);
     }
     for (int s = 0; s < p.w_stages; ++s) {
-      mbar_init(wfull + s, PAIR ? 2 : 1);
+      mbar_init(wfull + s, 1);
       mbar_init(wempty + s, 1);
     }
     for (int b = 0; b < 2; ++b) {
@@ -445,8 +433,11 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
             }
             continue;
           }
-          if (rank == 0) mbar_arrive_expect_tx(xfull + s, tx);
-          else mbar_arrive_expect_tx_cl(fb, tx);
+          // CTA pairs: only the leader arrives, expecting both CTAs' bytes (the peer's copies
+          // complete their bytes on the leader's barrier).  A remote arrive.expect_tx per stage
+          // from the peer (release at cluster scope) serialised its producer: measured, the
+          // leader's MMA waited 18 µs of every 32 µs unit on the peer's stages.
+          if (rank == 0) mbar_arrive_expect_tx(xfull + s, PAIR ? 2 * tx : tx);
           for (int t = 0; t < p.tiles; ++t) {  // tile t: kbs k-blocks at t * kbs * 16 KB
             uint8_t* dst = stg + static_cast<size_t>(t) * p.kbs * (kBM * kBK * 2);
             if (p.x3d) tma_3d<PAIR>(dst, &map_x, 0, row0 + t * kTileRows, xb * p.kbs, fb, pol_x);
@@ -489,8 +480,7 @@ __global__ void __launch_bounds__(kHeadThreads, 1)
             }
             continue;
           }
-          if (rank == 0) mbar_arrive_expect_tx(wfull + s, tx);
-          else mbar_arrive_expect_tx_cl(fb, tx);
+          if (rank == 0) mbar_arrive_expect_tx(wfull + s, PAIR ? 2 * tx : tx);
           for (int c = 0; c < p.n_chunks; ++c)
             tma_2d<PAIR>(stg + c * rows_c * (kBK * 2), &map_w, 0,
                          kb * p.n_cols + col0 + c * p.chunk + static_cast<int>(rank) * rows_c, fb, pol_w);
