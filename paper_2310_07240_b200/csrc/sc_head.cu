@@ -872,7 +872,7 @@ struct HeadLaunch {
   int units = 0;  // co-resident CTAs (single) or pairs
 };
 
-HeadLaunch pick_launch(size_t smem, int sms, int64_t n_tiles) {
+HeadLaunch pick_launch(size_t smem, int sms, int64_t n_tiles, bool prefer_pair) {
   int forced = 0;
   if (const char* e = std::getenv("SC_HEAD_CLUSTER")) forced = std::atoi(e);
   static std::mutex mu;
@@ -905,10 +905,12 @@ HeadLaunch pick_launch(size_t smem, int sms, int64_t n_tiles) {
     }
   }
   HeadLaunch hl;
-  // Pairs are correct (tests) but measured slower than lone CTAs on cfg2 (1.45 vs 1.01 ms at
-  // d = 2048): opt-in until the cross-CTA handshake is understood.
+  // CTA pairs with two row tiles per CTA are the default where the pairs cover >= 90 % of the
+  // SMs (B200, cfg2: d = 2048 0.800 vs 0.839 ms, d = 1024 0.434 vs 0.444 ms against lone CTAs);
+  // pairs with one tile (double-buffered accumulators, but each MMA feeds 128 rows per CTA)
+  // are slower (0.91 ms) and opt-in.  SC_HEAD_CLUSTER=1 / 2 forces lone CTAs / pairs.
   const bool pair_ok = pairs >= 1 && (forced == 2 || 2 * pairs * 10 >= sms * 9);
-  if (forced == 2 && pair_ok && n_tiles >= 2) {
+  if ((forced == 2 || (forced == 0 && prefer_pair)) && pair_ok && n_tiles >= 2) {
     hl.pair = true;
     hl.units = pairs;
   } else {
@@ -1150,8 +1152,10 @@ sc_status sc_head_loss_fwd_bwd(sc_context ctx, sc_head head, const sc_head_batch
     p.w_stage_bytes = (want_pair ? pass_cols / 2 : pass_cols) * sc::kBK * 2;
     // two row tiles per unit share every W stage (lone CTAs by default; CTA pairs with
     // SC_HEAD_PAIR_T2=1: 512 rows per pass over W)
+    // two row tiles per unit share every W stage (lone CTAs and, by default, CTA pairs: 512 rows
+    // per pass over W; SC_HEAD_PAIR_T2=0 gives pairs one tile and double-buffered accumulators)
     const char* pt2 = std::getenv("SC_HEAD_PAIR_T2");
-    p.tiles = (t2_ok && (!want_pair || (pt2 && std::atoi(pt2) == 1))) ? 2 : 1;
+    p.tiles = (t2_ok && (!want_pair || !(pt2 && std::atoi(pt2) == 0))) ? 2 : 1;
     // x: 3-D boxes of kbs k-blocks (rows read kbs*128 B at a time) when d % 64 == 0; as many
     // x bytes in flight as fit next to >= 3 W stages (>= 2 for wide heads)
     x3d = head->d % sc::kBK == 0 && !(std::getenv("SC_HEAD_X2D"));
@@ -1206,7 +1210,7 @@ sc_status sc_head_loss_fwd_bwd(sc_context ctx, sc_head head, const sc_head_batch
                                         static_cast<int>(kHeadSmemMax));
     });
     if (attr_err) return sc::set_error(SC_ERR_CUDA, "sc_head_loss_fwd_bwd: %s", cudaGetErrorString(attr_err));
-    hl = pick_launch(smem, sms, n_tiles);
+    hl = pick_launch(smem, sms, n_tiles, want_pair && p.tiles == 2);
     if (want_pair && !(hl.pair && head->pair_ok && (p.chunk / 2) % 8 == 0)) continue;  // re-plan for a lone CTA
     pair = want_pair;
     break;

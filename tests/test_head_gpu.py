@@ -235,13 +235,15 @@ def test_head_errors():
 @pytest.mark.parametrize("name,rows", [("cfg2", 148 * 128 * 2 + 1000), ("w300", 5000), ("cfg1", 300), ("w512", 700),
                                        ("cfg2", 148 * 512 + 777)])
 def test_head_single_and_pair(q, name, rows, monkeypatch):
-    """Lone CTAs (cta_group::1, M = 128) and CTA pairs (cta_group::2, M = 256, W halves in the
-    two CTAs), SC_HEAD_CLUSTER; "2t2": pairs with two row tiles per unit (512 rows per pass over
-    W, SC_HEAD_PAIR_T2); unit counts that leave some CTAs without rows in the last step, odd tile
+    """Lone CTAs (cta_group::1, M = 128, forced with SC_HEAD_CLUSTER=1) and CTA pairs
+    (cta_group::2, M = 256, W halves in the two CTAs) with one row tile (SC_HEAD_PAIR_T2=0) or
+    two ("2t2", the default where pairs fit: 512 rows per pass over W); unit counts that leave some CTAs without rows in the last step, odd tile
     counts (a pair's second CTA past the end)."""
     if q == "2t2":
         monkeypatch.setenv("SC_HEAD_PAIR_T2", "1")
         q = 2
+    elif q == 2:
+        monkeypatch.setenv("SC_HEAD_PAIR_T2", "0")  # pairs with one tile (double-buffered accumulators)
     torch, sc, synth, _ = _mods()
     spec = SPECS[name](synth)
     d = 320
