@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--compact", action="store_true",
                     help="column-compacted rows (sc_context_load_compact, NEXT f3): each row holds only the "
                          "mapped labels' logits, as a producer restricted to those columns emits them")
+    ap.add_argument("--grad", default="sparse", choices=["sparse", "dense"],
+                    help="gradient output: sparse slots (default) or the dense [rows, ld] f32 gradient "
+                         "(SURVEY.md 8(d): reported separately, adds ld*4 B/row of writes)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -333,7 +336,7 @@ def run_ours(args):
         data = wl.device_batch(rank * B, B, device=dev)  # this rank's rows of the global dataset
     logits, gt_off, gt_lab = data["logits"], data["gt_off"], data["gt_lab"]
     app = data.get("app")
-    ev = Evaluator(ctx, B, device=dev, group=group)
+    ev = Evaluator(ctx, B, device=dev, group=group, dense_ld=logits.stride(0) if args.grad == "dense" else 0)
     global_rows = B * world
 
     def barrier():
@@ -412,6 +415,8 @@ def run_ours(args):
     ld = logits.stride(0)
     sect = touched_sector_bytes(spec, ld, elt, rows=B, columns=columns)
     per_row = sect + 1 + 1 + 8 * ctx.grad_slots + (2 if app is not None else 0)  # sectors + G_i + decision + sparse grad (+ app)
+    if args.grad == "dense":
+        per_row += ld * 4  # the full f32 gradient row written
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     peak = peaks.get("hbm_gbs", 6650.0)
@@ -431,7 +436,8 @@ def run_ours(args):
         "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
         "config": {"workload": workload_name(cfg, args.dtype), "C": spec.C, "rows_per_gpu": B, "global_batch": global_rows,
                    "parallelism": f"dp{world}", "l2": f"no flush: {B * ld * elt / 1e9:.2f} GB of logits per step per GPU > 126 MB L2",
-                   "grad": f"sparse ({ctx.grad_slots} slots/row)", "order": args.order,
+                   "grad": (f"sparse ({ctx.grad_slots} slots/row)" if args.grad == "sparse"
+                            else f"dense f32 [rows, {ld}] + sparse slots"), "order": args.order,
                    "layout": (f"column-compacted: {len(columns)} of {spec.C} label columns per row (sc_context_load_compact)"
                               if args.compact else "dense rows, column c = label c")},
         "roofline": roofline,
