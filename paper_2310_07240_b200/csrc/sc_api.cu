@@ -132,6 +132,7 @@ sc_status run_eval(const sc_context_s* ctx, const sc_batch* b, const float* w, f
   if (!di.eval_attr) return fail(SC_ERR_CUDA, "cannot raise the kernel's shared-memory limit");
 
   sc::EvalParams p{};
+  p.pend_off = -1;
   p.ctx = dev_ctx(ctx);
   p.logits = static_cast<const uint8_t*>(b->logits);
   p.rows = b->rows;
@@ -316,7 +317,10 @@ sc_status run_eval(const sc_context_s* ctx, const sc_batch* b, const float* w, f
   const int64_t max_stages = epl > 0 ? 32 : 8;
   // dense-mapped rows read whole 512-B groups: up to 511 B past a row's last column
   const int64_t dm_slack = launch_pat == 2 ? 512 : 0;
-  const int64_t other = ent_bytes + pmtab_bytes + (wtab ? 1024 : 0) + 2 * 8 * max_stages + 256 + dm_slack;
+  // dense gradient on the whole-row paths with two arg maxima per row: per-warp slabs where the
+  // batch's gradient rows wait to be written between stages (sc_device.cuh dense_pair_rows)
+  const int64_t pend_bytes = (grad_dense && epl > 0 && launch_pat != 1) ? static_cast<int64_t>(W) * sc::kPendSlab : 0;
+  const int64_t other = ent_bytes + pmtab_bytes + (wtab ? 1024 : 0) + pend_bytes + 2 * 8 * max_stages + 256 + dm_slack;
   int64_t S = (static_cast<int64_t>(kSmemMax) - other) / p.stage_bytes;
   if (S > max_stages) S = max_stages;
   S -= S % p.ng;  // stage s always belongs to group s % ng
@@ -331,6 +335,8 @@ sc_status run_eval(const sc_context_s* ctx, const sc_batch* b, const float* w, f
   }
   p.wtab_off = wtab ? static_cast<int32_t>(off) : -1;
   off += wtab ? 1024 : 0;
+  p.pend_off = pend_bytes ? static_cast<int32_t>(round_up(off, 16)) : -1;
+  if (pend_bytes) off = p.pend_off + pend_bytes;
   p.bar_off = static_cast<int32_t>(round_up(off, 8));
   off = p.bar_off + 2 * 8 * S + dm_slack;
   const size_t smem = static_cast<size_t>(off);

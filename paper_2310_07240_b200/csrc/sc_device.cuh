@@ -132,8 +132,81 @@ struct RowBatch {
   int n;             // rows held (warp-uniform)
 };
 
-// a3-a9 epilogue for the rows in the batch: decision, correctness, loss and
-// gradient; per-row outputs and warp-aggregated counter atomics.
+// Dense gradient rows of a batch not yet written (kDefer epilogues of the TMA-ring kernel) are
+// parked in a per-warp shared-memory slab (kPendSlab bytes at EvalParams::pend_off; nothing
+// held in registers) and written a few at a time between stages (dense_drain) instead of as
+// one 32-row burst per batch.  Slab: {int32 np (rows parked), int32 pt (next to write), pad},
+// the rows' indices (int64 [32]), then {c0, c1, v0, v1} per row (16 B [32]).
+__device__ __forceinline__ uint32_t pend_slab(const EvalParams& p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  return smem_addr(smem) + static_cast<uint32_t>(p.pend_off) + ((threadIdx.x >> 5) - 1u) * kPendSlab;
+}
+
+// One dense gradient row (a9, optional dense layout): zeros except columns c0 / c1, written
+// coalesced by the warp with streaming 16-B stores.
+__device__ __forceinline__ void dense_row_store(const EvalParams& p, int64_t row, int32_t c0, int32_t c1, float v0,
+                                                float v1, int lane) {
+  float* out = p.grad_dense + row * p.ld;
+  const int32_t nv = static_cast<int32_t>(p.ld >> 2);
+  for (int32_t v = lane; v < nv; v += 32) {
+    float e[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int32_t c = 4 * v + q;
+      if (c == c0) e[q] = v0;
+      if (c == c1) e[q] = v1;
+    }
+    st_cs_f4(out + 4 * v, make_float4(e[0], e[1], e[2], e[3]));
+  }
+}
+
+// Write up to `upto` parked dense gradient rows of this warp (call with the whole warp).
+__device__ __forceinline__ void dense_drain(const EvalParams& p, int lane, int upto) {
+  const uint32_t slab = pend_slab(p);
+  uint32_t np, pt;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(np), "=r"(pt) : "r"(slab));
+  if (pt >= np) return;  // warp-uniform
+  const uint32_t end = np < pt + static_cast<uint32_t>(upto) ? np : pt + static_cast<uint32_t>(upto);
+  for (uint32_t t = pt; t < end; ++t) {
+    int64_t row;
+    uint32_t c0, c1, v0, v1;
+    asm volatile("ld.shared.s64 %0, [%1];" : "=l"(row) : "r"(slab + 16u + 8u * t));
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(c0), "=r"(c1), "=r"(v0), "=r"(v1)
+                 : "r"(slab + 272u + 16u * t));
+    dense_row_store(p, row, static_cast<int32_t>(c0), static_cast<int32_t>(c1), __uint_as_float(v0),
+                    __uint_as_float(v1), lane);
+  }
+  __syncwarp();
+  if (lane == 0) asm volatile("st.shared.u32 [%0], %1;" ::"r"(slab + 4u), "r"(end) : "memory");
+  __syncwarp();
+}
+
+// The batch's dense gradient rows: written now, or (kDefer, when the kernel planned slabs)
+// parked after the previous batch's leftovers are flushed; the caller drains them.
+template <bool kDefer>
+__device__ __forceinline__ void dense_pair_rows(const EvalParams& p, RowBatch& b, int lane, int32_t i0, int32_t i1,
+                                                float g0, float g1) {
+  if (kDefer && p.pend_off >= 0) {
+    dense_drain(p, lane, 32);
+    const uint32_t slab = pend_slab(p), l = static_cast<uint32_t>(lane);
+    if (lane < b.n) {
+      asm volatile("st.shared.s64 [%0], %1;" ::"r"(slab + 16u + 8u * l), "l"(b.row) : "memory");
+      asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(slab + 272u + 16u * l), "r"(i0), "r"(i1),
+                   "r"(__float_as_uint(g0)), "r"(__float_as_uint(g1))
+                   : "memory");
+    }
+    if (lane == 0)
+      asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(slab), "r"(static_cast<uint32_t>(b.n)), "r"(0u) : "memory");
+    __syncwarp();
+  } else {
+    for (int t = 0; t < b.n; ++t)
+      dense_row_store(p, __shfl_sync(kFull, b.row, t), __shfl_sync(kFull, i0, t), __shfl_sync(kFull, i1, t),
+                      __shfl_sync(kFull, g0, t), __shfl_sync(kFull, g1, t), lane);
+  }
+}
+
+template <bool kDefer = false>
 __device__ __forceinline__ void finish_batch(const EvalParams& p, RowBatch& b, const float* wtab_smem, int lane) {
   const bool active = lane < b.n;
   const unsigned act = __ballot_sync(kFull, active);
@@ -220,25 +293,7 @@ __device__ __forceinline__ void finish_batch(const EvalParams& p, RowBatch& b, c
     }
   }
   // dense gradient: the warp writes each row coalesced (zeros + <= 2 entries)
-  if (p.grad_dense) {
-    for (int t = 0; t < b.n; ++t) {
-      const int64_t row = __shfl_sync(kFull, b.row, t);
-      const int32_t c0 = __shfl_sync(kFull, i0, t), c1 = __shfl_sync(kFull, i1, t);
-      const float v0 = __shfl_sync(kFull, g0, t), v1 = __shfl_sync(kFull, g1, t);
-      float* out = p.grad_dense + row * p.ld;
-      const int64_t nv = p.ld >> 2;
-      for (int64_t v = lane; v < nv; v += 32) {
-        float e[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int64_t c = 4 * v + q;
-          if (c == c0) e[q] = v0;
-          if (c == c1) e[q] = v1;
-        }
-        st_cs_f4(out + 4 * v, make_float4(e[0], e[1], e[2], e[3]));
-      }
-    }
-  }
+  if (p.grad_dense) dense_pair_rows<kDefer>(p, b, lane, i0, i1, g0, g1);
   b.n = 0;
 }
 
@@ -409,6 +464,7 @@ __device__ __forceinline__ void deposit(RowBatch& b, int lane, float zp, uint32_
 // G_i = ∅ (zm, km) is over all of 𝕎 (P).  The decision is the first list holding an output
 // label (b.lo: lists with some z > tau).  Same formulas, in the same order, as the per-list
 // epilogue (finish_lists_core), so both give identical values.
+template <bool kDefer = false>
 __device__ __forceinline__ void finish_app_choice(const EvalParams& p, RowBatch& b, const float* wtab_smem, int lane) {
   const bool active = lane < b.n;
   const unsigned act = __ballot_sync(kFull, active);
@@ -483,25 +539,7 @@ __device__ __forceinline__ void finish_app_choice(const EvalParams& p, RowBatch&
       }
     }
   }
-  if (p.grad_dense) {
-    for (int t = 0; t < b.n; ++t) {
-      const int64_t row = __shfl_sync(kFull, b.row, t);
-      const int32_t c0 = __shfl_sync(kFull, i0, t), c1 = __shfl_sync(kFull, i1, t);
-      const float v0 = __shfl_sync(kFull, g0, t), v1 = __shfl_sync(kFull, g1, t);
-      float* out = p.grad_dense + row * p.ld;
-      const int64_t nv = p.ld >> 2;
-      for (int64_t v = lane; v < nv; v += 32) {
-        float e[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int64_t c = 4 * v + q;
-          if (c == c0) e[q] = v0;
-          if (c == c1) e[q] = v1;
-        }
-        st_cs_f4(out + 4 * v, make_float4(e[0], e[1], e[2], e[3]));
-      }
-    }
-  }
+  if (p.grad_dense) dense_pair_rows<kDefer>(p, b, lane, i0, i1, g0, g1);
   __syncwarp();
   b.n = 0;
 }

@@ -8,6 +8,7 @@ namespace sc {
 
 constexpr int kConsumerWarps = 16;                 // W: consumer warps per CTA
 constexpr int kThreads = 32 * (1 + kConsumerWarps);  // + 1 TMA producer warp
+constexpr uint32_t kPendSlab = 16 + 32 * 8 + 32 * 16;  // per-warp parked dense-gradient rows (sc_device.cuh)
 constexpr uint32_t kNone = 0xFFFFFFFFu;            // "no label" key
 constexpr uint8_t kCatNone = 0xFF;                 // label in no list (Multi-Choice tables)
 
@@ -97,6 +98,7 @@ struct EvalParams {
   int32_t blocked;          // units: one contiguous block per CTA (1) or round-robin over CTAs (0)
   int32_t ld_flavor;        // gather kernel global-load cache flavour (see ldg_stream_f32)
   int32_t dm_full;          // dense-mapped rows (pat 2): groups 0..NV-2 fully inside the row's n columns
+  int32_t pend_off;         // byte offset of the per-warp parked dense-gradient slabs (sc_device.cuh), or -1
 };
 
 struct HistParams {

@@ -647,6 +647,10 @@ __global__ void __launch_bounds__(kThreads, 1) eval_kernel(const EvalParams p) {
     const int ng = p.ng, wg = kConsumerWarps / p.ng;
     const int grp = cw / wg, wi = cw % wg;
     const uint32_t sbase = smem_addr(smem);
+    if (p.pend_off >= 0) {  // this warp's parked dense-gradient slab: none parked
+      if (lane == 0) asm volatile("st.shared.v2.u32 [%0], {%1, %1};" ::"r"(pend_slab(p)), "r"(0u) : "memory");
+      __syncwarp();
+    }
     // this group's units are the CTA-local indices grp, grp+ng, ...: stage and phase advance by ng
     int st_idx = grp;
     uint32_t ph = 0;
@@ -663,7 +667,9 @@ __global__ void __launch_bounds__(kThreads, 1) eval_kernel(const EvalParams p) {
       const SideBand wa = p.app ? sb_window(p.app, r0, nr, 2) : SideBand{0u, 0u};
       const uint32_t m_base = sbase + st_off + p.mask_off - wm.head;
       const uint32_t a_base = sbase + st_off + p.app_off - wa.head;
+      int nscan = 0;  // rows this warp scans in this stage
       for (int j = wi; j < nr; j += wg) {
+        ++nscan;
         const int64_t row = r0 + j;
         const uint32_t a = !p.app ? 0u
                            : (2u * j - wa.head < wa.nb ? lds_u16(a_base + 2u * j) : static_cast<uint32_t>(__ldg(p.app + row)));
@@ -691,7 +697,7 @@ __global__ void __launch_bounds__(kThreads, 1) eval_kernel(const EvalParams p) {
             kp = dm_cat(p, kp);
             km = dm_cat(p, km);
             if (b.n == lim) {
-              finish_batch(p, b, wtab, lane);
+              finish_batch<true>(p, b, wtab, lane);
               lim = 32;
             }
             deposit(b, lane, zp, kp, zm, km, G, a, row);
@@ -738,7 +744,7 @@ __global__ void __launch_bounds__(kThreads, 1) eval_kernel(const EvalParams p) {
           warp_argmax(zp, kp);
           warp_argmax(zm, km);
           if (b.n == lim) {
-            finish_app_choice(p, b, wtab, lane);
+            finish_app_choice<true>(p, b, wtab, lane);
             lim = 32;
           }
           deposit(b, lane, zp, kp, zm, km, G, a, row, lo);
@@ -754,7 +760,7 @@ __global__ void __launch_bounds__(kThreads, 1) eval_kernel(const EvalParams p) {
           uint32_t kp, km;
           scan_vals<EPL>(le, pm, zs, zp, kp, zm, km);
           if (b.n == lim) {  // several rows per warp in this stage
-            finish_batch(p, b, wtab, lane);
+            finish_batch<true>(p, b, wtab, lane);
             lim = 32;
           }
           deposit(b, lane, zp, kp, zm, km, G, a, row);
@@ -772,11 +778,14 @@ __global__ void __launch_bounds__(kThreads, 1) eval_kernel(const EvalParams p) {
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(empty + st_idx);
+      // dense gradient: the previous batch's rows, as many as rows were scanned, so the writes
+      // interleave with the reads instead of bursting at the batch boundary
+      if (kSplit && p.pend_off >= 0) dense_drain(p, lane, nscan);
       // the batch epilogue runs after the stage is released, and the warps' batch boundaries
       // are staggered (lim) so they do not all hold the pipeline in the same stage
       if (b.n == lim) {
-        if constexpr (PAT == 3) finish_app_choice(p, b, wtab, lane);
-        else if constexpr (kSplit) finish_batch(p, b, wtab, lane);
+        if constexpr (PAT == 3) finish_app_choice<true>(p, b, wtab, lane);
+        else if constexpr (kSplit) finish_batch<true>(p, b, wtab, lane);
         else finish_slots<EPL>(p, b, sz, sk, wtab, lane);
         lim = 32;
       }
@@ -784,10 +793,11 @@ __global__ void __launch_bounds__(kThreads, 1) eval_kernel(const EvalParams p) {
       if (st_idx >= p.stages) { st_idx -= p.stages; ph ^= 1u; }
     }
     if (b.n > 0) {
-      if constexpr (PAT == 3) finish_app_choice(p, b, wtab, lane);
-      else if constexpr (kSplit) finish_batch(p, b, wtab, lane);
+      if constexpr (PAT == 3) finish_app_choice<true>(p, b, wtab, lane);
+      else if constexpr (kSplit) finish_batch<true>(p, b, wtab, lane);
       else finish_slots<EPL>(p, b, sz, sk, wtab, lane);
     }
+    if (kSplit && p.pend_off >= 0) dense_drain(p, lane, 32);
     return;
   } else {
     // ---- generic: entries from a list, rows possibly split into column chunks
