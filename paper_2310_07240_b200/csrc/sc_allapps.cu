@@ -230,23 +230,16 @@ __device__ __forceinline__ uint32_t lds16(uint32_t a) {
   return v;
 }
 
-// One entry of a lane's split maxima: plus side iff the entry's list bit is in G.
-__device__ __forceinline__ void aa_entry(float z, uint32_t key, uint32_t G, float& zp, uint32_t& kp, float& zm,
-                                         uint32_t& km) {
+// One entry of a lane's arg max (strict '>': the earlier, smaller label keeps ties).
+__device__ __forceinline__ void aa_max(float z, uint32_t key, float& zb, uint32_t& kb) {
   asm("{\n\t"
-      ".reg .pred bp, gp, gm;\n\t"
-      ".reg .b32 t;\n\t"
-      "and.b32 t, %5, %6;\n\t"  // G < 256: only the list bits survive
-      "setp.ne.u32 bp, t, 0;\n\t"
-      "setp.gt.and.f32 gp, %4, %0, bp;\n\t"
-      "setp.gt.and.f32 gm, %4, %2, !bp;\n\t"
-      "@gp mov.f32 %0, %4;\n\t"
-      "@gp mov.b32 %1, %5;\n\t"
-      "@gm mov.f32 %2, %4;\n\t"
-      "@gm mov.b32 %3, %5;\n\t"
+      ".reg .pred g;\n\t"
+      "setp.gt.f32 g, %2, %0;\n\t"
+      "@g mov.f32 %0, %2;\n\t"
+      "@g mov.b32 %1, %3;\n\t"
       "}"
-      : "+f"(zp), "+r"(kp), "+f"(zm), "+r"(km)
-      : "f"(z), "r"(key), "r"(G));
+      : "+f"(zb), "+r"(kb)
+      : "f"(z), "r"(key));
 }
 
 // Lane per application (the default): the 32 lanes of a warp scan 32 different applications
@@ -341,32 +334,36 @@ __global__ void __launch_bounds__(kAAWarps * 32, 1) all_apps_lane_kernel(const A
       const bool live = a != 0xFFFFu;
       const uint32_t G = live ? gs[r * A + a] : 0u;
       const uint32_t rb = smem_u32(rowbuf + (buf * R + r) * p.row_bytes_pad);
-      float zp = -CUDART_INF_F, zm = -CUDART_INF_F;
-      uint32_t kp = kNone, km = kNone;
       const uint32_t e0 = smem_u32(ents + goff[g] + lane);
       const int n = (goff[g + 1] - goff[g]) >> 5;
-      // keys here are column << 8 | (1 << list): the class test is one AND with G; padding
-      // entries carry no list bit (the minus side) and point at z = -inf, which never wins
+      // The decision needs only the arg max over the application's 𝕎 (a3: the first mapped
+      // label in confidence order, then z > tau), not the split into 𝒲_i / 𝕎∖𝒲_i: one
+      // compare-select per entry.  Keys are column << 8 | (1 << list), ascending in the lane,
+      // so the strict '>' keeps the smaller label on ties (A4); padding entries point at
+      // z = -inf, which never wins.
+      float zb = -CUDART_INF_F;
+      uint32_t kb = kNone;
       if (p.bf16) {
+#pragma unroll 4
         for (int t = 0; t < n; ++t) {
           const uint32_t key = lds32(e0 + 128u * t);
           const float z = __uint_as_float(lds16(rb + 2u * (key >> 8)) << 16);
-          aa_entry(z, key, G, zp, kp, zm, km);
+          aa_max(z, key, zb, kb);
         }
       } else {
+#pragma unroll 4
         for (int t = 0; t < n; ++t) {
           const uint32_t key = lds32(e0 + 128u * t);
           const float z = __uint_as_float(lds32(rb + 4u * (key >> 8)));
-          aa_entry(z, key, G, zp, kp, zm, km);
+          aa_max(z, key, zb, kb);
         }
       }
       // back to column << 8 | list for the decision
-      if (kp != kNone) kp = (kp & ~0xFFu) | static_cast<uint32_t>(__ffs(kp & 0xFFu) - 1);
-      if (km != kNone) km = (km & ~0xFFu) | static_cast<uint32_t>(__ffs(km & 0xFFu) - 1);
+      if (kb != kNone) kb = (kb & ~0xFFu) | static_cast<uint32_t>(__ffs(kb & 0xFFu) - 1);
       if (live) {
         uint32_t dec;
         bool ok;
-        aa_decide(Split{zp, zm, kp, km}, G, nl[a], p.ctx.tau, dec, ok);
+        aa_decide(Split{zb, -CUDART_INF_F, kb, kNone}, G, nl[a], p.ctx.tau, dec, ok);
         if (!ok) atomicAdd(cnt_inc + a, 1u);
         atomicAdd(cnt_pred + a * 16 + dec, 1u);
         if (p.decision) p.decision[(u * R + r) * A + a] = static_cast<uint8_t>(dec);

@@ -247,33 +247,53 @@ __device__ __forceinline__ void finish_lists(const EvalParams& p, RowBatch& b, L
 // maxima are assembled per lane (one row each) in the batch epilogue.
 template <int EPL>
 struct SlotEnt {
-  uint32_t key[EPL];  // c << 8 | cat[c], kNone for padding
-  uint32_t off[EPL];  // byte offset of the label in a row (0 for padding)
+  uint32_t key[EPL];  // c << 8 | cat[c]; padding 0xFF (column 0, never a winner)
   int ns;             // slots of the application (warp-uniform)
-  uint32_t lists;     // list of slot s in bits 4s..4s+3 (DevContext::lslot)
+  uint32_t lastm;     // bit t: slot t is the last slot of its list (warp-uniform)
   int32_t app;
 };
+
+// Bit t set iff slot t (< ns) ends its list: the next slot holds another list, or none.
+__device__ __forceinline__ uint32_t slot_lastm(uint32_t lists, int ns) {
+  uint32_t m = 0;
+#pragma unroll
+  for (int t = 0; t < 8; ++t)
+    if (t < ns && (t + 1 == ns || ((lists >> (4 * t)) & 15u) != ((lists >> (4 * t + 4)) & 15u))) m |= 1u << t;
+  return m;
+}
 
 template <int EPL>
 __device__ __forceinline__ void slot_ent_load(SlotEnt<EPL>& se, const DevContext& c, int32_t app, int lane,
                                               uint32_t elt) {
   const int32_t e0 = __ldg(c.lent_off + app), e1 = __ldg(c.lent_off + app + 1);
   se.ns = (e1 - e0) >> 5;
-  se.lists = __ldg(c.lslot + app);
+  se.lastm = slot_lastm(__ldg(c.lslot + app), se.ns);
   se.app = app;
 #pragma unroll
   for (int t = 0; t < EPL; ++t) {
     const uint32_t k = t < se.ns ? __ldg(c.lent + e0 + t * 32 + lane) : kNone;
-    se.key[t] = k;
-    se.off[t] = k == kNone ? 0u : (k >> 8) * elt;
+    se.key[t] = k == kNone ? 0xFFu : k;  // the byte offset (key >> 8) * elt is 0 for padding
   }
 }
 
+// One entry of a list's fold: padding (key 0xFF) never wins; strict '>' keeps the smaller,
+// earlier label on ties (A4).
+__device__ __forceinline__ void slot_fold(float z, uint32_t key, float& fz, uint32_t& fk) {
+  asm("{\n\t"
+      ".reg .pred v, g;\n\t"
+      "setp.ne.u32 v, %3, 255;\n\t"
+      "setp.gt.and.f32 g, %2, %0, v;\n\t"
+      "@g mov.f32 %0, %2;\n\t"
+      "@g mov.b32 %1, %3;\n\t"
+      "}"
+      : "+f"(fz), "+r"(fk)
+      : "f"(z), "r"(key));
+}
+
 // a3 for one row: the arg max of every list; lane `slot` keeps them (sz, sk), at the
-// position of the list's last slot (the list's other slots hold kNone).  A list's slots are
-// consecutive and a lane's entries in them ascend, so each lane first folds its slots of one
-// list with a strict '>' (the smaller label keeps ties), then one warp arg max per list —
-// not one per 32-label slot.
+// position of the list's last slot (se.lastm; the other slots' sz / sk are left stale).  A
+// list's slots are consecutive and a lane's entries in them ascend, so each lane first folds
+// its slots of one list, then one warp arg max per list — not one per 32-label slot.
 template <int EPL>
 __device__ __forceinline__ void scan_slots(const SlotEnt<EPL>& se, const float (&zs)[EPL], float (&sz)[EPL],
                                            uint32_t (&sk)[EPL], int slot, int lane) {
@@ -282,13 +302,8 @@ __device__ __forceinline__ void scan_slots(const SlotEnt<EPL>& se, const float (
 #pragma unroll
   for (int t = 0; t < EPL; ++t) {
     if (t < se.ns) {  // warp-uniform
-      const uint32_t k = se.key[t];
-      if (k != kNone && (fk == kNone || zs[t] > fz)) {
-        fz = zs[t];
-        fk = k;
-      }
-      const bool last = t + 1 == se.ns || ((se.lists >> (4 * t)) & 15u) != ((se.lists >> (4 * t + 4)) & 15u);
-      if (last) {  // warp-uniform: list of slot t ends here
+      slot_fold(zs[t], se.key[t], fz, fk);
+      if ((se.lastm >> t) & 1u) {  // warp-uniform: list of slot t ends here
         float z = fz;
         uint32_t kk = fk;
         warp_argmax(z, kk);
@@ -298,8 +313,6 @@ __device__ __forceinline__ void scan_slots(const SlotEnt<EPL>& se, const float (
         }
         fz = -CUDART_INF_F;
         fk = kNone;
-      } else if (lane == slot) {
-        sk[t] = kNone;
       }
     }
   }
@@ -320,9 +333,10 @@ __device__ __forceinline__ void finish_slots(const EvalParams& p, RowBatch& b, c
   if (lane < b.n) {
     const uint32_t lists = __ldg(p.ctx.lslot + b.app);
     const int ns = (__ldg(p.ctx.lent_off + b.app + 1) - __ldg(p.ctx.lent_off + b.app)) >> 5;
+    const uint32_t lastm = slot_lastm(lists, ns);
 #pragma unroll
     for (int t = 0; t < EPL; ++t) {
-      if (t < ns && sk[t] != kNone) {
+      if (((lastm >> t) & 1u) && sk[t] != kNone) {
         const uint32_t j = (lists >> (4 * t)) & 15u;
 #pragma unroll
         for (int q = 0; q < 8; ++q)
@@ -767,7 +781,7 @@ __global__ void __launch_bounds__(kThreads, 1) eval_kernel(const EvalParams p) {
         } else {
           if (static_cast<int32_t>(a) != se.app) slot_ent_load(se, p.ctx, static_cast<int32_t>(a), lane, kElt);
 #pragma unroll
-          for (int t = 0; t < EPL; ++t) zs[t] = t < se.ns ? lds_z<BF16>(srow + se.off[t]) : 0.f;
+          for (int t = 0; t < EPL; ++t) zs[t] = t < se.ns ? lds_z<BF16>(srow + (se.key[t] >> 8) * kElt) : 0.f;
           if (b.n == lim) {  // the batch's slot maxima live in sz/sk: finish before the next scan
             finish_slots<EPL>(p, b, sz, sk, wtab, lane);
             lim = 32;
