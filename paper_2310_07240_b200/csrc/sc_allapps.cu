@@ -224,6 +224,11 @@ __device__ __forceinline__ uint32_t lds32(uint32_t a) {
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
   return v;
 }
+__device__ __forceinline__ float lds_f32(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
 __device__ __forceinline__ uint32_t lds16(uint32_t a) {
   unsigned short v;
   asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
@@ -378,6 +383,208 @@ __global__ void __launch_bounds__(kAAWarps * 32, 1) all_apps_lane_kernel(const A
       atomicAdd(p.hist_pred + (i >> 4) * 256 + (i & 15), static_cast<unsigned long long>(cnt_pred[i]));
 }
 
+// Lane per ROW (the default when C <= kTRMaxC): a unit of kTRRows = 32 rows is held
+// transposed in shared memory — element (r, c) at word kTRStride·c + r — so when the 32 lanes
+// of a warp (one row each) read the same column of their own rows they hit 32 distinct banks
+// (the lane-per-application kernel above reads 32 random columns of one row: ~3.5-way bank
+// conflicts per load, and shared-memory wavefronts bounded it).  A warp evaluates one
+// application on all 32 rows of the unit: its entries (16-bit word offsets of the columns,
+// ascending, every application's in shared memory) are warp-uniform 8-B broadcast loads of 4
+// entries, and per entry a lane does one address computation, one conflict-free shared load
+// and one compare-select — the arg max over 𝕎_a (a3; the strict '>' keeps the smaller label
+// on ties, A4), tracked by its shared address, from which the column and then its list
+// (catT) are recovered once per (row, application).  The next
+// unit's rows are loaded into registers (two rows per warp) while the current unit is
+// evaluated, then stored transposed; G per (row, application) comes from the row's ground
+// truth and the label-major category table (Eq. goal's correctness).
+template <bool BF16>
+__global__ void __launch_bounds__(kTRWarps * 32, 1) all_apps_rows_kernel(const AllAppsParams p) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int A = p.ctx.n_apps, C = p.ctx.C;
+  float* tr = reinterpret_cast<float*>(sm);                                        // [C + 1][kTRStride]
+  uint8_t* gtile = sm + 4 * static_cast<size_t>(kTRStride) * (C + 1);                // [A][kTRRows]
+  unsigned* cnt_inc = reinterpret_cast<unsigned*>(gtile + kTRRows * A + 3 - (kTRRows * A + 3) % 4);  // [A]
+  unsigned* cnt_pred = cnt_inc + A;                                                  // [A][16]
+  uint8_t* nl = reinterpret_cast<uint8_t*>(cnt_pred + 16 * A);                       // [A]
+  const size_t kofs = (4 * static_cast<size_t>(kTRStride) * (C + 1) + kTRRows * A + 4 * A + 64 * A + A + 15) / 16 * 16;
+  uint16_t* keys = reinterpret_cast<uint16_t*>(sm + kofs);                           // [tr_total]
+  int32_t* toff = reinterpret_cast<int32_t*>(keys + p.tr_total);                     // [A + 1] (tr_total % 4 == 0)
+  uint16_t* order = reinterpret_cast<uint16_t*>(toff + A + 1);                        // [A] applications, |W_a| descending
+  for (int i = tid; i < p.tr_total / 8; i += blockDim.x)
+    reinterpret_cast<uint4*>(keys)[i] = __ldg(reinterpret_cast<const uint4*>(p.tr_key) + i);
+  for (int i = p.tr_total / 8 * 8 + tid; i < p.tr_total; i += blockDim.x) keys[i] = __ldg(p.tr_key + i);
+  for (int i = tid; i <= A; i += blockDim.x) toff[i] = __ldg(p.tr_off + i);
+  for (int i = tid; i < A; i += blockDim.x) order[i] = __ldg(p.aa_perm + i);
+  for (int i = tid; i < kTRRows; i += blockDim.x) tr[kTRStride * C + i] = -CUDART_INF_F;  // padding column
+  for (int i = tid; i < A; i += blockDim.x) { cnt_inc[i] = 0; nl[i] = __ldg(p.ctx.nlists + i); }
+  for (int i = tid; i < 16 * A; i += blockDim.x) cnt_pred[i] = 0;
+
+  const int64_t n_units = (p.rows + kTRRows - 1) / kTRRows;
+  constexpr int kJ = BF16 ? kTRMaxC / 64 : kTRMaxC / 32;  // staged words per lane and row
+  uint32_t v[2][kJ];
+  // stage rows u*32 + 2w, 2w + 1 of unit u in registers (f32: column 32 j + lane; bf16: the
+  // column pair 64 j + 2 lane, +1)
+  auto stage = [&](int64_t u) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t row = u * kTRRows + 2 * warp + h;
+      const uint8_t* src = p.logits + row * p.ld_bytes;
+#pragma unroll
+      for (int j = 0; j < kJ; ++j) {
+        const int c = BF16 ? 64 * j + 2 * lane : 32 * j + lane;
+        v[h][j] = (u < n_units && row < p.rows && c < C) ? __ldg(reinterpret_cast<const uint32_t*>(src) + (BF16 ? c / 2 : c)) : 0u;
+      }
+    }
+  };
+  const int64_t first = blockIdx.x, step = gridDim.x;
+  stage(first);
+  __syncthreads();
+  const uint32_t lb = smem_u32(tr) + 4u * static_cast<uint32_t>(lane);
+  const float tau = p.ctx.tau;
+  for (int64_t u = first; u < n_units; u += step) {
+    const int64_t row0 = u * kTRRows;
+    const int nr = static_cast<int>(p.rows - row0 < kTRRows ? p.rows - row0 : kTRRows);
+    // the staged rows, transposed
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = 2 * warp + h;
+#pragma unroll
+      for (int j = 0; j < kJ; ++j) {
+        if constexpr (BF16) {
+          const int c = 64 * j + 2 * lane;
+          if (c < C) tr[kTRStride * c + r] = __uint_as_float(v[h][j] << 16);
+          if (c + 1 < C) tr[kTRStride * (c + 1) + r] = __uint_as_float(v[h][j] & 0xFFFF0000u);
+        } else {
+          const int c = 32 * j + lane;
+          if (c < C) tr[kTRStride * c + r] = __uint_as_float(v[h][j]);
+        }
+      }
+    }
+    // G of every (row, application), a2: warp w builds rows 2w, 2w + 1; the row's ground-truth
+    // labels are warp-uniform loads, each lane ORs the lists of applications lane + 32 k
+    // (independent, coalesced 32-B reads of the label-major category table)
+#pragma unroll 1
+    for (int h = 0; h < 2; ++h) {
+      const int r = 2 * warp + h;
+      const int64_t g0 = r < nr ? __ldg(p.gt_off + row0 + r) : 0, g1 = r < nr ? __ldg(p.gt_off + row0 + r + 1) : 0;
+      for (int a0 = 0; a0 < A; a0 += 256) {
+        uint32_t G[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int64_t t = g0; t < g1; ++t) {
+          const uint8_t* crow = p.catT + static_cast<int64_t>(__ldg(p.gt_lab + t)) * A;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const int a = a0 + 32 * k + lane;
+            if (a < A) G[k] |= label_lists(__ldg(crow + a), kApiOutput);
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int a = a0 + 32 * k + lane;
+          if (a < A) gtile[a * kTRRows + r] = static_cast<uint8_t>(G[k]);
+        }
+      }
+    }
+    __syncthreads();
+    stage(u + step);  // in flight while this unit is evaluated
+    const bool live_row = lane < nr;
+    const unsigned act = __ballot_sync(kFull, live_row);
+    // One application on the unit's 32 rows per item; applications in |W_a|-descending order,
+    // dealt in a snake over the warps.  The epilogue of an item (its list from catT, a global
+    // load) runs after the NEXT item's scan, so the load's latency hides behind that scan.
+    int pa = -1;          // the pending item's application
+    uint32_t pcat = 0;    // its winner's list (load in flight), 0xFF: default
+    auto finish = [&](int a, uint32_t cat) {
+      const uint32_t D = nl[a];
+      const uint32_t dec = cat != 0xFFu ? cat : D;
+      const uint32_t G = gtile[a * kTRRows + lane];
+      const bool ok = G ? (dec < D && ((G >> dec) & 1u)) : (dec == D);
+      const unsigned inc = __ballot_sync(kFull, live_row && !ok);
+      if (lane == 0 && inc) cnt_inc[a] += __popc(inc);  // application a: this warp only, this unit
+      if (live_row) {
+        const unsigned peers = __match_any_sync(act, dec);
+        if (lane == __ffs(peers) - 1) cnt_pred[a * 16 + dec] += __popc(peers);
+        gtile[a * kTRRows + lane] = static_cast<uint8_t>(dec);  // G is read; the tile now holds decisions
+      }
+    };
+    for (int k = 0;; ++k) {
+      const int i = (k >> 1) * 2 * kTRWarps + ((k & 1) ? 2 * kTRWarps - 1 - warp : warp);
+      if (i >= A) {
+        if (k & 1) continue;
+        break;
+      }
+      const int a = order[i];
+      const int32_t e0 = toff[a], n = toff[a + 1] - e0;
+      const uint32_t kb0 = smem_u32(keys + e0);
+      float zb = -CUDART_INF_F;
+      uint32_t ab = 0;  // shared address of the winner (0: none)
+#pragma unroll 2
+      for (int q = 0; q < n; q += 4) {
+        uint32_t k01, k23;  // four entries (16-bit word offsets of their columns), warp-uniform
+        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(k01), "=r"(k23) : "r"(kb0 + 2u * q));
+        // per entry: the address (extract + one multiply-add), a conflict-free load, and the
+        // strict '>' update of the running maximum and its address (A4: earlier entries win ties)
+        asm volatile(
+            "{\n\t"
+            ".reg .u32 a0, a1, a2, a3;\n\t"
+            ".reg .f32 z0, z1, z2, z3;\n\t"
+            ".reg .pred p;\n\t"
+            "and.b32 a0, %2, 65535;\n\t"
+            "shr.u32 a1, %2, 16;\n\t"
+            "and.b32 a2, %3, 65535;\n\t"
+            "shr.u32 a3, %3, 16;\n\t"
+            "mad.lo.u32 a0, a0, 4, %4;\n\t"
+            "mad.lo.u32 a1, a1, 4, %4;\n\t"
+            "mad.lo.u32 a2, a2, 4, %4;\n\t"
+            "mad.lo.u32 a3, a3, 4, %4;\n\t"
+            "ld.shared.f32 z0, [a0];\n\t"
+            "ld.shared.f32 z1, [a1];\n\t"
+            "ld.shared.f32 z2, [a2];\n\t"
+            "ld.shared.f32 z3, [a3];\n\t"
+            "setp.gt.f32 p, z0, %0;\n\t"
+            "@p mov.f32 %0, z0;\n\t"
+            "@p mov.u32 %1, a0;\n\t"
+            "setp.gt.f32 p, z1, %0;\n\t"
+            "@p mov.f32 %0, z1;\n\t"
+            "@p mov.u32 %1, a1;\n\t"
+            "setp.gt.f32 p, z2, %0;\n\t"
+            "@p mov.f32 %0, z2;\n\t"
+            "@p mov.u32 %1, a2;\n\t"
+            "setp.gt.f32 p, z3, %0;\n\t"
+            "@p mov.f32 %0, z3;\n\t"
+            "@p mov.u32 %1, a3;\n\t"
+            "}"
+            : "+f"(zb), "+r"(ab)
+            : "r"(k01), "r"(k23), "r"(lb));
+      }
+      // a3: the first mapped label in confidence order is an output iff z > tau; its list
+      // from catT (column recovered from the winner's address), loaded now, used next item
+      uint32_t cat = 0xFFu;
+      if (ab != 0 && zb > tau) {
+        const uint32_t c = (ab - lb) / (4u * kTRStride);
+        cat = __ldg(p.catT + static_cast<int64_t>(c) * A + a);
+      }
+      if (pa >= 0) finish(pa, pcat);
+      pa = a;
+      pcat = cat;
+    }
+    if (pa >= 0) finish(pa, pcat);
+    __syncthreads();
+    if (p.decision) {
+      for (int i = tid; i < nr * A; i += blockDim.x) {
+        const int r = i / A, a = i - r * A;
+        p.decision[(row0 + r) * A + a] = gtile[a * kTRRows + r];
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = tid; i < A; i += blockDim.x)
+    if (cnt_inc[i] && p.n_incorrect) atomicAdd(p.n_incorrect + i, static_cast<unsigned long long>(cnt_inc[i]));
+  for (int i = tid; i < A * 16; i += blockDim.x)
+    if (cnt_pred[i] && p.hist_pred)
+      atomicAdd(p.hist_pred + (i >> 4) * 256 + (i & 15), static_cast<unsigned long long>(cnt_pred[i]));
+}
+
 }  // namespace
 
 cudaError_t launch_all_apps_lane(const AllAppsParams& p, int grid, size_t smem, cudaStream_t st) {
@@ -385,6 +592,14 @@ cudaError_t launch_all_apps_lane(const AllAppsParams& p, int grid, size_t smem, 
                                        static_cast<int>(smem));
   if (e) return e;
   all_apps_lane_kernel<<<grid, kAAWarps * 32, smem, st>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_all_apps_rows(const AllAppsParams& p, int grid, size_t smem, cudaStream_t st) {
+  auto k = p.bf16 ? all_apps_rows_kernel<true> : all_apps_rows_kernel<false>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e) return e;
+  k<<<grid, kTRWarps * 32, smem, st>>>(p);
   return cudaGetLastError();
 }
 

@@ -573,6 +573,21 @@ static sc_status load_context(int32_t C, int32_t n_apps, const int32_t* n_lists,
     if (!e) e = cudaMemcpy(ctx->d_aa_ent, aent.data(), aent.size() * 4, cudaMemcpyHostToDevice);
     if (!e) e = cudaMemcpy(ctx->d_aa_goff, goff.data(), goff.size() * 4, cudaMemcpyHostToDevice);
     if (!e) e = cudaMemcpy(ctx->d_aa_perm, aperm.data(), aperm.size() * 2, cudaMemcpyHostToDevice);
+    if (C <= sc::kTRMaxC) {  // lane per row: word offsets of the columns in the transposed unit
+      std::vector<int32_t> toff(n_apps + 1, 0);
+      for (int32_t a = 0; a < n_apps; ++a) toff[a + 1] = toff[a] + (ent_off[a + 1] - ent_off[a] + 3) / 4 * 4;
+      const uint16_t pad = static_cast<uint16_t>(sc::kTRStride * C);
+      std::vector<uint16_t> tkey(std::max<int32_t>(toff[n_apps], 4), pad);
+      for (int32_t a = 0; a < n_apps; ++a)
+        for (int32_t t = ent_off[a]; t < ent_off[a + 1]; ++t) {
+          tkey[toff[a] + t - ent_off[a]] = static_cast<uint16_t>(sc::kTRStride * (ent[t] >> 8));
+        }
+      ctx->tr_total = static_cast<int32_t>(tkey.size());
+      if (!e) e = cudaMalloc(&ctx->d_tr_key, tkey.size() * 2);
+      if (!e) e = cudaMalloc(&ctx->d_tr_off, toff.size() * 4);
+      if (!e) e = cudaMemcpy(ctx->d_tr_key, tkey.data(), tkey.size() * 2, cudaMemcpyHostToDevice);
+      if (!e) e = cudaMemcpy(ctx->d_tr_off, toff.data(), toff.size() * 4, cudaMemcpyHostToDevice);
+    }
   }
   if (!e) e = cudaMemcpy(ctx->d_cat, cat.data(), cat.size(), cudaMemcpyHostToDevice);
   if (!e) e = cudaMemcpy(ctx->d_ent, ent.data(), ent.size() * 4, cudaMemcpyHostToDevice);
@@ -604,6 +619,8 @@ sc_status sc_context_free(sc_context ctx) {
   cudaFree(ctx->d_aa_ent);
   cudaFree(ctx->d_aa_goff);
   cudaFree(ctx->d_aa_perm);
+  cudaFree(ctx->d_tr_key);
+  cudaFree(ctx->d_tr_off);
   cudaFree(ctx->d_col_label);
   delete ctx;
   return SC_OK;
@@ -759,7 +776,27 @@ sc_status sc_decide_all_apps(sc_context ctx, const sc_batch* b, uint64_t* n_inco
   p.decision = decision;
   const int64_t A = ctx->n_apps;
   const char* aa_env = std::getenv("SC_ALLAPPS");
-  if (!(aa_env && std::string(aa_env) == "warp")) {
+  const std::string aa_mode = aa_env ? aa_env : "";
+  if (aa_mode.empty() && ctx->d_tr_key) {
+    // lane per row: the unit transposed in shared memory ([C+1] columns of kTRStride words),
+    // G / decision tile [A][kTRRows], counters [A] + [A][16], D' [A]
+    p.tr_key = ctx->d_tr_key;
+    p.tr_off = ctx->d_tr_off;
+    p.aa_perm = ctx->d_aa_perm;
+    p.tr_total = ctx->tr_total;
+    const int64_t o = round_up(4 * static_cast<int64_t>(sc::kTRStride) * (ctx->C + 1) + sc::kTRRows * A + 4 * A + 64 * A + A, 16) +
+                      2 * static_cast<int64_t>(ctx->tr_total) + 4 * (A + 1) + 2 * A;  // + entries, offsets, order
+    const size_t sm = static_cast<size_t>(round_up(o, 16));
+    if (sm <= kSmemMax) {
+      const int grid = static_cast<int>(std::min<int64_t>((b->rows + sc::kTRRows - 1) / sc::kTRRows, di.sms));
+      if (cudaError_t e = sc::launch_all_apps_rows(p, grid, sm, static_cast<cudaStream_t>(stream)))
+        return cuda_fail(e, "all-apps kernel launch");
+      g_last_kernel = "all_apps_rows";
+      g_launches.fetch_add(1, std::memory_order_relaxed);
+      return SC_OK;
+    }
+  }
+  if (aa_mode != "warp") {
     // lane per application: [2 units x R] row buffers (each with a -inf slot at column C),
     // transposed entries, group offsets, perm, counters, G [2][R][A], D'
     p.aa_ent = ctx->d_aa_ent;

@@ -42,6 +42,10 @@ struct sc_context_s {
   int32_t* d_aa_goff = nullptr;
   uint16_t* d_aa_perm = nullptr;
   int32_t aa_groups = 0, aa_ent_total = 0;
+  // all-apps pass, lane per row (C <= kTRMaxC; see AllAppsParams::tr_*)
+  uint16_t* d_tr_key = nullptr;
+  int32_t tr_total = 0;
+  int32_t* d_tr_off = nullptr;
 };
 
 namespace sc {

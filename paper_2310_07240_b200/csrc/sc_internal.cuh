@@ -141,9 +141,23 @@ struct AllAppsParams {
   int32_t n_groups, aa_ent_total;
   int32_t rows_per_unit;    // R
   uint32_t dummy_key;       // key of a padding entry: column = the row buffer's -inf slot, no list bit
+  // lane-per-row layout (all_apps_rows_kernel, C <= kTRMaxC): a unit of kTRRows rows is held
+  // transposed in shared memory, element (row r, column c) at word kTRStride * c + r (every
+  // lane of a warp reads the same column of its own row: 32 distinct banks), column C = -inf.
+  // Application a's entries tr_key[tr_off[a] .. tr_off[a+1]) = kTRStride * c (the word
+  // offset of column c, < 2^16), ascending, padded to a multiple of 4 with column C (a winner's
+  // list is read from catT).  Applications are dealt in aa_perm order (|W_a| descending).
+  const uint16_t* tr_key;
+  int32_t tr_total;         // entries of all applications (padded)
+  const int32_t* tr_off;    // [n_apps + 1]
 };
+constexpr int kTRRows = 32;               // rows per unit of the lane-per-row kernel (one per lane)
+constexpr int kTRStride = kTRRows + 1;    // words between columns of the transposed unit
+constexpr int kTRWarps = 16;              // warps per CTA of the lane-per-row kernel
+constexpr int kTRMaxC = 1024;             // columns a unit's rows may have (two rows staged per warp in registers)
 constexpr int kAllAppsRows = 4;  // rows per barrier interval of the warp-per-application kernel
 cudaError_t launch_all_apps_lane(const AllAppsParams& p, int grid, size_t smem, cudaStream_t st);
+cudaError_t launch_all_apps_rows(const AllAppsParams& p, int grid, size_t smem, cudaStream_t st);
 cudaError_t launch_all_apps(const AllAppsParams& p, int grid, size_t smem, cudaStream_t st);
 
 // Launchers (sc_kernels.cu).  Return cudaError_t of the launch.
