@@ -9,7 +9,9 @@ weights, the weights kernel, the all-apps kernel, the value-ranges kernels (pack
 match counters, fast and far S arguments, unaligned arrays), the sampler, and the fused
 classifier head.  Round 2 adds: the dense-mapped eval path (column-compacted rows, f32 /
 bf16), the host-buffer entry (copy and zero copy), the lane-per-application all-apps kernel,
-the head under every pattern and with column passes (CTA pairs with two row tiles too).
+the head under every pattern and with column passes (CTA pairs with two row tiles too);
+session 3: the lane-per-row all-apps kernel (f32 / bf16, ragged units) and the parked dense
+gradient rows (every grad_dense step on the TMA ring).
 Side bands at unaligned offsets and ragged row counts exercise the clamped TMA windows.  Outputs are checked against each other only lightly (the parity tests do the
 real checking); the point is a clean sanitizer report.
 """
@@ -134,14 +136,20 @@ def main():
     ni = torch.zeros(256, dtype=torch.int64, device="cuda")
     hp = torch.zeros(256 * 256, dtype=torch.int64, device="cuda")
     dec = torch.empty(77 * 256, dtype=torch.uint8, device="cuda")
-    for impl in ("lane", "warp"):
-        if impl == "warp":
-            os.environ["SC_ALLAPPS"] = "warp"
+    for impl in ("rows", "lane", "warp"):
+        if impl != "rows":
+            os.environ["SC_ALLAPPS"] = impl
         sc.sc_decide_all_apps(ctx, sc.Batch(logits=d["logits"], gt_off=d["gt_off"], gt_lab=d["gt_lab"]),
                               n_incorrect=ni, hist_pred=hp, decision=dec)
         torch.cuda.synchronize()
         seen.append(("all_apps", sc.sc_last_kernel()))
     os.environ.pop("SC_ALLAPPS")
+    bb = synth.Workload(spec, seed=4, dtype="bf16", layout=1).host_batch(0, 45)  # bf16 rows, ragged unit
+    db = dev_batch(bb, "bf16")
+    sc.sc_decide_all_apps(ctx, sc.Batch(logits=db["logits"], gt_off=db["gt_off"], gt_lab=db["gt_lab"]),
+                          n_incorrect=ni, hist_pred=hp, decision=dec[:45 * 256])
+    torch.cuda.synchronize()
+    seen.append(("all_apps_bf16", sc.sc_last_kernel()))
 
     # value ranges: 2-8 bins packed, 21 ballot, 41 match; far S arguments; unaligned arrays
     for m, off, scale in ((7, 0, 1.0), (7, 1, 12.0), (20, 0, 1.0), (40, 3, 12.0)):
