@@ -319,7 +319,8 @@ sc_status run_eval(const sc_context_s* ctx, const sc_batch* b, const float* w, f
   const int64_t dm_slack = launch_pat == 2 ? 512 : 0;
   // dense gradient on the whole-row paths with two arg maxima per row: per-warp slabs where the
   // batch's gradient rows wait to be written between stages (sc_device.cuh dense_pair_rows)
-  const int64_t pend_bytes = (grad_dense && epl > 0 && launch_pat != 1) ? static_cast<int64_t>(W) * sc::kPendSlab : 0;
+  const int64_t pend_bytes = (grad_dense && epl > 0 && epl <= 8 && (launch_pat == 0 || launch_pat == 3))
+                                 ? static_cast<int64_t>(W) * sc::kPendSlab : 0;  // eval_kernel<..., DEFER>
   const int64_t other = ent_bytes + pmtab_bytes + (wtab ? 1024 : 0) + pend_bytes + 2 * 8 * max_stages + 256 + dm_slack;
   int64_t S = (static_cast<int64_t>(kSmemMax) - other) / p.stage_bytes;
   if (S > max_stages) S = max_stages;

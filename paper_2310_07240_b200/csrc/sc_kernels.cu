@@ -499,7 +499,10 @@ struct UnitSched {
 // PAT = 1: the per-list patterns (application-choice order, Multi-Select) on the same
 // ring — EPL = list-major slots per app, one warp arg max per slot (scan_slots), list
 // maxima assembled in the batch epilogue (finish_slots).
-template <int EPL, bool BF16, int PAT>
+// DEFER: dense gradient rows parked per warp and written between stages (dense_pair_rows); a
+// separate instantiation, so the register allocation of the sparse-gradient kernels is the
+// one without it (the shared code cost bf16 5.8 % on the same box, profiles/r4p_*).
+template <int EPL, bool BF16, int PAT, bool DEFER = false>
 __global__ void __launch_bounds__(kThreads, 1) eval_kernel(const EvalParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.bar_off);
@@ -661,7 +664,7 @@ __global__ void __launch_bounds__(kThreads, 1) eval_kernel(const EvalParams p) {
     const int ng = p.ng, wg = kConsumerWarps / p.ng;
     const int grp = cw / wg, wi = cw % wg;
     const uint32_t sbase = smem_addr(smem);
-    if (p.pend_off >= 0) {  // this warp's parked dense-gradient slab: none parked
+    if (DEFER) {  // this warp's parked dense-gradient slab: none parked
       if (lane == 0) asm volatile("st.shared.v2.u32 [%0], {%1, %1};" ::"r"(pend_slab(p)), "r"(0u) : "memory");
       __syncwarp();
     }
@@ -681,7 +684,7 @@ __global__ void __launch_bounds__(kThreads, 1) eval_kernel(const EvalParams p) {
       const SideBand wa = p.app ? sb_window(p.app, r0, nr, 2) : SideBand{0u, 0u};
       const uint32_t m_base = sbase + st_off + p.mask_off - wm.head;
       const uint32_t a_base = sbase + st_off + p.app_off - wa.head;
-      int nscan = 0;  // rows this warp scans in this stage
+      [[maybe_unused]] int nscan = 0;  // rows this warp scans in this stage (DEFER)
       for (int j = wi; j < nr; j += wg) {
         ++nscan;
         const int64_t row = r0 + j;
@@ -711,7 +714,7 @@ __global__ void __launch_bounds__(kThreads, 1) eval_kernel(const EvalParams p) {
             kp = dm_cat(p, kp);
             km = dm_cat(p, km);
             if (b.n == lim) {
-              finish_batch<true>(p, b, wtab, lane);
+              finish_batch<DEFER>(p, b, wtab, lane);
               lim = 32;
             }
             deposit(b, lane, zp, kp, zm, km, G, a, row);
@@ -758,7 +761,7 @@ __global__ void __launch_bounds__(kThreads, 1) eval_kernel(const EvalParams p) {
           warp_argmax(zp, kp);
           warp_argmax(zm, km);
           if (b.n == lim) {
-            finish_app_choice<true>(p, b, wtab, lane);
+            finish_app_choice<DEFER>(p, b, wtab, lane);
             lim = 32;
           }
           deposit(b, lane, zp, kp, zm, km, G, a, row, lo);
@@ -774,7 +777,7 @@ __global__ void __launch_bounds__(kThreads, 1) eval_kernel(const EvalParams p) {
           uint32_t kp, km;
           scan_vals<EPL>(le, pm, zs, zp, kp, zm, km);
           if (b.n == lim) {  // several rows per warp in this stage
-            finish_batch<true>(p, b, wtab, lane);
+            finish_batch<DEFER>(p, b, wtab, lane);
             lim = 32;
           }
           deposit(b, lane, zp, kp, zm, km, G, a, row);
@@ -794,12 +797,12 @@ __global__ void __launch_bounds__(kThreads, 1) eval_kernel(const EvalParams p) {
       if (lane == 0) mbar_arrive(empty + st_idx);
       // dense gradient: the previous batch's rows, as many as rows were scanned, so the writes
       // interleave with the reads instead of bursting at the batch boundary
-      if (kSplit && p.pend_off >= 0) dense_drain(p, lane, nscan);
+      if constexpr (DEFER) dense_drain(p, lane, nscan);
       // the batch epilogue runs after the stage is released, and the warps' batch boundaries
       // are staggered (lim) so they do not all hold the pipeline in the same stage
       if (b.n == lim) {
-        if constexpr (PAT == 3) finish_app_choice<true>(p, b, wtab, lane);
-        else if constexpr (kSplit) finish_batch<true>(p, b, wtab, lane);
+        if constexpr (PAT == 3) finish_app_choice<DEFER>(p, b, wtab, lane);
+        else if constexpr (kSplit) finish_batch<DEFER>(p, b, wtab, lane);
         else finish_slots<EPL>(p, b, sz, sk, wtab, lane);
         lim = 32;
       }
@@ -807,11 +810,11 @@ __global__ void __launch_bounds__(kThreads, 1) eval_kernel(const EvalParams p) {
       if (st_idx >= p.stages) { st_idx -= p.stages; ph ^= 1u; }
     }
     if (b.n > 0) {
-      if constexpr (PAT == 3) finish_app_choice<true>(p, b, wtab, lane);
-      else if constexpr (kSplit) finish_batch<true>(p, b, wtab, lane);
+      if constexpr (PAT == 3) finish_app_choice<DEFER>(p, b, wtab, lane);
+      else if constexpr (kSplit) finish_batch<DEFER>(p, b, wtab, lane);
       else finish_slots<EPL>(p, b, sz, sk, wtab, lane);
     }
-    if (kSplit && p.pend_off >= 0) dense_drain(p, lane, 32);
+    if constexpr (DEFER) dense_drain(p, lane, 32);
     return;
   } else {
     // ---- generic: entries from a list, rows possibly split into column chunks
@@ -1251,12 +1254,12 @@ __device__ void weights_one_app(const unsigned long long* H, float* w_app) {
 
 }  // namespace
 
-template <int EPL, int PAT = 0>
+template <int EPL, int PAT = 0, bool DEFER = false>
 static cudaError_t set_limit_t(size_t smem) {
-  cudaError_t e = cudaFuncSetAttribute(eval_kernel<EPL, false, PAT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e = cudaFuncSetAttribute(eval_kernel<EPL, false, PAT, DEFER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e) return e;
-  return cudaFuncSetAttribute(eval_kernel<EPL, true, PAT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  return cudaFuncSetAttribute(eval_kernel<EPL, true, PAT, DEFER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               static_cast<int>(smem));
 }
 
@@ -1264,6 +1267,7 @@ static cudaError_t set_limit_t(size_t smem) {
 #define SC_EVAL_EPLS_PAT(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8)  // per-list patterns: slots (PAT = 1)
 #define SC_EVAL_NV_DM(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8)     // dense-mapped rows: 16-B groups (PAT = 2)
 #define SC_EVAL_EPLS_AC(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8)   // application-choice, two maxima (PAT = 3)
+#define SC_EVAL_EPLS_DEFER(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) // dense gradient parked (PAT 0 / 3, DEFER)
 
 cudaError_t set_eval_smem_limit(size_t smem) {
   cudaError_t e = set_limit_t<0>(smem);
@@ -1278,6 +1282,9 @@ cudaError_t set_eval_smem_limit(size_t smem) {
 #undef SC_SET
 #define SC_SET(N) if (!e) e = set_limit_t<N, 3>(smem);
   SC_EVAL_EPLS_AC(SC_SET)
+#undef SC_SET
+#define SC_SET(N) if (!e) e = set_limit_t<N, 0, true>(smem); if (!e) e = set_limit_t<N, 3, true>(smem);
+  SC_EVAL_EPLS_DEFER(SC_SET)
 #undef SC_SET
   return e;
 }
@@ -1296,6 +1303,19 @@ int eval_epl_for(int max_ent, int pat) {
 
 template <bool BF16>
 static void launch_eval_dt(const EvalParams& p, int epl, int pat, int grid, size_t smem, cudaStream_t st) {
+  if (p.pend_off >= 0) {  // dense gradient parked (host: PAT 0 / 3, epl <= 8)
+    switch (epl) {
+#define SC_CASE(N)                                                                \
+  case N:                                                                         \
+    if (pat == 3) eval_kernel<N, BF16, 3, true><<<grid, kThreads, smem, st>>>(p); \
+    else eval_kernel<N, BF16, 0, true><<<grid, kThreads, smem, st>>>(p);          \
+    break;
+      SC_EVAL_EPLS_DEFER(SC_CASE)
+#undef SC_CASE
+      default: break;
+    }
+    return;
+  }
   if (pat == 3) {
     switch (epl) {
 #define SC_CASE(N) case N: eval_kernel<N, BF16, 3><<<grid, kThreads, smem, st>>>(p); break;
