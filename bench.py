@@ -92,10 +92,12 @@ def workload_name(cfg, dtype):
     return f"{WORKLOADS[cfg]}, {dtype} logits"
 
 
-def touched_sector_bytes(spec, ld, elt, rows=None, layout_rows_per_app=1 << 18, columns=None):
+def touched_sector_bytes(spec, ld, elt, rows=None, layout_rows_per_app=1 << 18, columns=None, granule=32):
     """Mean bytes per row of the 32-B sectors holding at least one mapped label of the
     row's application (SURVEY.md §8(d)'s algorithmic minimum), row base addresses r*ld*elt.
-    columns: the labels of a compacted row's columns (sc_context_columns), else column c = label c."""
+    columns: the labels of a compacted row's columns (sc_context_columns), else column c = label c.
+    granule=128: the same over 128-B lines, the unit HBM is read in for scattered sectors
+    (lts__t_sectors_srcunit_tex_op_read = dram__sectors_read for the gather)."""
     import numpy as np
     m = spec.mapped()
     per_app = []
@@ -106,13 +108,14 @@ def touched_sector_bytes(spec, ld, elt, rows=None, layout_rows_per_app=1 << 18, 
         if len(cols) == 0:
             per_app.append(0.0)
             continue
-        if (ld * elt) % 32 == 0:
-            per_app.append(len(np.unique((cols * elt) // 32)) * 32.0)
-        else:  # rows not sector aligned: average over the two phases
+        if (ld * elt) % granule == 0:
+            per_app.append(len(np.unique((cols * elt) // granule)) * float(granule))
+        else:  # rows not granule aligned: average over the row phases (rows are 16-B aligned)
+            phases = range(0, granule, 16)
             tot = 0
-            for ph in (0, 16):
-                tot += len(np.unique((ph + cols * elt) // 32)) * 32
-            per_app.append(tot / 2)
+            for ph in phases:
+                tot += len(np.unique((ph + cols * elt) // granule)) * granule
+            per_app.append(tot / len(phases))
     if rows is None or spec.n_apps == 1:
         return float(np.mean(per_app))
     apps = (np.arange(rows) // layout_rows_per_app) % spec.n_apps
@@ -414,6 +417,7 @@ def run_ours(args):
     elt = 4 if args.dtype == "f32" else 2
     ld = logits.stride(0)
     sect = touched_sector_bytes(spec, ld, elt, rows=B, columns=columns)
+    lines = touched_sector_bytes(spec, ld, elt, rows=B, columns=columns, granule=128)
     per_row = sect + 1 + 1 + 8 * ctx.grad_slots + (2 if app is not None else 0)  # sectors + G_i + decision + sparse grad (+ app)
     if args.grad == "dense":
         per_row += ld * 4  # the full f32 gradient row written
@@ -427,6 +431,9 @@ def run_ours(args):
                 "traffic": traffic, "kernel": "eval_kernel (sc_loss_fwd_bwd)", "kernel_ms": k_ms,
                 "algorithmic_bytes_per_row": per_row, "dense_bytes_per_row": ld * elt + 18,
                 "dense_frac": B * (ld * elt + 18) / (k_ms / 1e3) / 1e9 / peak,
+                # the same with the 128-B lines holding a mapped label in place of the sectors
+                "line_bytes_per_row": per_row - sect + lines,
+                "line_frac": B * (per_row - sect + lines) / (k_ms / 1e3) / 1e9 / peak,
                 "eval_kernel": kname, "traffic_source": tpath,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)" if peaks else "fallback 6.65 TB/s"}
 
