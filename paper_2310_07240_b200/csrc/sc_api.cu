@@ -133,6 +133,7 @@ sc_status run_eval(const sc_context_s* ctx, const sc_batch* b, const float* w, f
 
   sc::EvalParams p{};
   p.pend_off = -1;
+  p.hdr_off = -1;
   p.ctx = dev_ctx(ctx);
   p.logits = static_cast<const uint8_t*>(b->logits);
   p.rows = b->rows;
@@ -321,7 +322,7 @@ sc_status run_eval(const sc_context_s* ctx, const sc_batch* b, const float* w, f
   // batch's gradient rows wait to be written between stages (sc_device.cuh dense_pair_rows)
   const int64_t pend_bytes = (grad_dense && epl > 0 && epl <= 8 && (launch_pat == 0 || launch_pat == 3))
                                  ? static_cast<int64_t>(W) * sc::kPendSlab : 0;  // eval_kernel<..., DEFER>
-  const int64_t other = ent_bytes + pmtab_bytes + (wtab ? 1024 : 0) + pend_bytes + 2 * 8 * max_stages + 256 + dm_slack;
+  const int64_t other = ent_bytes + pmtab_bytes + (wtab ? 1024 : 0) + pend_bytes + (2 * 8 + 32) * max_stages + 256 + dm_slack;
   int64_t S = (static_cast<int64_t>(kSmemMax) - other) / p.stage_bytes;
   if (S > max_stages) S = max_stages;
   S -= S % p.ng;  // stage s always belongs to group s % ng
@@ -338,8 +339,9 @@ sc_status run_eval(const sc_context_s* ctx, const sc_batch* b, const float* w, f
   off += wtab ? 1024 : 0;
   p.pend_off = pend_bytes ? static_cast<int32_t>(round_up(off, 16)) : -1;
   if (pend_bytes) off = p.pend_off + pend_bytes;
-  p.bar_off = static_cast<int32_t>(round_up(off, 8));
-  off = p.bar_off + 2 * 8 * S + dm_slack;
+  p.bar_off = static_cast<int32_t>(round_up(off, 16));
+  p.hdr_off = static_cast<int32_t>(p.bar_off + 2 * 8 * S);  // unit headers, 32 B per stage (16-B aligned)
+  off = p.hdr_off + 32 * S + dm_slack;
   const size_t smem = static_cast<size_t>(off);
 
   p.split_copy = std::getenv("SC_SPLIT_COPY") ? 1 : 0;

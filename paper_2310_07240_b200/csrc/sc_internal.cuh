@@ -99,6 +99,7 @@ struct EvalParams {
   int32_t ld_flavor;        // gather kernel global-load cache flavour (see ldg_stream_f32)
   int32_t dm_full;          // dense-mapped rows (pat 2): groups 0..NV-2 fully inside the row's n columns
   int32_t pend_off;         // byte offset of the per-warp parked dense-gradient slabs (sc_device.cuh), or -1
+  int32_t hdr_off;          // byte offset of the per-stage unit headers (32 B: r0, nr, side-band windows), or -1
 };
 
 struct HistParams {

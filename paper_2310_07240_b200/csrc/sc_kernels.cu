@@ -567,6 +567,19 @@ __global__ void __launch_bounds__(kThreads, 1) eval_kernel(const EvalParams p) {
             const uint32_t cb = static_cast<uint32_t>(rem < p.chunk_bytes ? rem : p.chunk_bytes);
             bytes = cb * nr;
           }
+          if (kc == 0 && p.hdr_off >= 0) {
+            // the unit's header for the consumers (visible after their full-barrier wait: the
+            // arrive below releases it): r0, nr and the side-band windows, so a consumer warp
+            // reads 32 B instead of redoing the 64-bit unit and window arithmetic per stage
+            const SideBand wm = p.gt_mask ? sb_window(p.gt_mask, r0, nr, 1) : SideBand{0u, 0u};
+            const SideBand wa = p.app ? sb_window(p.app, r0, nr, 2) : SideBand{0u, 0u};
+            const uint32_t h = smem_addr(smem) + static_cast<uint32_t>(p.hdr_off) + 32u * static_cast<uint32_t>(s);
+            asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(h), "r"(static_cast<uint32_t>(r0)),
+                         "r"(static_cast<uint32_t>(r0 >> 32)) : "memory");
+            asm volatile("st.shared.u32 [%0], %1;" ::"r"(h + 8u), "r"(static_cast<uint32_t>(nr)) : "memory");
+            asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(h + 16u), "r"(wm.head), "r"(wm.nb), "r"(wa.head),
+                         "r"(wa.nb) : "memory");
+          }
           mbar_arrive_expect_tx(full + s, bytes + nb_m + nb_a);
           if (p.nchunks == 1 && !p.split_copy) {
             bulk_g2s(st, p.logits + r0 * p.ld_bytes, bytes, full + s, pol);
@@ -674,14 +687,24 @@ __global__ void __launch_bounds__(kThreads, 1) eval_kernel(const EvalParams p) {
     const UnitSched us(p);
     int lim = 32 - 2 * (cw % 16);  // first batch size of this warp (staggered), then 32
     for (int64_t i = grp; i < us.count; i += ng) {
-      const int64_t u = us.unit(i);
-      const int64_t r0 = u * p.R;
-      const int nr = static_cast<int>((p.rows - r0 < p.R ? p.rows - r0 : (int64_t)p.R));
       mbar_wait(full + st_idx, ph);
       const uint32_t st_off = static_cast<uint32_t>(st_idx) * p.stage_bytes;
-      // side-band windows: the aligned interior of rows [r0, r0 + nr) is in the stage
-      const SideBand wm = p.gt_mask ? sb_window(p.gt_mask, r0, nr, 1) : SideBand{0u, 0u};
-      const SideBand wa = p.app ? sb_window(p.app, r0, nr, 2) : SideBand{0u, 0u};
+      // the unit's header (written by the producer): r0, nr and the side-band windows (the
+      // aligned interior of rows [r0, r0 + nr) is in the stage)
+      int64_t r0;
+      int nr;
+      SideBand wm, wa;
+      {
+        const uint32_t h = sbase + static_cast<uint32_t>(p.hdr_off) + 32u * static_cast<uint32_t>(st_idx);
+        uint32_t lo, hi, n;
+        asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(lo), "=r"(hi) : "r"(h));
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(n) : "r"(h + 8u));
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(wm.head), "=r"(wm.nb), "=r"(wa.head), "=r"(wa.nb)
+                     : "r"(h + 16u));
+        r0 = static_cast<int64_t>((static_cast<uint64_t>(hi) << 32) | lo);
+        nr = static_cast<int>(n);
+      }
       const uint32_t m_base = sbase + st_off + p.mask_off - wm.head;
       const uint32_t a_base = sbase + st_off + p.app_off - wa.head;
       [[maybe_unused]] int nscan = 0;  // rows this warp scans in this stage (DEFER)
