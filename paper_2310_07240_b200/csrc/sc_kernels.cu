@@ -300,20 +300,18 @@ __device__ __forceinline__ void scan_slots(const SlotEnt<EPL>& se, const float (
   float fz = -CUDART_INF_F;
   uint32_t fk = kNone;
 #pragma unroll
-  for (int t = 0; t < EPL; ++t) {
-    if (t < se.ns) {  // warp-uniform
-      slot_fold(zs[t], se.key[t], fz, fk);
-      if ((se.lastm >> t) & 1u) {  // warp-uniform: list of slot t ends here
-        float z = fz;
-        uint32_t kk = fk;
-        warp_argmax(z, kk);
-        if (lane == slot) {
-          sz[t] = z;
-          sk[t] = kk;
-        }
-        fz = -CUDART_INF_F;
-        fk = kNone;
+  for (int t = 0; t < EPL; ++t) {  // slots >= ns hold padding keys only and end no list
+    slot_fold(zs[t], se.key[t], fz, fk);
+    if ((se.lastm >> t) & 1u) {  // warp-uniform: list of slot t ends here
+      float z = fz;
+      uint32_t kk = fk;
+      warp_argmax(z, kk);
+      if (lane == slot) {
+        sz[t] = z;
+        sk[t] = kk;
       }
+      fz = -CUDART_INF_F;
+      fk = kNone;
     }
   }
 }
@@ -685,7 +683,19 @@ __global__ void __launch_bounds__(kThreads, 1) eval_kernel(const EvalParams p) {
     int st_idx = grp;
     uint32_t ph = 0;
     const UnitSched us(p);
-    int lim = 32 - 2 * (cw % 16);  // first batch size of this warp (staggered), then 32
+    // A warp scans at most rpw rows per stage, and its batch epilogue runs only after it has
+    // released the stage (never inside the row loop): a batch ends at the first stage boundary
+    // where it holds >= lim rows, so lim <= 33 - rpw keeps it within 32 rows; the first batch
+    // sizes are staggered over the warps so they do not all hold the ring in the same stage.
+    // (The f32 split-maxima path, HBM-bound, keeps the in-loop epilogue of rounds 1-2 and
+    // 32-row batches: same-box A/B, the stage-boundary-only epilogue ran 1.2 % slower there
+    // while bf16 gained 6 % and Multi-Select 12 %, profiles/r4s_*, r4t_*.)
+    constexpr bool kEpiInLoop = !BF16 && PAT == 0;
+    const int rpw = p.R / wg;
+    const int lim_max = kEpiInLoop ? 32 : 33 - rpw;
+    int lim = 32 - 2 * (cw % 16);
+    if (lim > lim_max) lim = lim_max;
+    if (lim < 1) lim = 1;
     for (int64_t i = grp; i < us.count; i += ng) {
       mbar_wait(full + st_idx, ph);
       const uint32_t st_off = static_cast<uint32_t>(st_idx) * p.stage_bytes;
@@ -736,10 +746,6 @@ __global__ void __launch_bounds__(kThreads, 1) eval_kernel(const EvalParams p) {
             warp_argmax(zm, km);
             kp = dm_cat(p, kp);
             km = dm_cat(p, km);
-            if (b.n == lim) {
-              finish_batch<DEFER>(p, b, wtab, lane);
-              lim = 32;
-            }
             deposit(b, lane, zp, kp, zm, km, G, a, row);
           }
         } else if constexpr (PAT == 3) {
@@ -783,10 +789,6 @@ __global__ void __launch_bounds__(kThreads, 1) eval_kernel(const EvalParams p) {
           lo = __reduce_or_sync(kFull, lo);
           warp_argmax(zp, kp);
           warp_argmax(zm, km);
-          if (b.n == lim) {
-            finish_app_choice<DEFER>(p, b, wtab, lane);
-            lim = 32;
-          }
           deposit(b, lane, zp, kp, zm, km, G, a, row, lo);
         } else if constexpr (PAT == 0) {
           if (static_cast<int32_t>(a) != le.app) {
@@ -799,19 +801,17 @@ __global__ void __launch_bounds__(kThreads, 1) eval_kernel(const EvalParams p) {
           float zp, zm;
           uint32_t kp, km;
           scan_vals<EPL>(le, pm, zs, zp, kp, zm, km);
-          if (b.n == lim) {  // several rows per warp in this stage
-            finish_batch<DEFER>(p, b, wtab, lane);
-            lim = 32;
+          if constexpr (kEpiInLoop) {
+            if (b.n == lim) {  // several rows per warp in this stage
+              finish_batch<DEFER>(p, b, wtab, lane);
+              lim = 32;
+            }
           }
           deposit(b, lane, zp, kp, zm, km, G, a, row);
         } else {
           if (static_cast<int32_t>(a) != se.app) slot_ent_load(se, p.ctx, static_cast<int32_t>(a), lane, kElt);
 #pragma unroll
-          for (int t = 0; t < EPL; ++t) zs[t] = t < se.ns ? lds_z<BF16>(srow + (se.key[t] >> 8) * kElt) : 0.f;
-          if (b.n == lim) {  // the batch's slot maxima live in sz/sk: finish before the next scan
-            finish_slots<EPL>(p, b, sz, sk, wtab, lane);
-            lim = 32;
-          }
+          for (int t = 0; t < EPL; ++t) zs[t] = lds_z<BF16>(srow + (se.key[t] >> 8) * kElt);  // slots >= ns: key 0xFF, column 0
           scan_slots<EPL>(se, zs, sz, sk, b.n, lane);
           deposit(b, lane, 0.f, kNone, 0.f, kNone, G, a, row);
         }
@@ -823,11 +823,11 @@ __global__ void __launch_bounds__(kThreads, 1) eval_kernel(const EvalParams p) {
       if constexpr (DEFER) dense_drain(p, lane, nscan);
       // the batch epilogue runs after the stage is released, and the warps' batch boundaries
       // are staggered (lim) so they do not all hold the pipeline in the same stage
-      if (b.n == lim) {
+      if (kEpiInLoop ? b.n == lim : b.n >= lim) {
         if constexpr (PAT == 3) finish_app_choice<DEFER>(p, b, wtab, lane);
         else if constexpr (kSplit) finish_batch<DEFER>(p, b, wtab, lane);
         else finish_slots<EPL>(p, b, sz, sk, wtab, lane);
-        lim = 32;
+        lim = lim_max;
       }
       st_idx += ng;
       if (st_idx >= p.stages) { st_idx -= p.stages; ph ^= 1u; }
