@@ -394,7 +394,7 @@ __global__ void __launch_bounds__(kAAWarps * 32, 1) all_apps_lane_kernel(const A
 // and one compare-select — the arg max over 𝕎_a (a3; the strict '>' keeps the smaller label
 // on ties, A4), tracked by its shared address, from which the column and then its list
 // (catT) are recovered once per (row, application).  The next
-// unit's rows are loaded into registers (two rows per warp) while the current unit is
+// unit's rows are loaded into registers (one row per warp) while the current unit is
 // evaluated, then stored transposed; G per (row, application) comes from the row's ground
 // truth and the label-major category table (Eq. goal's correctness).
 template <bool BF16>
@@ -422,13 +422,14 @@ __global__ void __launch_bounds__(kTRWarps * 32, 1) all_apps_rows_kernel(const A
 
   const int64_t n_units = (p.rows + kTRRows - 1) / kTRRows;
   constexpr int kJ = BF16 ? kTRMaxC / 64 : kTRMaxC / 32;  // staged words per lane and row
-  uint32_t v[2][kJ];
-  // stage rows u*32 + 2w, 2w + 1 of unit u in registers (f32: column 32 j + lane; bf16: the
+  constexpr int kRW = kTRRows / kTRWarps;  // rows staged per warp
+  uint32_t v[kRW][kJ];
+  // stage row u*32 + w of unit u in registers (f32: column 32 j + lane; bf16: the
   // column pair 64 j + 2 lane, +1)
   auto stage = [&](int64_t u) {
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int64_t row = u * kTRRows + 2 * warp + h;
+    for (int h = 0; h < kRW; ++h) {
+      const int64_t row = u * kTRRows + kRW * warp + h;
       const uint8_t* src = p.logits + row * p.ld_bytes;
 #pragma unroll
       for (int j = 0; j < kJ; ++j) {
@@ -447,8 +448,8 @@ __global__ void __launch_bounds__(kTRWarps * 32, 1) all_apps_rows_kernel(const A
     const int nr = static_cast<int>(p.rows - row0 < kTRRows ? p.rows - row0 : kTRRows);
     // the staged rows, transposed
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int r = 2 * warp + h;
+    for (int h = 0; h < kRW; ++h) {
+      const int r = kRW * warp + h;
 #pragma unroll
       for (int j = 0; j < kJ; ++j) {
         if constexpr (BF16) {
@@ -461,12 +462,12 @@ __global__ void __launch_bounds__(kTRWarps * 32, 1) all_apps_rows_kernel(const A
         }
       }
     }
-    // G of every (row, application), a2: warp w builds rows 2w, 2w + 1; the row's ground-truth
+    // G of every (row, application), a2: warp w builds row w; the row's ground-truth
     // labels are warp-uniform loads, each lane ORs the lists of applications lane + 32 k
     // (independent, coalesced 32-B reads of the label-major category table)
 #pragma unroll 1
-    for (int h = 0; h < 2; ++h) {
-      const int r = 2 * warp + h;
+    for (int h = 0; h < kRW; ++h) {
+      const int r = kRW * warp + h;
       const int64_t g0 = r < nr ? __ldg(p.gt_off + row0 + r) : 0, g1 = r < nr ? __ldg(p.gt_off + row0 + r + 1) : 0;
       for (int a0 = 0; a0 < A; a0 += 256) {
         uint32_t G[8] = {0, 0, 0, 0, 0, 0, 0, 0};

@@ -154,8 +154,8 @@ struct AllAppsParams {
 };
 constexpr int kTRRows = 32;               // rows per unit of the lane-per-row kernel (one per lane)
 constexpr int kTRStride = kTRRows + 1;    // words between columns of the transposed unit
-constexpr int kTRWarps = 16;              // warps per CTA of the lane-per-row kernel
-constexpr int kTRMaxC = 1024;             // columns a unit's rows may have (two rows staged per warp in registers)
+constexpr int kTRWarps = 32;              // warps per CTA of the lane-per-row kernel (one staged row each)
+constexpr int kTRMaxC = 1024;             // columns a unit's rows may have (staged in registers)
 constexpr int kAllAppsRows = 4;  // rows per barrier interval of the warp-per-application kernel
 cudaError_t launch_all_apps_lane(const AllAppsParams& p, int grid, size_t smem, cudaStream_t st);
 cudaError_t launch_all_apps_rows(const AllAppsParams& p, int grid, size_t smem, cudaStream_t st);
