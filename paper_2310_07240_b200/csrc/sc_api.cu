@@ -718,7 +718,9 @@ static sc_status run_hist(sc_context ctx, const sc_batch* b, uint64_t* hist_gt, 
   const char* hk = std::getenv("SC_HIST");
   const bool rows_kernel = ctx->n_apps == 1 && ctx->C <= 128 * 1024 && !(hk && std::string(hk) == "warp");
   if (rows_kernel) {
-    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((b->rows + 255) / 256, static_cast<int64_t>(di.sms) * 8));
+    const char* gps = std::getenv("SC_HIST_CTAS_PER_SM");  // experiment knob (default 8)
+    const int64_t per_sm = gps ? std::max(1, std::atoi(gps)) : 8;
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((b->rows + 255) / 256, static_cast<int64_t>(di.sms) * per_sm));
     if (cudaError_t e = sc::launch_hist_rows(p, static_cast<int>(blocks), static_cast<cudaStream_t>(stream)))
       return cuda_fail(e, "hist kernel launch");
     g_launches.fetch_add(1, std::memory_order_relaxed);
