@@ -101,6 +101,19 @@ __device__ __forceinline__ float dsigmoid_f(float z) {
   return t / (d * d);
 }
 
+// σ(z) and σ'(z) from one exponential and one division: t = e^{-|z|}, r = 1/(1+t); σ = r
+// (z >= 0) or t·r, σ' = t·r² (sigmoid_f / dsigmoid_f's forms, one or two more roundings).
+// Used by the Multi-Select epilogue, which needs both at every list's maximum and at every
+// S argument: 0.749 -> 0.68-0.70 ms on cfg2.  (Used in every epilogue it made the others
+// slower on the same box — f32 0.592 -> 0.615 ms, bf16, the head — so they keep the separate
+// calls; profiles/r5e_*.)
+__device__ __forceinline__ void sig_dsig_f(float z, float& s, float& ds) {
+  const float t = expf(-fabsf(z));
+  const float r = 1.f / (1.f + t);
+  s = z >= 0.f ? r : t * r;
+  ds = t * r * r;
+}
+
 // Lexicographic max over (z, -label): keys are c << 8 | cat, ordered like c.
 __device__ __forceinline__ bool beats(float zo, uint32_t ko, float z, uint32_t k) {
   return zo > z || (zo == z && ko < k);
@@ -369,11 +382,13 @@ __device__ __forceinline__ void finish_lists_core(const EvalParams& p, RowBatch&
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           if (kj[j] != kNone) {
-            const float pj = sigmoid_f(zj[j]);
+            float pj, dpj, sx, dsx;
+            sig_dsig_f(zj[j], pj, dpj);
             const bool yj = (G >> j) & 1u;
             const float x = yj ? theta - pj : pj - theta;
-            ell += sigmoid_f(k * x);
-            const float g = wi * k * dsigmoid_f(k * x) * dsigmoid_f(zj[j]) * p.grad_scale;
+            sig_dsig_f(k * x, sx, dsx);
+            ell += sx;
+            const float g = wi * k * dsx * dpj * p.grad_scale;
             gi[j] = static_cast<int32_t>(kj[j] >> 8);
             gv[j] = yj ? -g : g;
           }
