@@ -51,3 +51,23 @@ def test_reference_arm_line():
     assert line["impl"] == "reference" and line["unit"] == "samples/s" and line["value"] > 0
     assert line["cpu_baseline"]["kind"] == "oracle" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["higher_is_better"] is True
+
+
+def test_touched_bytes_granules():
+    """The roofline's algorithmic bytes: 32-B sectors holding a mapped label,
+    and the same over 128-B lines (line_frac); checked against a direct count on a tiny context
+    and the ordering sector <= line <= whole row (+ the partial lines of an unaligned row)."""
+    import numpy as np
+    import bench
+    import synth
+    spec = synth.ContextSpec(64, [[[0, 9, 40], [63]]], 0.0, 10.0)  # one app: f32 columns 0, 9, 40, 63
+    # rows of 64 f32 = 256 B (sector / line aligned): sectors {0, 1, 5, 7}, lines {0, 1}
+    assert bench.touched_sector_bytes(spec, 64, 4) == 4 * 32
+    assert bench.touched_sector_bytes(spec, 64, 4, granule=128) == 2 * 128
+    for cfg in (2, 3, 4):
+        sp = synth.config_context(cfg)
+        ld = synth.default_ld(sp.C, "f32")
+        s = bench.touched_sector_bytes(sp, ld, 4, rows=1 << 20)
+        ln = bench.touched_sector_bytes(sp, ld, 4, rows=1 << 20, granule=128)
+        assert 0 < s <= ln <= ld * 4 + 128, (cfg, s, ln)
+    assert np.isclose(bench.touched_sector_bytes(synth.config_context(2), 1000, 4), 3168.0)
