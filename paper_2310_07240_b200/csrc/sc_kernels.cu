@@ -1199,7 +1199,9 @@ __global__ void __launch_bounds__(256) hist_rows_kernel(const HistParams p) {
   uint8_t* cat_s = hsm + 256 * 8;                                          // [C]
   __shared__ bool last_block;
   for (int i = threadIdx.x; i < 256; i += blockDim.x) sh_hist[i] = 0;
-  for (int c = threadIdx.x; c < p.ctx.C; c += blockDim.x) cat_s[c] = __ldg(p.ctx.cat + c);
+  // the table holds each label's list bits (label_lists), so a label costs one shared load and an OR
+  for (int c = threadIdx.x; c < p.ctx.C; c += blockDim.x)
+    cat_s[c] = static_cast<uint8_t>(label_lists(__ldg(p.ctx.cat + c), p.ctx.order));
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
@@ -1208,8 +1210,10 @@ __global__ void __launch_bounds__(256) hist_rows_kernel(const HistParams p) {
     const bool act = row < p.rows;
     uint32_t G = 0;
     if (act) {
-      const int64_t lo = __ldg(p.gt_off + row), hi = __ldg(p.gt_off + row + 1);
-      for (int64_t t = lo; t < hi; ++t) G |= label_lists(cat_s[__ldg(p.gt_lab + t)], p.ctx.order);
+      const int64_t lo = __ldg(p.gt_off + row);
+      const int n = static_cast<int>(__ldg(p.gt_off + row + 1) - lo);
+      const int32_t* lab = p.gt_lab + lo;
+      for (int t = 0; t < n; ++t) G |= cat_s[__ldg(lab + t)];
       if (p.gt_mask_out) p.gt_mask_out[row] = static_cast<uint8_t>(G);
     }
     const unsigned am = __ballot_sync(kFull, act);
