@@ -261,6 +261,10 @@ sc_status run_eval(const sc_context_s* ctx, const sc_batch* b, const float* w, f
     int64_t rpw = 1;
     while (rpw < 32 && 2 * rpw * p.ld_bytes <= 4096) rpw *= 2;
     p.ng = static_cast<int32_t>(std::min<int64_t>(4, rpw));
+    // the per-list slot path (Multi-Select): two groups of 8 warps on 8-row stages — a warp's
+    // long batch epilogue then holds back only its group's stages (same box: 0.680 -> 0.663 ms
+    // on cfg2, profiles/r5k_*; the split-maxima paths are best with one group)
+    if (launch_pat == 1 && p.ng == 1) p.ng = 2;
     if (const char* ng_env = std::getenv("SC_NG")) p.ng = std::atoi(ng_env);
     if (p.ng != 1 && p.ng != 2 && p.ng != 4 && p.ng != 8 && p.ng != 16) p.ng = 1;
     const int wg = W / p.ng;
